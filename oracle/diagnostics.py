@@ -1,0 +1,134 @@
+"""O5 — diagnostics of App. A.2.2.  fp64, dense where
+needed (small N only).  Test infrastructure (see oracle/__init__.py).
+
+Units: objectives are reported in physical units, c(x, y) = h^2 |k - l|^2
+and eps = eps' h^2 (reading R2).
+"""
+from __future__ import annotations
+
+from collections import deque
+
+import numpy as np
+
+from .partitions import composite_partition
+from .sinkhorn import lse, sqdist
+
+
+def marginal_errors(st):
+    """L1 marginal errors of the state (Table rows):
+    X: sum_x |P_X pi(x) - mu(x)| for the plans of the last sweep
+       (pre-balance; equals the sum of per-cell stopping errors);
+    Y: sum_y |sum_i nu_i(y) - nu(y)| of the stored basic-cell marginals."""
+    ex = float(np.abs(st.last["PX"] - st.mu).sum()) if "PX" in st.last else float("nan")
+    tot = np.zeros((st.N1, st.N2))
+    for r0, c0, d in st.boxes:
+        tot[r0:r0 + d.shape[0], c0:c0 + d.shape[1]] += d
+    ey = float(np.abs(tot - st.nu).sum())
+    return ex, ey
+
+
+def transport_cost(st):
+    """<c, pi> of the last sweep's plans: h^2 sum_i m_i Q_i (physical units)."""
+    return float(st.h * st.h * np.sum(st.m * st.last["Q"]))
+
+
+def dense_state_plan(st):
+    """Materialise the global plan pi = sum_J pi_J of the last sweep (needs
+    keep_plans=True; small N).  Returns (N1 N2) x (N1 N2) fp64."""
+    P = np.zeros((st.N1 * st.N2, st.N1 * st.N2))
+    for (R, C, ly, a, b, plan) in st.last["plans"].values():
+        xi = R * st.N2 + C
+        yi = ly[:, 0] * st.N2 + ly[:, 1]
+        P[np.ix_(xi, yi)] += plan
+    return P
+
+
+def primal_score(st, P=None):
+    """E(pi) = <c, pi> + eps KL(pi | mu (x) nu) (Eq. KL
+    PAPER.md:154-167 with phi(0) = 1) of the materialised plan."""
+    if P is None:
+        P = dense_state_plan(st)
+    N1, N2 = st.N1, st.N2
+    k = np.stack(np.meshgrid(np.arange(N1), np.arange(N2), indexing="ij"), -1).reshape(-1, 2)
+    c = sqdist(k, k) * st.h * st.h
+    ref = np.outer(st.mu.ravel(), st.nu.ravel())
+    pos = P > 0
+    if np.any(pos & (ref <= 0)):
+        return float("inf")
+    kl = float(np.sum(P[pos] * np.log(P[pos] / ref[pos])) - P.sum() + ref.sum())
+    return float(np.sum(c * P) + st.eps * kl)
+
+
+def dual_score(st, a: np.ndarray, b: np.ndarray):
+    """D(alpha, beta) = <alpha, mu> + <beta, nu> + eps <1 - exp((alpha + beta
+    - c)/eps), mu (x) nu>, with alpha = eps a,
+    beta = eps b given per pixel (b ignored where nu = 0).  Dense."""
+    N1, N2 = st.N1, st.N2
+    k = np.stack(np.meshgrid(np.arange(N1), np.arange(N2), indexing="ij"), -1).reshape(-1, 2)
+    Ce = sqdist(k, k) / st.eps_p
+    mu, nu = st.mu.ravel(), st.nu.ravel()
+    bb = np.where(nu > 0, b.ravel(), 0.0)
+    ex = np.exp(a.ravel()[:, None] + bb[None, :] - Ce)
+    val = np.sum(a.ravel() * mu) + np.sum(bb * nu) + np.sum(mu[:, None] * nu[None, :] * (1.0 - ex))
+    return float(st.eps * val)
+
+
+def stitch_alpha(st):
+    """Global X-potential alpha† from the cell potentials of the last A and B
+    sweeps, following the proof of Prop. convergence-hybrid
+    as the stitching of BoSch2020 §6.3 (not reproduced in the paper,
+    PAPER.md:1413; reading R15): BFS spanning tree of the partition graph from
+    A-cell 0; across an edge (J, J') sharing basic cell i the offset changes by
+    the mu-weighted mean of (a_J' - a_J) over X_i; alpha† = a_J - s_J on
+    A-cells.  Returns a† per pixel (nat units)."""
+    n1, n2, s = st.n1, st.n2, st.s
+    A = composite_partition(n1, n2, "A")
+    B = composite_partition(n1, n2, "B")
+    fa, fb = st.alpha["A"], st.alpha["B"]
+    cells = {("A", k): J for k, J in enumerate(A)}
+    cells.update({("B", k): J for k, J in enumerate(B)})
+    pot = {"A": fa, "B": fb}
+    owner = {}
+    for key, J in cells.items():
+        for i in J:
+            owner.setdefault(i, []).append(key)
+    off = {("A", 0): 0.0}
+    dq = deque([("A", 0)])
+    while dq:
+        u = dq.popleft()
+        for i in cells[u]:
+            for v in owner[i]:
+                if v in off:
+                    continue
+                i1, i2 = divmod(i, n2)
+                sl = (slice(i1 * s, (i1 + 1) * s), slice(i2 * s, (i2 + 1) * s))
+                wgt = st.mu[sl]
+                diff = pot[v[0]][sl] - pot[u[0]][sl]
+                off[v] = off[u] + float(np.sum(wgt * diff) / np.sum(wgt))
+                dq.append(v)
+    a = np.zeros((st.N1, st.N2))
+    for k, J in enumerate(A):
+        for i in J:
+            i1, i2 = divmod(i, n2)
+            sl = (slice(i1 * s, (i1 + 1) * s), slice(i2 * s, (i2 + 1) * s))
+            a[sl] = fa[sl] - off[("A", k)]
+    return a
+
+
+def y_response(st, a: np.ndarray):
+    """Exact global Y-update b(y) = -log sum_x exp(a(x) - c/eps) mu(x)."""
+    N1, N2 = st.N1, st.N2
+    k = np.stack(np.meshgrid(np.arange(N1), np.arange(N2), indexing="ij"), -1).reshape(-1, 2)
+    Ce = sqdist(k, k) / st.eps_p
+    return (-lse(a.ravel()[:, None] + np.log(st.mu.ravel())[:, None] - Ce, axis=0)).reshape(N1, N2)
+
+
+def pd_gap(st, P=None):
+    """Relative primal-dual gap (E(pi) - D(alpha†, beta†)) / D
+    with alpha† from stitch_alpha and beta† its exact Y-response.
+    Returns (E, D, rel_gap)."""
+    E = primal_score(st, P)
+    a = stitch_alpha(st)
+    b = y_response(st, a)
+    D = dual_score(st, a, b)
+    return E, D, (E - D) / D

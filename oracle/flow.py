@@ -1,0 +1,224 @@
+"""O3 — the flow update (§3.2, Def. flow-update) with the
+product gluing candidate pi_hat_ij = mu_j/m_j (x) nu_i/m_i (Remark eps-gamma,
+PAPER.md:550-552; reading R12) on the 5-point neighbourhood.
+Test infrastructure (see oracle/__init__.py).
+
+Steps follow §5.1:
+  1. edge costs c_bar_ij = <c, pi_hat_ij - pi_hat_ii> (Eq. edge-cost
+     PAPER.md:419-421) by direct double sums;
+  2. min-cost flow (Eq. MinCostFlow PAPER.md:378-381 with the divergence
+     constraint PAPER.md:350-354) — exact LP on integer data (reading R11);
+  3. new basic-cell Y-marginals nu_hat_j = sum_i w_ij nu_i/m_i
+     (Lemma, Eq. flow-update-cell-marginals PAPER.md:453-456).
+Arc order per source cell: 0 self, 1 up, 2 down, 3 left, 4 right.
+"""
+from __future__ import annotations
+
+import itertools
+
+import numpy as np
+import scipy.sparse as sp
+from scipy.optimize import linprog
+
+from .domdec import truncate_box
+
+ARC_D = ((0, 0), (-1, 0), (1, 0), (0, -1), (0, 1))
+COST_SCALE = 1024.0  # C_ij = round_half_even(c_bar_ij [px^2] * 2^10), reading R11
+
+
+def neighbour(i: int, a: int, n1: int, n2: int) -> int:
+    """Index of the a-th neighbour of basic cell i, or -1 outside the grid."""
+    i1, i2 = divmod(i, n2)
+    j1, j2 = i1 + ARC_D[a][0], i2 + ARC_D[a][1]
+    if 0 <= j1 < n1 and 0 <= j2 < n2:
+        return j1 * n2 + j2
+    return -1
+
+
+def edge_costs(st, Q=None):
+    """c_bar (I x 5, px^2 units, NaN for arcs leaving the grid), c_bar_ii = 0.
+    For i != j, with the product candidate:
+        c_bar_ij = (1/m_i) sum_{x in X_j} sum_y |x - y|^2 (mu(x)/m_j) nu_i(y) - Q_i
+    where Q_i = <c, pi_i>/m_i is the plan cost of basic cell i from the last
+    sweep (pi_hat_ii = pi_i/m_i; reading R13).  Direct double
+    sums over pixels (no moment shortcut)."""
+    if Q is None:
+        Q = st.last["Q"]
+    n1, n2, s = st.n1, st.n2, st.s
+    I = n1 * n2
+    cbar = np.full((I, 5), np.nan)
+    for i in range(I):
+        r0, c0, d = st.boxes[i]
+        yr, yc = np.nonzero(d > 0)
+        vals = d[yr, yc]
+        Y1 = (yr + r0).astype(np.float64)
+        Y2 = (yc + c0).astype(np.float64)
+        cbar[i, 0] = 0.0
+        for a in range(1, 5):
+            j = neighbour(i, a, n1, n2)
+            if j < 0:
+                continue
+            j1, j2 = divmod(j, n2)
+            xr, xc = np.meshgrid(np.arange(j1 * s, (j1 + 1) * s), np.arange(j2 * s, (j2 + 1) * s),
+                                 indexing="ij")
+            xr, xc = xr.ravel().astype(np.float64), xc.ravel().astype(np.float64)
+            mux = st.mu[xr.astype(int), xc.astype(int)]
+            d2 = (xr[:, None] - Y1[None, :]) ** 2 + (xc[:, None] - Y2[None, :]) ** 2
+            tot = float(np.sum(d2 * mux[:, None] * vals[None, :]))
+            cbar[i, a] = tot / (st.m[i] * st.m[j]) - Q[i]
+    return cbar
+
+
+def integer_instance(cbar: np.ndarray, q: np.ndarray):
+    """Integer data of the min-cost flow (reading R11): C_ij =
+    round_half_even(c_bar_ij * 2^10) (0 on self / invalid arcs), q_i exact."""
+    C = np.where(np.isnan(cbar), 0.0, np.rint(cbar * COST_SCALE)).astype(np.int64)
+    C[:, 0] = 0
+    return C, q.astype(np.int64)
+
+
+def flow_objective(w: np.ndarray, C: np.ndarray) -> int:
+    """sum_ij w_ij C_ij in exact (Python) integers."""
+    return int(sum(int(a) * int(b) for a, b in zip(w.ravel().tolist(), C.ravel().tolist())))
+
+
+def check_flow(w: np.ndarray, q: np.ndarray, n1: int, n2: int) -> bool:
+    """Both divergence constraints of Eq. div-constraint,
+    exactly, and w >= 0, and no mass on arcs leaving the grid."""
+    I = n1 * n2
+    if np.any(w < 0):
+        return False
+    out = w.sum(axis=1)
+    inn = np.zeros(I, dtype=np.int64)
+    for i in range(I):
+        for a in range(5):
+            j = neighbour(i, a, n1, n2)
+            if j < 0:
+                if w[i, a] != 0:
+                    return False
+                continue
+            inn[j] += w[i, a]
+    return bool(np.array_equal(out, q) and np.array_equal(inn, q))
+
+
+def min_cost_flow(q: np.ndarray, C: np.ndarray, n1: int, n2: int):
+    """Exact optimum of Eq. MinCostFlow on integer data:
+    transportation LP (sources i, sinks j, arcs (i, j) in N) solved by a
+    library simplex (HiGHS dual simplex — a library primitive; the paper uses
+    OR-tools).  The constraint matrix is totally unimodular, so
+    the vertex solution is integral; it is rounded and verified exactly.
+    Returns (w (I x 5 int64), objective (exact int))."""
+    I = n1 * n2
+    var_i, var_a, var_j = [], [], []
+    for i in range(I):
+        for a in range(5):
+            j = neighbour(i, a, n1, n2)
+            if j >= 0:
+                var_i.append(i)
+                var_a.append(a)
+                var_j.append(j)
+    nv = len(var_i)
+    cost = np.array([C[i, a] for i, a in zip(var_i, var_a)], dtype=np.float64)
+    rows = np.concatenate([np.array(var_i), I + np.array(var_j)])
+    cols = np.concatenate([np.arange(nv), np.arange(nv)])
+    A = sp.csr_matrix((np.ones(2 * nv), (rows, cols)), shape=(2 * I, nv))
+    b = np.concatenate([q, q]).astype(np.float64)
+    res = linprog(cost, A_eq=A, b_eq=b, bounds=(0, None), method="highs-ds")
+    if res.status != 0:
+        raise RuntimeError(f"min-cost flow LP failed: {res.message}")
+    x = np.rint(res.x).astype(np.int64)
+    w = np.zeros((I, 5), dtype=np.int64)
+    for k in range(nv):
+        w[var_i[k], var_a[k]] = x[k]
+    if not check_flow(w, q, n1, n2):
+        raise RuntimeError("rounded LP solution is not an exact flow")
+    return w, flow_objective(w, C)
+
+
+def mcf_bruteforce(q: np.ndarray, C: np.ndarray, n1: int, n2: int):
+    """Exhaustive enumeration of all integer flows (tiny instances, <= 6
+    nodes, small q).  The LP is totally unimodular, so the integer optimum is
+    the LP optimum.  Returns the optimal objective."""
+    I = n1 * n2
+    arcs = [[(a, neighbour(i, a, n1, n2)) for a in range(5) if neighbour(i, a, n1, n2) >= 0]
+            for i in range(I)]
+
+    def compositions(total, k):
+        if k == 1:
+            yield (total,)
+            return
+        for first in range(total + 1):
+            for rest in compositions(total - first, k - 1):
+                yield (first,) + rest
+
+    options = [list(compositions(int(q[i]), len(arcs[i]))) for i in range(I)]
+    best = None
+    for choice in itertools.product(*options):
+        inn = [0] * I
+        obj = 0
+        for i in range(I):
+            for (a, j), v in zip(arcs[i], choice[i]):
+                inn[j] += v
+                obj += v * int(C[i, a])
+        if inn == [int(x) for x in q]:
+            if best is None or obj < best:
+                best = obj
+    return best
+
+
+def apply_flow(st, w: np.ndarray, q: np.ndarray, tau: float = 1e-15):
+    """nu_hat_j = sum_{i in N(j)} w_ij nu_i / m_i (Eq. flow-update-cell-
+    marginals), realised as (w_ij / q_i) nu_i with the
+    exact supplies q_i = m_i 2^E (reading R11).  Only cells with inflow from a
+    neighbour (w_jj < q_j) change; their new box is the hull of the
+    contributing boxes, followed by truncate + minimal box.
+    Summation order: self, from up, from down, from left, from right.
+    Returns the number of rewritten cells."""
+    n1, n2 = st.n1, st.n2
+    I = n1 * n2
+    # source arc a' such that neighbour(i, a') = j, for i = neighbour(j, a)
+    rev = {1: 2, 2: 1, 3: 4, 4: 3}
+    new_boxes = list(st.boxes)
+    changed = 0
+    for j in range(I):
+        if w[j, 0] == q[j]:
+            continue
+        changed += 1
+        contrib = [(j, float(w[j, 0]) / float(q[j]))] if w[j, 0] > 0 else []
+        for a in (1, 2, 3, 4):
+            i = neighbour(j, a, n1, n2)
+            if i < 0:
+                continue
+            wij = w[i, rev[a]]
+            if wij > 0:
+                contrib.append((i, float(wij) / float(q[i])))
+        L1 = min(st.boxes[i][0] for i, _ in contrib)
+        L2 = min(st.boxes[i][1] for i, _ in contrib)
+        U1 = max(st.boxes[i][0] + st.boxes[i][2].shape[0] for i, _ in contrib)
+        U2 = max(st.boxes[i][1] + st.boxes[i][2].shape[1] for i, _ in contrib)
+        acc = np.zeros((U1 - L1, U2 - L2))
+        for i, f in contrib:
+            r0, c0, d = st.boxes[i]
+            acc[r0 - L1:r0 - L1 + d.shape[0], c0 - L2:c0 - L2 + d.shape[1]] += f * d
+        r0, c0, d, dr = truncate_box(L1, L2, acc, tau)
+        st.dropped += dr
+        new_boxes[j] = [r0, c0, d]
+    st.boxes = new_boxes
+    return changed
+
+
+def flow_update(st, q: np.ndarray, tau: float = 1e-15):
+    """FlowUpdate(pi) of Alg. 3: edge costs, exact min-cost
+    flow, accept iff the optimal objective is strictly negative (the
+    stationary flow has objective 0), then apply.
+    Returns dict(stationary, objective, changed, w, C, cbar)."""
+    cbar = edge_costs(st)
+    C, q = integer_instance(cbar, q)
+    w, obj = min_cost_flow(q, C, st.n1, st.n2)
+    out = {"objective": obj, "w": w, "C": C, "cbar": cbar, "changed": 0}
+    if obj < 0:
+        out["changed"] = apply_flow(st, w, q, tau)
+        out["stationary"] = False
+    else:
+        out["stationary"] = True
+    return out
