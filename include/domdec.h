@@ -1,0 +1,222 @@
+/*
+ * domdec.h — C-ABI of the B200 (sm_100a) hot path of arXiv 2405.09400,
+ * "Flow updates for domain decomposition of entropic optimal transport".
+ *
+ * The library (libdomdec.so) runs single-scale entropic domain decomposition
+ * on N1 x N2 pixel grids with squared-Euclidean cost:
+ *   domdec_sweep  = DomDecIter on partition A or B (Alg. 1, PAPER.md:261-285,
+ *                   realised as Alg. 4): BasicToComposite,
+ *                   batched log-domain separable Sinkhorn, CompositeToBasic,
+ *                   Balance, Truncate — one fused CUDA kernel;
+ *   flow_update   = the flow update (Def. flow-update, steps
+ *                   of §5.1) with product gluing candidates
+ *                   (PAPER.md:552): edge costs, exact min-cost flow on the GPU,
+ *                   apply flow — CUDA kernels;
+ *   marginal_error / primal_dual_gap = diagnostics of App. A.2.2
+ *                   (PAPER.md:1357-1359, 1395-1419).
+ * The state is dual potentials plus basic-cell Y-marginals in bounding-box
+ * form.  See DESIGN.md for the readings (R#) of the
+ * points where the paper is silent.
+ *
+ * Conventions
+ *  - Pixel (r, c) has physical centre (-1 + (r+1/2) h, -1 + (c+1/2) h);
+ *    cost c(x, y) = |x - y|^2 (physical), i.e. h^2 |k - l|^2 in pixels.
+ *  - Basic cell i = i1 * n2 + i2 covers rows [i1 s, i1 s + s) and columns
+ *    [i2 s, i2 s + s); n1 = N1/s, n2 = N2/s, I = n1 n2.
+ *  - Arc order of the 5-point neighbourhood: 0 self, 1 up
+ *    (i1-1), 2 down (i1+1), 3 left (i2-1), 4 right (i2+1).  Per-arc arrays
+ *    are [I][5] row-major, indexed by the SOURCE cell.
+ *  - Boxes: off = (row, col) of the lower corner, ext = (rows, cols); the
+ *    data of a box is row-major with row stride ext[1].
+ *  - All work is ordered on the ctx's CUDA stream.  Calls that return host
+ *    values synchronise that stream; domdec_sweep / flow_update with a NULL
+ *    stats pointer are fully asynchronous (no host round trip).  Errors raised
+ *    inside asynchronous kernels are sticky and are reported by the next
+ *    synchronising call.  A ctx is not thread-safe.
+ *  - Every function returns dd_status and never aborts; dd_last_error()
+ *    gives a message.  The library owns all device memory it allocates.
+ *  - There is no CPU fallback: without a usable CUDA device domdec_init
+ *    returns DD_ERR_CUDA.
+ */
+#ifndef DOMDEC_H
+#define DOMDEC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dd_ctx dd_ctx;
+
+typedef enum {
+  DD_OK = 0,
+  DD_ERR_ARG = 1,      /* bad argument (NULL, eps <= 0, s not dividing N, ...) */
+  DD_ERR_PRECOND = 2,  /* violated precondition of the method (zero-mass basic
+                          cell PAPER.md:233, initial boxes not reproducing nu,
+                          ||nu_i|| != m_i, ...)                                 */
+  DD_ERR_NUMERIC = 3,  /* box capacity exceeded, NaN/Inf, min-cost flow failure */
+  DD_ERR_CUDA = 4,     /* CUDA runtime error / no device                        */
+  DD_ERR_OOM = 6       /* device allocation failed                              */
+} dd_status;
+
+typedef enum { DD_PART_A = 0, DD_PART_B = 1 } dd_partition;
+
+/* Problem data, host memory, copied by domdec_init (caller keeps ownership). */
+typedef struct {
+  int32_t N1, N2;          /* pixels per axis                                   */
+  double h;                /* grid spacing (2/N on [-1,1]^2)      */
+  double eps;              /* entropic regularisation in physical units (> 0)   */
+  int32_t cell_size;       /* s, basic cells are s x s pixels; must divide N1,N2*/
+  const double *mu;        /* [N1*N2] >= 0, row-major; every basic cell > 0     */
+  const double *nu;        /* [N1*N2] >= 0, sum nu = sum mu                     */
+  /* initial coupling as basic-cell Y-marginals nu_i^0 in bounding-box form    */
+  const int32_t *init_off; /* [I][2]                                            */
+  const int32_t *init_ext; /* [I][2]                                            */
+  const int64_t *init_pos; /* [I] start of box i in init_data                   */
+  const double *init_data; /* concatenated row-major boxes, values >= 0         */
+  int32_t mass_exponent;   /* E: min-cost-flow supplies q_i = rint(m_i 2^E)     */
+                           /* (exact for the dyadic synthetic inputs)           */
+} dd_problem;
+
+typedef struct {
+  double err;          /* Sinkhorn stopping tolerance Err; 1e-4 */
+  int32_t max_iter;    /* per-cell iteration cap per sweep (paper silent); 2000 */
+  int32_t fixed_iter;  /* > 0: parity mode, exactly this many passes per cell   */
+  double trunc;        /* truncation threshold tau; 1e-15       */
+  int32_t slot_cap;    /* capacity (elements) of one basic-cell box slot;      */
+                       /* 0 = automatic from eps                                */
+  int32_t comp_cap;    /* composite box side of the fast size class of the     */
+                       /* sweep kernel (larger hulls go to a second, large-    */
+                       /* shared-memory class on the device); 0 = automatic    */
+  int32_t device;      /* CUDA device ordinal                                   */
+  void *stream;        /* cudaStream_t to order all work on (NULL = the legacy */
+                       /* default stream)                                       */
+} dd_options;
+
+/* Filled by domdec_sweep when a non-NULL pointer is passed (synchronises). */
+typedef struct {
+  int64_t cells;          /* composite cells solved                            */
+  int64_t nonconverged;   /* cells that hit max_iter (counted, not an error)   */
+  int64_t iters_total;    /* sum of Sinkhorn passes                            */
+  int32_t iters_max;
+  int32_t overflow;       /* cells left unchanged because a box exceeded caps  */
+  double l1x_entry;       /* sum_J e_J after the first pass (reading R14)      */
+  double l1x_final;       /* sum_J e_J of the returned plans = L1 X-error      */
+  double dropped_mass;    /* mass removed by truncation in this sweep          */
+  double mufu_ops;        /* algorithmic ex2 + lg2 count of this sweep         */
+  double bytes;           /* algorithmic HBM bytes of this sweep               */
+} dd_sweep_stats;
+
+/* Filled by flow_update when a non-NULL pointer is passed (synchronises). */
+typedef struct {
+  int32_t stationary;     /* 1: the stationary flow is optimal, nothing moved */
+  int32_t certificate;    /* 1: stationarity proven by the negative-cycle test */
+  int32_t refines;        /* cost-scaling refine phases run by the solver      */
+  int32_t rounds;         /* push/relabel rounds run by the solver             */
+  int64_t objective;      /* optimal sum_ij w_ij C_ij (integer costs, R11)     */
+  int64_t changed_cells;  /* basic cells whose marginal was rewritten          */
+} dd_flow_stats;
+
+/* Create a context: validate (DD_ERR_ARG / DD_ERR_PRECOND), copy the problem to
+ * the device, build the A and B composite partitions (2x2 groups, B staggered
+ * by one basic cell with ragged border groups, reading R4).  *out receives the
+ * context; on error *out is NULL. */
+dd_status domdec_init(const dd_problem *problem, const dd_options *options, dd_ctx **out);
+
+/* One DomDecIter on partition A or B (Alg. 1 / Alg. 4).  Warm start: the X
+ * potential of the previous sweep on the same partition (zero on the first,
+ * reading R7).  stats may be NULL (asynchronous). */
+dd_status domdec_sweep(dd_ctx *ctx, dd_partition part, dd_sweep_stats *stats);
+
+/* One flow update (Def. flow-update) using the plan costs of
+ * the most recent sweep: edge costs (product candidates), integer instance
+ * (C_ij = rint(c_bar_ij[px^2] * 1024), q_i = rint(m_i 2^E)), negative-cycle
+ * certificate, exact min-cost flow (GPU cost scaling) if needed, apply flow
+ * iff the optimal objective is < 0.  Requires a previous sweep
+ * (DD_ERR_PRECOND otherwise).  stats may be NULL (asynchronous). */
+dd_status flow_update(dd_ctx *ctx, dd_flow_stats *stats);
+
+/* L1 marginal errors (Table rows), fp64:
+ * l1_x = sum_x |P_X pi(x) - mu(x)| of the last sweep's plans,
+ * l1_y = sum_y |sum_i nu_i(y) - nu(y)| of the stored basic-cell marginals.
+ * Synchronises. */
+dd_status marginal_error(dd_ctx *ctx, double *l1_x, double *l1_y);
+
+/* Primal score E(pi) = <c,pi> + eps KL(pi|mu (x) nu) of the last sweep's plans,
+ * dual score D(alpha†, beta†) of the stitched potentials (reading R15) and the
+ * relative gap (E - D)/D; transport_cost = <c, pi>.
+ * Needs at least one A and one B sweep.  Any output pointer may be NULL.
+ * Synchronises. */
+dd_status primal_dual_gap(dd_ctx *ctx, double *primal, double *dual, double *rel_gap,
+                          double *transport_cost);
+
+/* Copy the basic-cell marginals to host buffers (boxes concatenated in cell
+ * order).  Pass data == NULL to query the required length in *data_len.
+ * off/ext are [I][2], pos is [I].  Synchronises. */
+dd_status domdec_export_cells(dd_ctx *ctx, int32_t *off, int32_t *ext, int64_t *pos,
+                              double *data, int64_t data_cap, int64_t *data_len);
+
+/* Copy the X potential a = alpha/eps (dimensionless, global pixel gauge) of the
+ * last sweep on a partition to host [N1*N2]; each composite cell is shifted so
+ * that its mu-weighted mean is 0 (potentials are unique only up to constants,
+ * PAPER.md:216).  DD_ERR_PRECOND if the partition was never swept. */
+dd_status domdec_export_alpha(dd_ctx *ctx, dd_partition part, double *alpha);
+
+/* Per basic cell plan cost of the last sweep, Q_i m_i = <c, pi_i> in pixel^2
+ * units (reading R13), host [I].  Synchronises. */
+dd_status domdec_export_plan_cost(dd_ctx *ctx, double *Qm);
+
+/* Step 1 of the flow update alone: edge costs of the current state.
+ * cbar [I][5] fp64 pixel^2 units (NaN on arcs leaving the grid, 0 on self),
+ * C [I][5] int64 integer costs, q [I] supplies.  Any pointer may be NULL. */
+dd_status flow_edge_costs(dd_ctx *ctx, double *cbar, int64_t *C, int64_t *q);
+
+/* Step 3 of the flow update alone: apply a host flow w [I][5] (int64, must
+ * satisfy both divergence constraints with the ctx supplies q, else
+ * DD_ERR_PRECOND): nu_hat_j = sum_i (w_ij / q_i) nu_i,
+ * then truncate + minimal box. */
+dd_status flow_apply(dd_ctx *ctx, const int64_t *w);
+
+/* Standalone exact min-cost flow on the n1 x n2 grid graph (Eq. MinCostFlow
+ * PAPER.md:378-381 with the divergence constraints PAPER.md:350-354) on the
+ * GPU: q [I] > 0 supplies, C [I][5] integer arc costs (column 0 ignored, arcs
+ * leaving the grid ignored), |C| < 2^40.  Writes an optimal flow w [I][5] and
+ * the optimal objective.  Host buffers; stream may be NULL.  stats may be NULL. */
+dd_status dd_mincost_flow(int32_t n1, int32_t n2, const int64_t *q, const int64_t *C,
+                          int64_t *w, int64_t *objective, dd_flow_stats *stats,
+                          int32_t device, void *stream);
+
+/* Cumulative work counters since domdec_init / domdec_reset_counters (for
+ * roofline accounting without per-call synchronisation).  Synchronises. */
+typedef struct {
+  int64_t sweeps;         /* domdec_sweep calls                                */
+  int64_t flow_updates;   /* flow_update calls                                 */
+  int64_t cells;          /* composite-cell solves                             */
+  int64_t iters;          /* Sinkhorn passes                                   */
+  double mufu_ops;        /* algorithmic ex2 + lg2 of the sweeps   */
+  double bytes;           /* algorithmic HBM bytes of the sweeps               */
+} dd_counters;
+dd_status domdec_counters(dd_ctx *ctx, dd_counters *out);
+dd_status domdec_reset_counters(dd_ctx *ctx);
+
+/* Measured ex2.approx.f32 throughput of the device (ops/s): a grid-wide
+ * kernel of independent MUFU chains — the denominator of the sweep roofline
+ * (DESIGN.md "Roofline"). */
+dd_status dd_mufu_peak(int32_t device, double *ops_per_s);
+
+/* Release all device memory of ctx.  NULL is a no-op. */
+dd_status domdec_destroy(dd_ctx *ctx);
+
+/* Message of the last error on ctx (or of the last failed domdec_init /
+ * dd_mincost_flow when ctx is NULL).  Never NULL. */
+const char *dd_last_error(const dd_ctx *ctx);
+
+/* Library build string (arch, version). */
+const char *dd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DOMDEC_H */

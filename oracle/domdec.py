@@ -67,11 +67,18 @@ def basic_to_composite(boxes, members):
 
 
 def balance(parts, targets):
-    """Balance (Alg. 4 line 6; procedure = reading R8,
-    proportional pooling).  parts: list of arrays (same shape) nu_i, i in J;
-    targets t_i with sum t_i = sum ||nu_i||.  Donors (delta > 0) scale down,
-    the pooled mass P is shared among receivers in proportion to their deficit.
-    Preserves sum_i nu_i pointwise and gives ||nu_i|| = t_i."""
+    """Balance (Alg. 4 line 6; the procedure is deferred to
+    BoSch2020 §6, PAPER.md:1205 — reading R8, overlap-weighted transfer).
+    parts: list of arrays (same shape) nu_k, k in J; targets t_k with
+    sum t_k = sum ||nu_k||.  With delta_k = ||nu_k|| - t_k, donors (delta > 0)
+    send f_dr = delta_d (-delta_r) / Delta to receivers (Delta = sum of donor
+    deltas), distributed over the pixels where both are present:
+        transfer_dr(y) = f_dr / T_dr * nu_d(y) nu_r(y) / nu_J(y),
+        T_dr = sum_y nu_d(y) nu_r(y) / nu_J(y),  nu_J = sum_k nu_k.
+    Preserves sum_k nu_k pointwise, gives ||nu_k|| = t_k and keeps nu_k >= 0
+    when sum_r f_dr / T_dr <= 1 for every donor; otherwise (tiny overlaps) the
+    donors are scaled down and the pooled mass is shared in proportion to the
+    receivers' deficits (both rules exact)."""
     mass = np.array([p.sum() for p in parts])
     delta = mass - np.asarray(targets)
     donors = np.flatnonzero(delta > 0)
@@ -79,17 +86,40 @@ def balance(parts, targets):
     if len(donors) == 0 or len(recv) == 0:
         return [p.copy() for p in parts]
     D = float(delta[donors].sum())
+    nuJ = np.zeros_like(parts[0])
+    for p in parts:
+        nuJ = nuJ + p
+    safe = np.where(nuJ > 0, nuJ, 1.0)
+    T = {}
+    ok = True
+    for d in donors:
+        load = 0.0
+        for r in recv:
+            T[d, r] = float(np.sum(parts[d] * parts[r] / safe))
+            f = delta[d] * (-delta[r]) / D
+            if T[d, r] <= 0:
+                ok = False
+            else:
+                load += f / T[d, r]
+        if load > 1.0:
+            ok = False
+    out = [p.copy() for p in parts]
+    if ok:
+        for d in donors:
+            for r in recv:
+                f = delta[d] * (-delta[r]) / D
+                tr = (f / T[d, r]) * parts[d] * parts[r] / safe
+                out[d] = out[d] - tr
+                out[r] = out[r] + tr
+        return out
     P = np.zeros_like(parts[0])
     for d in donors:
         P += (delta[d] / mass[d]) * parts[d]
-    out = []
-    for k, p in enumerate(parts):
+    for k in range(len(parts)):
         if delta[k] > 0:
-            out.append(p * (1.0 - delta[k] / mass[k]))
+            out[k] = parts[k] * (1.0 - delta[k] / mass[k])
         elif delta[k] < 0:
-            out.append(p + (-delta[k] / D) * P)
-        else:
-            out.append(p.copy())
+            out[k] = parts[k] + (-delta[k] / D) * P
     return out
 
 
@@ -139,7 +169,8 @@ def domdec_sweep(st: OracleState, kind: str, err: float = 1e-4, fixed_iter: int 
       6. Truncate + minimal box (PAPER.md:1233, 1265);
       7. store a.
     By-products kept in st.last: per basic cell Q_i = <c, pi_i>/m_i in px^2
-    (reading R13), plan X-marginal per pixel, per-cell (iters, e0, e).
+    and the pre-balance cell marginal nu_i^pre = P_Y pi_i (reading R13), plan
+    X-marginal per pixel, per-cell (iters, e0, e).
 
     cells: optional list of composite-cell indices to process (sampled parity
     at full size); then the state is NOT advanced and the per-cell results are
@@ -154,6 +185,7 @@ def domdec_sweep(st: OracleState, kind: str, err: float = 1e-4, fixed_iter: int 
     alpha_old = st.alpha[kind]
     alpha_new = np.zeros((st.N1, st.N2)) if alpha_old is None else alpha_old.copy()
     Q = np.zeros(st.n1 * st.n2)
+    nu_pre = [None] * (st.n1 * st.n2)
     PX = np.zeros((st.N1, st.N2))
     stats = {"iters": [], "e0": [], "e": [], "dropped": 0.0, "mass_X": []}
     plans = {}
@@ -178,6 +210,7 @@ def domdec_sweep(st: OracleState, kind: str, err: float = 1e-4, fixed_iter: int 
             part = np.zeros_like(nuJ)
             part[yr, yc] = plan[sel].sum(axis=0)
             parts.append(part)
+            nu_pre[i] = (L1, L2, part.copy())
             d2 = (kx[sel, 0:1] - ly[None, :, 0]) ** 2 + (kx[sel, 1:2] - ly[None, :, 1]) ** 2
             Q[i] = float(np.sum(d2 * plan[sel])) / st.m[i]
         PX[R, Cc] = plan.sum(axis=1)
@@ -205,7 +238,7 @@ def domdec_sweep(st: OracleState, kind: str, err: float = 1e-4, fixed_iter: int 
     st.boxes = new_boxes
     st.alpha[kind] = alpha_new
     st.dropped += stats["dropped"]
-    st.last = {"kind": kind, "Q": Q, "PX": PX, "plans": plans if keep_plans else None}
+    st.last = {"kind": kind, "Q": Q, "PX": PX, "nu_pre": nu_pre, "plans": plans if keep_plans else None}
     stats["e0_sum"] = float(np.sum(stats["e0"]))
     stats["e_sum"] = float(np.sum(stats["e"]))
     return stats

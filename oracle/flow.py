@@ -35,20 +35,27 @@ def neighbour(i: int, a: int, n1: int, n2: int) -> int:
     return -1
 
 
-def edge_costs(st, Q=None):
+def edge_costs(st, Q=None, nus=None):
     """c_bar (I x 5, px^2 units, NaN for arcs leaving the grid), c_bar_ii = 0.
     For i != j, with the product candidate:
         c_bar_ij = (1/m_i) sum_{x in X_j} sum_y |x - y|^2 (mu(x)/m_j) nu_i(y) - Q_i
-    where Q_i = <c, pi_i>/m_i is the plan cost of basic cell i from the last
-    sweep (pi_hat_ii = pi_i/m_i; reading R13).  Direct double
-    sums over pixels (no moment shortcut)."""
+    where pi_i is the last sweep's plan on X_i, Q_i = <c, pi_i>/m_i
+    (pi_hat_ii = pi_i/m_i) and nu_i = P_Y pi_i its Y-marginal
+    (reading R13: the paper instantiates pi_i for this step).
+    Direct double sums over pixels (no moment shortcut).  Q and nus (list of
+    (r0, c0, array)) may be given explicitly; by default both come from
+    st.last."""
     if Q is None:
         Q = st.last["Q"]
+        if nus is None:
+            nus = st.last["nu_pre"]
+    if nus is None:
+        nus = st.boxes
     n1, n2, s = st.n1, st.n2, st.s
     I = n1 * n2
     cbar = np.full((I, 5), np.nan)
     for i in range(I):
-        r0, c0, d = st.boxes[i]
+        r0, c0, d = nus[i]
         yr, yc = np.nonzero(d > 0)
         vals = d[yr, yc]
         Y1 = (yr + r0).astype(np.float64)

@@ -1,0 +1,261 @@
+"""ctypes binding of libdomdec (include/domdec.h) — argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of libdomdec.so; this
+module only converts numpy arrays to pointers and status codes to
+exceptions.  There is no CPU fallback: if the shared library is missing or
+no CUDA device is usable, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdomdec.so")
+
+DD_OK, DD_ERR_ARG, DD_ERR_PRECOND, DD_ERR_NUMERIC, DD_ERR_CUDA, DD_ERR_OOM = 0, 1, 2, 3, 4, 6
+PART_A, PART_B = 0, 1
+
+
+class DomDecError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"libdomdec status {status}: {msg}")
+        self.status = status
+
+
+class _Problem(C.Structure):
+    _fields_ = [("N1", C.c_int32), ("N2", C.c_int32), ("h", C.c_double), ("eps", C.c_double),
+                ("cell_size", C.c_int32), ("mu", C.POINTER(C.c_double)), ("nu", C.POINTER(C.c_double)),
+                ("init_off", C.POINTER(C.c_int32)), ("init_ext", C.POINTER(C.c_int32)),
+                ("init_pos", C.POINTER(C.c_int64)), ("init_data", C.POINTER(C.c_double)),
+                ("mass_exponent", C.c_int32)]
+
+
+class _Options(C.Structure):
+    _fields_ = [("err", C.c_double), ("max_iter", C.c_int32), ("fixed_iter", C.c_int32),
+                ("trunc", C.c_double), ("slot_cap", C.c_int32), ("comp_cap", C.c_int32),
+                ("device", C.c_int32), ("stream", C.c_void_p)]
+
+
+class SweepStats(C.Structure):
+    _fields_ = [("cells", C.c_int64), ("nonconverged", C.c_int64), ("iters_total", C.c_int64),
+                ("iters_max", C.c_int32), ("overflow", C.c_int32), ("l1x_entry", C.c_double),
+                ("l1x_final", C.c_double), ("dropped_mass", C.c_double), ("mufu_ops", C.c_double),
+                ("bytes", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class FlowStats(C.Structure):
+    _fields_ = [("stationary", C.c_int32), ("certificate", C.c_int32), ("refines", C.c_int32),
+                ("rounds", C.c_int32), ("objective", C.c_int64), ("changed_cells", C.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class Counters(C.Structure):
+    _fields_ = [("sweeps", C.c_int64), ("flow_updates", C.c_int64), ("cells", C.c_int64), ("iters", C.c_int64),
+                ("mufu_ops", C.c_double), ("bytes", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    """Load libdomdec.so (built in-tree by __graft_entry__.build())."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        vp = C.c_void_p
+        L.domdec_init.argtypes = [C.POINTER(_Problem), C.POINTER(_Options), C.POINTER(vp)]
+        L.domdec_sweep.argtypes = [vp, C.c_int, C.POINTER(SweepStats)]
+        L.flow_update.argtypes = [vp, C.POINTER(FlowStats)]
+        L.marginal_error.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.primal_dual_gap.argtypes = [vp] + [C.POINTER(C.c_double)] * 4
+        L.domdec_export_cells.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int64),
+                                          C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_int64)]
+        L.domdec_export_alpha.argtypes = [vp, C.c_int, C.POINTER(C.c_double)]
+        L.domdec_export_plan_cost.argtypes = [vp, C.POINTER(C.c_double)]
+        L.flow_edge_costs.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.flow_apply.argtypes = [vp, C.POINTER(C.c_int64)]
+        L.dd_mincost_flow.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                      C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(FlowStats),
+                                      C.c_int32, vp]
+        L.domdec_destroy.argtypes = [vp]
+        L.domdec_counters.argtypes = [vp, C.POINTER(Counters)]
+        L.domdec_reset_counters.argtypes = [vp]
+        L.dd_mufu_peak.argtypes = [C.c_int32, C.POINTER(C.c_double)]
+        L.dd_last_error.argtypes = [vp]
+        L.dd_last_error.restype = C.c_char_p
+        L.dd_version.restype = C.c_char_p
+        for fn in ("domdec_init", "domdec_sweep", "flow_update", "marginal_error", "primal_dual_gap",
+                   "domdec_export_cells", "domdec_export_alpha", "domdec_export_plan_cost",
+                   "flow_edge_costs", "flow_apply", "dd_mincost_flow", "domdec_destroy", "domdec_counters",
+                   "domdec_reset_counters", "dd_mufu_peak"):
+            getattr(L, fn).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+EXPORTED = ("domdec_init", "domdec_sweep", "flow_update", "marginal_error", "primal_dual_gap",
+            "domdec_export_cells", "domdec_export_alpha", "domdec_export_plan_cost", "flow_edge_costs",
+            "flow_apply", "dd_mincost_flow", "domdec_destroy", "dd_last_error", "dd_version", "domdec_counters",
+            "domdec_reset_counters", "dd_mufu_peak")
+
+
+def _ptr(a, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+def _check(status, ctx):
+    if status != DD_OK:
+        msg = lib().dd_last_error(ctx)
+        raise DomDecError(status, msg.decode() if msg else "")
+
+
+class DomDec:
+    """One solver context (device state = basic-cell marginals + potentials).
+
+    Construction copies mu, nu and the initial basic-cell boxes to the GPU
+    (domdec_init); all further calls operate on device-resident state."""
+
+    def __init__(self, mu, nu, cell_size, eps, h, init_off, init_ext, init_pos, init_data, mass_exponent,
+                 err=1e-4, max_iter=2000, fixed_iter=0, trunc=1e-15, slot_cap=0, comp_cap=0, device=0,
+                 stream=None):
+        self._keep = [np.ascontiguousarray(mu, np.float64), np.ascontiguousarray(nu, np.float64),
+                      np.ascontiguousarray(init_off, np.int32), np.ascontiguousarray(init_ext, np.int32),
+                      np.ascontiguousarray(init_pos, np.int64), np.ascontiguousarray(init_data, np.float64)]
+        mu_, nu_, off_, ext_, pos_, data_ = self._keep
+        self.N1, self.N2 = mu_.shape
+        self.s = int(cell_size)
+        self.n1, self.n2 = self.N1 // self.s, self.N2 // self.s
+        self.I = self.n1 * self.n2
+        P = _Problem(self.N1, self.N2, float(h), float(eps), self.s, _ptr(mu_, C.c_double), _ptr(nu_, C.c_double),
+                     _ptr(off_, C.c_int32), _ptr(ext_, C.c_int32), _ptr(pos_, C.c_int64), _ptr(data_, C.c_double),
+                     int(mass_exponent))
+        O = _Options(float(err), int(max_iter), int(fixed_iter), float(trunc), int(slot_cap), int(comp_cap),
+                     int(device), C.c_void_p(stream) if stream else None)
+        ctx = C.c_void_p()
+        _check(lib().domdec_init(C.byref(P), C.byref(O), C.byref(ctx)), None)
+        self._ctx = ctx
+
+    @classmethod
+    def from_problem(cls, p, **kw):
+        """Build from a synth.Problem-like object (attributes mu, nu, s, eps, h,
+        init_off, init_ext, init_pos, init_data, E)."""
+        return cls(p.mu, p.nu, p.s, p.eps, p.h, p.init_off, p.init_ext, p.init_pos, p.init_data, p.E, **kw)
+
+    def sweep(self, part, stats=False):
+        st = SweepStats() if stats else None
+        _check(lib().domdec_sweep(self._ctx, PART_A if part in ("A", 0) else PART_B,
+                                  C.byref(st) if st is not None else None), self._ctx)
+        return st.as_dict() if st is not None else None
+
+    def flow_update(self, stats=False):
+        st = FlowStats() if stats else None
+        _check(lib().flow_update(self._ctx, C.byref(st) if st is not None else None), self._ctx)
+        return st.as_dict() if st is not None else None
+
+    def marginal_error(self):
+        x, y = C.c_double(), C.c_double()
+        _check(lib().marginal_error(self._ctx, C.byref(x), C.byref(y)), self._ctx)
+        return x.value, y.value
+
+    def primal_dual_gap(self):
+        v = [C.c_double() for _ in range(4)]
+        _check(lib().primal_dual_gap(self._ctx, *[C.byref(a) for a in v]), self._ctx)
+        return tuple(a.value for a in v)
+
+    def export_cells(self):
+        I = self.I
+        off = np.zeros((I, 2), np.int32)
+        ext = np.zeros((I, 2), np.int32)
+        pos = np.zeros(I, np.int64)
+        n = C.c_int64()
+        _check(lib().domdec_export_cells(self._ctx, _ptr(off, C.c_int32), _ptr(ext, C.c_int32),
+                                         _ptr(pos, C.c_int64), None, 0, C.byref(n)), self._ctx)
+        data = np.zeros(max(1, n.value), np.float64)
+        _check(lib().domdec_export_cells(self._ctx, _ptr(off, C.c_int32), _ptr(ext, C.c_int32),
+                                         _ptr(pos, C.c_int64), _ptr(data, C.c_double), data.size, C.byref(n)),
+               self._ctx)
+        return off, ext, pos, data[:n.value]
+
+    def boxes(self):
+        """Basic-cell marginals as a list of (r0, c0, 2-D array)."""
+        off, ext, pos, data = self.export_cells()
+        return [(int(off[i, 0]), int(off[i, 1]),
+                 data[pos[i]:pos[i] + ext[i, 0] * ext[i, 1]].reshape(ext[i, 0], ext[i, 1]))
+                for i in range(self.I)]
+
+    def export_alpha(self, part):
+        a = np.zeros((self.N1, self.N2), np.float64)
+        _check(lib().domdec_export_alpha(self._ctx, PART_A if part in ("A", 0) else PART_B, _ptr(a, C.c_double)),
+               self._ctx)
+        return a
+
+    def export_plan_cost(self):
+        q = np.zeros(self.I, np.float64)
+        _check(lib().domdec_export_plan_cost(self._ctx, _ptr(q, C.c_double)), self._ctx)
+        return q
+
+    def edge_costs(self):
+        cbar = np.zeros((self.I, 5), np.float64)
+        Cc = np.zeros((self.I, 5), np.int64)
+        q = np.zeros(self.I, np.int64)
+        _check(lib().flow_edge_costs(self._ctx, _ptr(cbar, C.c_double), _ptr(Cc, C.c_int64), _ptr(q, C.c_int64)),
+               self._ctx)
+        return cbar, Cc, q
+
+    def apply_flow(self, w):
+        w = np.ascontiguousarray(w, np.int64)
+        assert w.shape == (self.I, 5)
+        _check(lib().flow_apply(self._ctx, _ptr(w, C.c_int64)), self._ctx)
+
+    def counters(self):
+        cnt = Counters()
+        _check(lib().domdec_counters(self._ctx, C.byref(cnt)), self._ctx)
+        return cnt.as_dict()
+
+    def reset_counters(self):
+        _check(lib().domdec_reset_counters(self._ctx), self._ctx)
+
+    def close(self):
+        if getattr(self, "_ctx", None):
+            lib().domdec_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def mufu_peak(device=0):
+    """Measured ex2 throughput of the device (ops/s)."""
+    v = C.c_double()
+    _check(lib().dd_mufu_peak(int(device), C.byref(v)), None)
+    return v.value
+
+
+def mincost_flow(n1, n2, q, Cc, device=0, stream=None):
+    """Standalone GPU exact min-cost flow (dd_mincost_flow).  Returns
+    (w [I,5] int64, objective, stats dict)."""
+    q = np.ascontiguousarray(q, np.int64)
+    Cc = np.ascontiguousarray(Cc, np.int64)
+    w = np.zeros((n1 * n2, 5), np.int64)
+    obj = C.c_int64()
+    st = FlowStats()
+    _check(lib().dd_mincost_flow(int(n1), int(n2), _ptr(q, C.c_int64), _ptr(Cc, C.c_int64), _ptr(w, C.c_int64),
+                                 C.byref(obj), C.byref(st), int(device), C.c_void_p(stream) if stream else None),
+           None)
+    return w, obj.value, st.as_dict()

@@ -1,0 +1,634 @@
+// api.cu — C-ABI entry points of libdomdec (include/domdec.h).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ctx.cuh"
+
+using namespace dd;
+
+static std::string g_last_error;   // errors with no ctx (init / standalone solver)
+
+namespace {
+
+__global__ void k_init_mu(const double* __restrict__ mu, float* __restrict__ muf, float* __restrict__ l2,
+                          long long n) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t < n) {
+    const double v = mu[t];
+    muf[t] = (float)v;
+    l2[t] = v > 0.0 ? (float)log2(v) : kNeg;
+  }
+}
+
+// Y-marginal of the stored state: scatter-add all boxes (diagnostic, fp64).
+__global__ void k_scatter_boxes(const double* __restrict__ pool, const int* __restrict__ off,
+                                const int* __restrict__ ext, long long slot, int N2, double* __restrict__ acc) {
+  const int i = blockIdx.x;
+  const int r0 = off[2 * i], c0 = off[2 * i + 1], e1 = ext[2 * i], e2 = ext[2 * i + 1];
+  const double* src = pool + (long long)i * slot;
+  for (int t = threadIdx.x; t < e1 * e2; t += blockDim.x) {
+    const int r = t / e2, c = t - r * e2;
+    atomicAdd(&acc[(long long)(r0 + r) * N2 + c0 + c], src[t]);
+  }
+}
+
+// Deterministic single-block reductions for the diagnostics.
+__global__ void k_l1_diff(const double* __restrict__ a, const double* __restrict__ b, long long n,
+                          double* __restrict__ out) {
+  __shared__ double sh[1024];
+  double s = 0.0;
+  for (long long t = threadIdx.x; t < n; t += blockDim.x) s += fabs(a[t] - b[t]);
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = sh[0];
+}
+
+__global__ void k_sum_stats(const CellStats* __restrict__ st, int n, double* __restrict__ out) {
+  __shared__ double s0[256], s1[256];
+  double a = 0.0, b = 0.0;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) {
+    a += (double)st[t].e;
+    b += (double)st[t].e0;
+  }
+  s0[threadIdx.x] = a;
+  s1[threadIdx.x] = b;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      s0[threadIdx.x] += s0[threadIdx.x + o];
+      s1[threadIdx.x] += s1[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = s0[0];
+    out[1] = s1[0];
+  }
+}
+
+std::vector<CompCell> build_partition(int n1, int n2, int s, int kind) {
+  // Def. partitions; A = {2j, 2j+1}, B = {2j-1, 2j} clipped (R4)
+  std::vector<std::vector<int>> rows, cols;
+  if (kind == 0) {
+    for (int j = 0; 2 * j < n1; ++j) {
+      std::vector<int> r;
+      for (int x : {2 * j, 2 * j + 1})
+        if (x < n1) r.push_back(x);
+      rows.push_back(r);
+    }
+    for (int j = 0; 2 * j < n2; ++j) {
+      std::vector<int> r;
+      for (int x : {2 * j, 2 * j + 1})
+        if (x < n2) r.push_back(x);
+      cols.push_back(r);
+    }
+  } else {
+    for (int j = 0; j <= n1 / 2; ++j) {
+      std::vector<int> r;
+      for (int x : {2 * j - 1, 2 * j})
+        if (x >= 0 && x < n1) r.push_back(x);
+      if (!r.empty()) rows.push_back(r);
+    }
+    for (int j = 0; j <= n2 / 2; ++j) {
+      std::vector<int> r;
+      for (int x : {2 * j - 1, 2 * j})
+        if (x >= 0 && x < n2) r.push_back(x);
+      if (!r.empty()) cols.push_back(r);
+    }
+  }
+  std::vector<CompCell> out;
+  for (auto& rr : rows)
+    for (auto& cc : cols) {
+      CompCell c{};
+      c.r0 = rr[0] * s;
+      c.c0 = cc[0] * s;
+      c.n1 = (int)rr.size() * s;
+      c.n2 = (int)cc.size() * s;
+      c.nmem = 0;
+      for (size_t a = 0; a < rr.size(); ++a)
+        for (size_t b = 0; b < cc.size(); ++b) {
+          c.mem[c.nmem] = rr[a] * n2 + cc[b];
+          c.quad[c.nmem] = ((int)a << 1) | (int)b;
+          ++c.nmem;
+        }
+      for (int k = c.nmem; k < 4; ++k) {
+        c.mem[k] = -1;
+        c.quad[k] = 0;
+      }
+      out.push_back(c);
+    }
+  return out;
+}
+
+template <class T>
+dd_status dalloc(dd_ctx* c, T** p, size_t n) {
+  cudaError_t e = cudaMalloc((void**)p, n * sizeof(T) + 16);
+  if (e != cudaSuccess) {
+    c->err = std::string("cudaMalloc: ") + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? DD_ERR_OOM : DD_ERR_CUDA;
+  }
+  return DD_OK;
+}
+
+void free_ctx(dd_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  void* ptrs[] = {c->d_mu, c->d_log2mu, c->d_nu, c->d_m, c->d_q, c->d_pool[0], c->d_pool[1], c->d_off[0],
+                  c->d_off[1], c->d_ext[0], c->d_ext[1], c->d_cells[0], c->d_cells[1], c->d_alpha[0],
+                  c->d_alpha[1], c->d_gauge[0], c->d_gauge[1], c->d_stats[0], c->d_stats[1], c->d_totals[0],
+                  c->d_totals[1], c->d_mom, c->d_xbar, c->d_var, c->d_cbar, c->d_C, c->d_w, c->d_mcf,
+                  c->d_flow_info, c->d_scratch, c->d_red, c->d_ovf, c->d_cum};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+}  // namespace
+
+#define TRY(x)                     \
+  do {                             \
+    dd_status s_ = (x);            \
+    if (s_ != DD_OK) return s_;    \
+  } while (0)
+
+static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c) {
+  if (!P || !P->mu || !P->nu || !P->init_off || !P->init_ext || !P->init_pos || !P->init_data) {
+    c->err = "NULL problem pointer";
+    return DD_ERR_ARG;
+  }
+  if (P->N1 <= 0 || P->N2 <= 0 || P->cell_size <= 0 || P->N1 % P->cell_size || P->N2 % P->cell_size) {
+    c->err = "cell_size must be positive and divide N1 and N2";
+    return DD_ERR_ARG;
+  }
+  if (!(P->eps > 0) || !(P->h > 0)) {
+    c->err = "eps and h must be > 0";
+    return DD_ERR_ARG;
+  }
+  c->N1 = P->N1;
+  c->N2 = P->N2;
+  c->s = P->cell_size;
+  c->n1 = c->N1 / c->s;
+  c->n2 = c->N2 / c->s;
+  c->I = c->n1 * c->n2;
+  c->h = P->h;
+  c->eps = P->eps;
+  c->eps_p = P->eps / (P->h * P->h);
+  c->E = P->mass_exponent;
+  dd_options def{};
+  def.err = 1e-4;
+  def.max_iter = 2000;
+  def.fixed_iter = 0;
+  def.trunc = 1e-15;
+  c->opt = O ? *O : def;
+  if (!(c->opt.err > 0)) c->opt.err = 1e-4;
+  if (c->opt.max_iter <= 0) c->opt.max_iter = 2000;
+  if (c->opt.trunc < 0) {
+    c->err = "trunc must be >= 0";
+    return DD_ERR_ARG;
+  }
+  if (O == nullptr) c->opt.trunc = 1e-15;
+  c->device = c->opt.device;
+  const long long NN = (long long)c->N1 * c->N2;
+  const int I = c->I, s = c->s;
+  // ---- host validation (PAPER.md:233 m_i > 0; feasibility of pi^0) ----------
+  std::vector<double> m(I, 0.0);
+  double smu = 0, snu = 0;
+  for (long long t = 0; t < NN; ++t) {
+    if (!(P->mu[t] >= 0) || !(P->nu[t] >= 0) || !std::isfinite(P->mu[t]) || !std::isfinite(P->nu[t])) {
+      c->err = "mu and nu must be finite and >= 0";
+      return DD_ERR_PRECOND;
+    }
+    smu += P->mu[t];
+    snu += P->nu[t];
+    const int r = (int)(t / c->N2), cl = (int)(t % c->N2);
+    m[(r / s) * c->n2 + cl / s] += P->mu[t];
+  }
+  for (int i = 0; i < I; ++i)
+    if (!(m[i] > 0)) {
+      c->err = "zero-mass basic cell " + std::to_string(i) + " (PAPER.md:233 requires m_i > 0)";
+      return DD_ERR_PRECOND;
+    }
+  if (std::fabs(smu - snu) > 1e-6 * smu) {
+    c->err = "sum(mu) != sum(nu)";
+    return DD_ERR_PRECOND;
+  }
+  std::vector<double> acc(NN, 0.0);
+  int maxext1 = 0, maxext2 = 0;
+  long long maxbox = 0;
+  for (int i = 0; i < I; ++i) {
+    const int r0 = P->init_off[2 * i], c0 = P->init_off[2 * i + 1];
+    const int e1 = P->init_ext[2 * i], e2 = P->init_ext[2 * i + 1];
+    if (e1 < 1 || e2 < 1 || r0 < 0 || c0 < 0 || r0 + e1 > c->N1 || c0 + e2 > c->N2 || P->init_pos[i] < 0) {
+      c->err = "initial box " + std::to_string(i) + " outside the grid";
+      return DD_ERR_PRECOND;
+    }
+    double mass = 0;
+    for (int a = 0; a < e1; ++a)
+      for (int b = 0; b < e2; ++b) {
+        const double v = P->init_data[P->init_pos[i] + (long long)a * e2 + b];
+        if (!(v >= 0) || !std::isfinite(v)) {
+          c->err = "initial box values must be finite and >= 0";
+          return DD_ERR_PRECOND;
+        }
+        acc[(long long)(r0 + a) * c->N2 + c0 + b] += v;
+        mass += v;
+      }
+    if (std::fabs(mass - m[i]) > 1e-6 * m[i]) {
+      c->err = "initial ||nu_i|| != m_i for cell " + std::to_string(i);
+      return DD_ERR_PRECOND;
+    }
+    maxext1 = std::max(maxext1, e1);
+    maxext2 = std::max(maxext2, e2);
+    maxbox = std::max(maxbox, (long long)e1 * e2);
+  }
+  double l1 = 0;
+  for (long long t = 0; t < NN; ++t) l1 += std::fabs(acc[t] - P->nu[t]);
+  if (l1 > 1e-6 * snu) {
+    c->err = "initial boxes do not reproduce nu (L1 = " + std::to_string(l1) + ")";
+    return DD_ERR_PRECOND;
+  }
+  // ---- capacities -------------------------
+  const double tail = std::sqrt(c->eps_p * std::log(1e10));   // radius where nu_i drops ~1e-10 of its peak
+  int side = std::max(maxext1, maxext2);
+  // small size class: typical composite hull; large class: everything that
+  // fits in 227 KB of shared memory.
+  c->ccap = c->opt.comp_cap > 0 ? c->opt.comp_cap : 2 * s + 2 * (int)std::ceil(tail) + 4;
+  c->ccap = std::min(c->ccap, std::max(c->N1, c->N2));
+  c->ccap_big = c->ccap;
+  while (c->ccap_big < std::max(c->N1, c->N2) && sweep_smem_bytes(c->ccap_big + 1, s) <= 200 * 1024) ++c->ccap_big;
+  if (sweep_smem_bytes(c->ccap, s) > 200 * 1024) {
+    c->err = "composite box capacity too large for shared memory (eps too large for this build)";
+    return DD_ERR_ARG;
+  }
+  side = std::max(side, std::min(c->ccap_big, 2 * s + 2 * (int)std::ceil(tail) + 24));
+  c->slot = c->opt.slot_cap > 0 ? c->opt.slot_cap : std::max<long long>((long long)side * side, maxbox);
+  // ---- device --------------------------------------------------------------
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= c->device) {
+    c->err = "no CUDA device available (libdomdec has no CPU fallback)";
+    return DD_ERR_CUDA;
+  }
+  DD_CUDA(cudaSetDevice(c->device));
+  c->stream = (cudaStream_t)c->opt.stream;   // NULL = legacy default stream
+  cudaStream_t st = c->stream;
+  TRY(dalloc(c, &c->d_mu, NN));
+  TRY(dalloc(c, &c->d_log2mu, NN));
+  TRY(dalloc(c, &c->d_nu, NN));
+  TRY(dalloc(c, &c->d_m, I));
+  TRY(dalloc(c, &c->d_q, I));
+  TRY(dalloc(c, &c->d_mom, (size_t)I * 6));
+  DD_CUDA(cudaMemsetAsync(c->d_mom, 0, (size_t)I * 6 * 8, c->stream));
+  TRY(dalloc(c, &c->d_scratch, NN));
+  TRY(dalloc(c, &c->d_red, 64));
+  TRY(dalloc(c, &c->d_cum, 1));
+  DD_CUDA(cudaMemsetAsync(c->d_cum, 0, sizeof(SweepTotals), c->stream));
+  for (int b = 0; b < 2; ++b) {
+    TRY(dalloc(c, &c->d_pool[b], (size_t)I * c->slot));
+    TRY(dalloc(c, &c->d_off[b], (size_t)I * 2));
+    TRY(dalloc(c, &c->d_ext[b], (size_t)I * 2));
+    c->h_cells[b] = build_partition(c->n1, c->n2, s, b);
+    c->ncells[b] = (int)c->h_cells[b].size();
+    TRY(dalloc(c, &c->d_cells[b], c->ncells[b]));
+    TRY(dalloc(c, &c->d_alpha[b], NN));
+    TRY(dalloc(c, &c->d_gauge[b], (size_t)c->ncells[b] * 2));
+    TRY(dalloc(c, &c->d_stats[b], c->ncells[b]));
+    if (b == 1) TRY(dalloc(c, &c->d_ovf, (size_t)std::max(c->ncells[0], c->ncells[1]) + 4));
+    TRY(dalloc(c, &c->d_totals[b], 1));
+    DD_CUDA(cudaMemcpyAsync(c->d_cells[b], c->h_cells[b].data(), sizeof(CompCell) * c->ncells[b],
+                            cudaMemcpyHostToDevice, st));
+    DD_CUDA(cudaMemsetAsync(c->d_totals[b], 0, sizeof(SweepTotals), st));
+    DD_CUDA(cudaMemsetAsync(c->d_stats[b], 0, sizeof(CellStats) * c->ncells[b], st));
+  }
+  // mu / nu / masses / supplies
+  DD_CUDA(cudaMemcpyAsync(c->d_nu, P->nu, NN * 8, cudaMemcpyHostToDevice, st));
+  DD_CUDA(cudaMemcpyAsync(c->d_scratch, P->mu, NN * 8, cudaMemcpyHostToDevice, st));
+  k_init_mu<<<(unsigned)((NN + 255) / 256), 256, 0, st>>>(c->d_scratch, c->d_mu, c->d_log2mu, NN);
+  DD_CUDA(cudaGetLastError());
+  std::vector<int64_t> q(I);
+  const double scale = std::ldexp(1.0, c->E);
+  for (int i = 0; i < I; ++i) q[i] = (int64_t)std::llrint(m[i] * scale);
+  for (int i = 0; i < I; ++i)
+    if (q[i] <= 0) {
+      c->err = "mass_exponent too small: a supply q_i = rint(m_i 2^E) is 0";
+      return DD_ERR_PRECOND;
+    }
+  DD_CUDA(cudaMemcpyAsync(c->d_m, m.data(), I * 8, cudaMemcpyHostToDevice, st));
+  DD_CUDA(cudaMemcpyAsync(c->d_q, q.data(), I * 8, cudaMemcpyHostToDevice, st));
+  // initial boxes -> pool[0] (slots)
+  {
+    std::vector<double> pool((size_t)I * c->slot, 0.0);
+    for (int i = 0; i < I; ++i) {
+      const long long len = (long long)P->init_ext[2 * i] * P->init_ext[2 * i + 1];
+      std::memcpy(&pool[(size_t)i * c->slot], P->init_data + P->init_pos[i], len * 8);
+    }
+    DD_CUDA(cudaMemcpyAsync(c->d_pool[0], pool.data(), pool.size() * 8, cudaMemcpyHostToDevice, st));
+    DD_CUDA(cudaMemcpyAsync(c->d_off[0], P->init_off, I * 8, cudaMemcpyHostToDevice, st));
+    DD_CUDA(cudaMemcpyAsync(c->d_ext[0], P->init_ext, I * 8, cudaMemcpyHostToDevice, st));
+    DD_CUDA(cudaStreamSynchronize(st));   // host staging buffer goes out of scope
+  }
+  c->cur = 0;
+  TRY(flow_init_static(c));
+  DD_CUDA(cudaStreamSynchronize(st));
+  return DD_OK;
+}
+
+extern "C" {
+
+dd_status domdec_init(const dd_problem* problem, const dd_options* options, dd_ctx** out) {
+  if (!out) {
+    g_last_error = "out is NULL";
+    return DD_ERR_ARG;
+  }
+  *out = nullptr;
+  dd_ctx* c = new dd_ctx();
+  dd_status s = init_impl(problem, options, c);
+  if (s != DD_OK) {
+    g_last_error = c->err;
+    free_ctx(c);
+    return s;
+  }
+  *out = c;
+  return DD_OK;
+}
+
+dd_status domdec_sweep(dd_ctx* c, dd_partition part, dd_sweep_stats* stats) {
+  if (!c || (part != DD_PART_A && part != DD_PART_B)) return DD_ERR_ARG;
+  DD_CUDA(cudaSetDevice(c->device));
+  const int b = (int)part;
+  SweepParams p{};
+  p.N1 = c->N1;
+  p.N2 = c->N2;
+  p.s = c->s;
+  p.w = (float)(1.4426950408889634 / c->eps_p);
+  p.mu = c->d_mu;
+  p.log2mu = c->d_log2mu;
+  p.cells = c->d_cells[b];
+  p.ncells = c->ncells[b];
+  p.pool_in = c->d_pool[c->cur];
+  p.off_in = c->d_off[c->cur];
+  p.ext_in = c->d_ext[c->cur];
+  p.pool_out = c->d_pool[1 - c->cur];
+  p.off_out = c->d_off[1 - c->cur];
+  p.ext_out = c->d_ext[1 - c->cur];
+  p.slot = c->slot;
+  p.ccap = c->ccap;
+  p.alpha = c->d_alpha[b];
+  p.gauge = c->d_gauge[b];
+  p.alpha_valid = c->alpha_valid[b];
+  p.m = c->d_m;
+  p.tol = (float)c->opt.err;
+  p.max_iter = c->opt.max_iter;
+  p.fixed_iter = c->opt.fixed_iter;
+  p.tau = c->opt.trunc;
+  p.stats = c->d_stats[b];
+  p.totals = c->d_totals[b];
+  p.cum = c->d_cum;
+  p.mom = c->d_mom;
+  DD_CUDA(cudaMemsetAsync(c->d_totals[b], 0, sizeof(SweepTotals), c->stream));
+  p.ovf_count = c->d_ovf;
+  p.ovf_list = c->d_ovf + 1;
+  DD_CUDA(launch_sweep(p, c->ccap, c->ccap_big, c->stream));
+  c->cur = 1 - c->cur;
+  ++c->n_sweeps;
+  c->alpha_valid[b] = 1;
+  c->last_part = b;
+  c->swept |= (1 << b);
+  if (stats) {
+    SweepTotals t{};
+    DD_CUDA(cudaMemcpyAsync(&t, c->d_totals[b], sizeof(t), cudaMemcpyDeviceToHost, c->stream));
+    DD_CUDA(cudaStreamSynchronize(c->stream));
+    stats->cells = (int64_t)t.cells;
+    stats->nonconverged = (int64_t)t.nonconv;
+    stats->iters_total = (int64_t)t.iters;
+    stats->iters_max = t.iters_max;
+    stats->overflow = (int32_t)t.overflow;
+    stats->l1x_entry = t.e0;
+    stats->l1x_final = t.e;
+    stats->dropped_mass = t.dropped;
+    stats->mufu_ops = (double)t.mufu;
+    stats->bytes = (double)t.bytes;
+    if (t.overflow) {
+      c->err = "box capacity exceeded in " + std::to_string(t.overflow) + " composite cells (left unchanged)";
+      return DD_ERR_NUMERIC;
+    }
+  }
+  return DD_OK;
+}
+
+dd_status marginal_error(dd_ctx* c, double* l1_x, double* l1_y) {
+  if (!c) return DD_ERR_ARG;
+  DD_CUDA(cudaSetDevice(c->device));
+  const long long NN = (long long)c->N1 * c->N2;
+  double hx = NAN, hy = NAN;
+  if (c->last_part >= 0) {
+    k_sum_stats<<<1, 256, 0, c->stream>>>(c->d_stats[c->last_part], c->ncells[c->last_part], c->d_red);
+    DD_CUDA(cudaGetLastError());
+    DD_CUDA(cudaMemcpyAsync(&hx, c->d_red, 8, cudaMemcpyDeviceToHost, c->stream));
+  }
+  DD_CUDA(cudaMemsetAsync(c->d_scratch, 0, NN * 8, c->stream));
+  k_scatter_boxes<<<c->I, 128, 0, c->stream>>>(c->d_pool[c->cur], c->d_off[c->cur], c->d_ext[c->cur], c->slot,
+                                               c->N2, c->d_scratch);
+  DD_CUDA(cudaGetLastError());
+  k_l1_diff<<<1, 1024, 0, c->stream>>>(c->d_scratch, c->d_nu, NN, c->d_red + 8);
+  DD_CUDA(cudaGetLastError());
+  DD_CUDA(cudaMemcpyAsync(&hy, c->d_red + 8, 8, cudaMemcpyDeviceToHost, c->stream));
+  DD_CUDA(cudaStreamSynchronize(c->stream));
+  if (l1_x) *l1_x = hx;
+  if (l1_y) *l1_y = hy;
+  return DD_OK;
+}
+
+dd_status domdec_export_cells(dd_ctx* c, int32_t* off, int32_t* ext, int64_t* pos, double* data,
+                              int64_t data_cap, int64_t* data_len) {
+  if (!c) return DD_ERR_ARG;
+  DD_CUDA(cudaSetDevice(c->device));
+  const int I = c->I;
+  std::vector<int> ho(2 * I), he(2 * I);
+  DD_CUDA(cudaMemcpyAsync(ho.data(), c->d_off[c->cur], I * 8, cudaMemcpyDeviceToHost, c->stream));
+  DD_CUDA(cudaMemcpyAsync(he.data(), c->d_ext[c->cur], I * 8, cudaMemcpyDeviceToHost, c->stream));
+  DD_CUDA(cudaStreamSynchronize(c->stream));
+  int64_t total = 0;
+  for (int i = 0; i < I; ++i) total += (int64_t)he[2 * i] * he[2 * i + 1];
+  if (data_len) *data_len = total;
+  if (off) std::memcpy(off, ho.data(), I * 8);
+  if (ext) std::memcpy(ext, he.data(), I * 8);
+  if (pos) {
+    int64_t p = 0;
+    for (int i = 0; i < I; ++i) {
+      pos[i] = p;
+      p += (int64_t)he[2 * i] * he[2 * i + 1];
+    }
+  }
+  if (!data) return DD_OK;
+  if (data_cap < total) {
+    c->err = "data_cap too small";
+    return DD_ERR_ARG;
+  }
+  std::vector<double> pool((size_t)I * c->slot);
+  DD_CUDA(cudaMemcpyAsync(pool.data(), c->d_pool[c->cur], pool.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  DD_CUDA(cudaStreamSynchronize(c->stream));
+  int64_t p = 0;
+  for (int i = 0; i < I; ++i) {
+    const int64_t len = (int64_t)he[2 * i] * he[2 * i + 1];
+    std::memcpy(data + p, &pool[(size_t)i * c->slot], len * 8);
+    p += len;
+  }
+  return DD_OK;
+}
+
+dd_status domdec_export_alpha(dd_ctx* c, dd_partition part, double* alpha) {
+  if (!c || !alpha || (part != DD_PART_A && part != DD_PART_B)) return DD_ERR_ARG;
+  const int b = (int)part;
+  if (!c->alpha_valid[b]) {
+    c->err = "partition never swept";
+    return DD_ERR_PRECOND;
+  }
+  DD_CUDA(cudaSetDevice(c->device));
+  const long long NN = (long long)c->N1 * c->N2;
+  std::vector<float> a(NN), mu(NN);
+  std::vector<int> g(2 * c->ncells[b]);
+  DD_CUDA(cudaMemcpyAsync(a.data(), c->d_alpha[b], NN * 4, cudaMemcpyDeviceToHost, c->stream));
+  DD_CUDA(cudaMemcpyAsync(mu.data(), c->d_mu, NN * 4, cudaMemcpyDeviceToHost, c->stream));
+  DD_CUDA(cudaMemcpyAsync(g.data(), c->d_gauge[b], g.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+  DD_CUDA(cudaStreamSynchronize(c->stream));
+  // a(k) = ln2 * A2(kappa) + (|D|^2 + 2 D.kappa)/eps' with D = K - G;
+  // then subtract the mu-weighted mean per composite cell.
+  for (int J = 0; J < c->ncells[b]; ++J) {
+    const CompCell& cc = c->h_cells[b][J];
+    const double D1 = cc.r0 - g[2 * J], D2 = cc.c0 - g[2 * J + 1];
+    double sw = 0, swa = 0;
+    for (int k1 = 0; k1 < cc.n1; ++k1)
+      for (int k2 = 0; k2 < cc.n2; ++k2) {
+        const long long pix = (long long)(cc.r0 + k1) * c->N2 + cc.c0 + k2;
+        const double v = 0.69314718055994531 * a[pix] + (D1 * D1 + D2 * D2 + 2 * (D1 * k1 + D2 * k2)) / c->eps_p;
+        alpha[pix] = v;
+        sw += mu[pix];
+        swa += mu[pix] * v;
+      }
+    const double mean = swa / sw;
+    for (int k1 = 0; k1 < cc.n1; ++k1)
+      for (int k2 = 0; k2 < cc.n2; ++k2) alpha[(long long)(cc.r0 + k1) * c->N2 + cc.c0 + k2] -= mean;
+  }
+  return DD_OK;
+}
+
+dd_status domdec_export_plan_cost(dd_ctx* c, double* Qm) {
+  if (!c || !Qm) return DD_ERR_ARG;
+  DD_CUDA(cudaSetDevice(c->device));
+  std::vector<double> mom((size_t)c->I * 6);
+  DD_CUDA(cudaMemcpyAsync(mom.data(), c->d_mom, mom.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  DD_CUDA(cudaStreamSynchronize(c->stream));
+  // <c, pi_i> = sum_y nu_i^pre(y) E[|x - y|^2 | y] = G0 - 2 G1 + M2 (centred moments)
+  for (int i = 0; i < c->I; ++i) Qm[i] = mom[6 * i + 3] - 2.0 * mom[6 * i + 4] + mom[6 * i + 5];
+  return DD_OK;
+}
+
+dd_status flow_update(dd_ctx* c, dd_flow_stats* stats) {
+  if (!c) return DD_ERR_ARG;
+  if (c->last_part < 0) {
+    c->err = "flow_update needs a previous sweep (plan costs, reading R13)";
+    return DD_ERR_PRECOND;
+  }
+  DD_CUDA(cudaSetDevice(c->device));
+  return flow_update_impl(c, stats);
+}
+
+dd_status primal_dual_gap(dd_ctx* c, double* primal, double* dual, double* rel_gap, double* transport_cost) {
+  if (!c) return DD_ERR_ARG;
+  if (c->swept != 3) {
+    c->err = "primal_dual_gap needs at least one A and one B sweep";
+    return DD_ERR_PRECOND;
+  }
+  DD_CUDA(cudaSetDevice(c->device));
+  return pd_gap_impl(c, primal, dual, rel_gap, transport_cost);
+}
+
+dd_status domdec_counters(dd_ctx* c, dd_counters* out) {
+  if (!c || !out) return DD_ERR_ARG;
+  DD_CUDA(cudaSetDevice(c->device));
+  SweepTotals t{};
+  DD_CUDA(cudaMemcpyAsync(&t, c->d_cum, sizeof(t), cudaMemcpyDeviceToHost, c->stream));
+  DD_CUDA(cudaStreamSynchronize(c->stream));
+  out->sweeps = c->n_sweeps;
+  out->flow_updates = c->n_flows;
+  out->cells = (int64_t)t.cells;
+  out->iters = (int64_t)t.iters;
+  out->mufu_ops = (double)t.mufu;
+  out->bytes = (double)t.bytes;
+  return DD_OK;
+}
+
+dd_status domdec_reset_counters(dd_ctx* c) {
+  if (!c) return DD_ERR_ARG;
+  DD_CUDA(cudaSetDevice(c->device));
+  DD_CUDA(cudaMemsetAsync(c->d_cum, 0, sizeof(SweepTotals), c->stream));
+  c->n_sweeps = 0;
+  c->n_flows = 0;
+  return DD_OK;
+}
+
+static __global__ void k_mufu_probe(float* out, int iters) {
+  // 8 independent ex2 chains per thread (latency hidden by ILP + occupancy)
+  float x[8];
+  for (int k = 0; k < 8; ++k) x[k] = -0.001f * (threadIdx.x + k);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float y;
+      asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x[k]));
+      x[k] = y - 1.0f;
+    }
+  }
+  float s = 0.f;
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == 12345.f) out[0] = s;
+}
+
+dd_status dd_mufu_peak(int32_t device, double* ops_per_s) {
+  if (!ops_per_s) return DD_ERR_ARG;
+  if (cudaSetDevice(device) != cudaSuccess) return DD_ERR_CUDA;
+  int nsm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+  float* d = nullptr;
+  if (cudaMalloc(&d, 16) != cudaSuccess) return DD_ERR_OOM;
+  const int blocks = nsm * 8, threads = 256, iters = 4096;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  k_mufu_probe<<<blocks, threads>>>(d, 64);   // warm-up
+  cudaEventRecord(e0);
+  k_mufu_probe<<<blocks, threads>>>(d, iters);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  if (cudaGetLastError() != cudaSuccess || ms <= 0) return DD_ERR_CUDA;
+  *ops_per_s = (double)blocks * threads * iters * 8.0 / (ms * 1e-3);
+  return DD_OK;
+}
+
+dd_status domdec_destroy(dd_ctx* c) {
+  free_ctx(c);
+  return DD_OK;
+}
+
+const char* dd_last_error(const dd_ctx* c) {
+  if (c) return c->err.c_str();
+  return g_last_error.c_str();
+}
+
+const char* dd_version(void) { return "libdomdec 0.1 sm_100a (arXiv 2405.09400 hot path)"; }
+
+}  // extern "C"

@@ -1,0 +1,77 @@
+// ctx.cuh — the dd_ctx object (internal).
+#pragma once
+#include <string>
+#include <vector>
+
+#include "../../include/domdec.h"
+#include "internal.cuh"
+
+struct dd_ctx {
+  // problem
+  int N1 = 0, N2 = 0, s = 0, n1 = 0, n2 = 0, I = 0;
+  double h = 0, eps = 0, eps_p = 0;
+  int E = 0;
+  dd_options opt{};
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int device = 0;
+  std::string err;
+  // device data
+  float* d_mu = nullptr;
+  float* d_log2mu = nullptr;
+  double* d_nu = nullptr;
+  double* d_m = nullptr;
+  int64_t* d_q = nullptr;
+  double* d_pool[2] = {nullptr, nullptr};
+  int* d_off[2] = {nullptr, nullptr};
+  int* d_ext[2] = {nullptr, nullptr};
+  int cur = 0;
+  long long slot = 0;
+  int ccap = 0;        // small size class (composite hull side)
+  int ccap_big = 0;    // large size class
+  int* d_ovf = nullptr; // [max ncells + 1] deferred-cell queue (count at [0])
+  dd::CompCell* d_cells[2] = {nullptr, nullptr};
+  int ncells[2] = {0, 0};
+  std::vector<dd::CompCell> h_cells[2];
+  float* d_alpha[2] = {nullptr, nullptr};
+  int* d_gauge[2] = {nullptr, nullptr};
+  int alpha_valid[2] = {0, 0};
+  dd::CellStats* d_stats[2] = {nullptr, nullptr};
+  dd::SweepTotals* d_totals[2] = {nullptr, nullptr};
+  dd::SweepTotals* d_cum = nullptr;
+  long long n_sweeps = 0, n_flows = 0;
+  int last_part = -1;
+  int swept = 0;
+  double* d_mom = nullptr;   // [I][6] plan moments of the last sweep (R13)
+  // flow update
+  double* d_xbar = nullptr;   // [I][2] mu-mean of X_i (pixel units)
+  double* d_var = nullptr;    // [I] trace of the covariance of mu_i / m_i
+  double* d_cbar = nullptr;   // [I][5]
+  int64_t* d_C = nullptr;     // [I][5]
+  int64_t* d_w = nullptr;     // [I][5]
+  void* d_mcf = nullptr;      // solver workspace
+  size_t mcf_bytes = 0;
+  int* d_flow_info = nullptr; // [16] device flags of the last flow update
+  // diagnostics scratch
+  double* d_scratch = nullptr; // [N1*N2]
+  double* d_red = nullptr;     // [64]
+};
+
+namespace dd {
+dd_status flow_update_impl(dd_ctx* c, dd_flow_stats* stats);
+dd_status flow_costs_impl(dd_ctx* c);
+dd_status flow_apply_impl(dd_ctx* c);
+dd_status mcf_solve_device(int n1, int n2, const int64_t* d_q, const int64_t* d_C, int64_t* d_w,
+                           void** d_ws, size_t* ws_bytes, int* d_info, cudaStream_t st, std::string& err);
+dd_status flow_init_static(dd_ctx* c);
+dd_status pd_gap_impl(dd_ctx* c, double* primal, double* dual, double* rel_gap, double* transport);
+}  // namespace dd
+
+#define DD_CUDA(call)                                                        \
+  do {                                                                       \
+    cudaError_t e_ = (call);                                                 \
+    if (e_ != cudaSuccess) {                                                 \
+      c->err = std::string(#call) + ": " + cudaGetErrorString(e_);           \
+      return (e_ == cudaErrorMemoryAllocation) ? DD_ERR_OOM : DD_ERR_CUDA;   \
+    }                                                                        \
+  } while (0)

@@ -1,0 +1,421 @@
+// flow.cu — flow update steps 1 and 3 (§5.1) and the
+// flow-related C-ABI entry points.
+//
+// Step 1 (F1): edge costs c_bar_ij = <c, pi_hat_ij - pi_hat_ii> (Eq. edge-cost
+// PAPER.md:419-421) with the product gluing candidate
+// pi_hat_ij = mu_j/m_j (x) nu_i/m_i, where pi_i is the last
+// sweep's plan on X_i and nu_i = P_Y pi_i (reading R13).  Closed form through
+// moments about the cell centre z_i:
+//   m_i c_bar_ij = M0 W_ij - G0 - 2 M1 . (xbar_j - z_i) + 2 G1,
+//   W_ij = E_{mu_j}|x - z_i|^2 = V_j + |xbar_j - z_i|^2,
+// the |y|^2 terms cancelling exactly.  One thread per basic cell, no plan is
+// instantiated (this sidesteps the memory bottleneck noted at PAPER.md:927).
+// Step 3 (F3): nu_hat_j = sum_{i in N(j)} (w_ij / q_i) nu_i (Lemma, Eq.
+// flow-update-cell-marginals PAPER.md:453-456), bounding-box merge + truncate
+// + minimal box, one CTA per changed cell.
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "ctx.cuh"
+
+namespace dd {
+
+long long* mcf_info_ptr(void* ws, int I);
+
+namespace {
+
+__device__ __forceinline__ int nbr_cell(int i, int a, int n1, int n2) {
+  const int i1 = i / n2, i2 = i - (i / n2) * n2;
+  switch (a) {
+    case 0: return i;
+    case 1: return i1 > 0 ? i - n2 : -1;
+    case 2: return i1 + 1 < n1 ? i + n2 : -1;
+    case 3: return i2 > 0 ? i - 1 : -1;
+    default: return i2 + 1 < n2 ? i + 1 : -1;
+  }
+}
+
+// Static mu moments of each basic cell: xbar_i (pixel coords) and
+// V_i = E_{mu_i/m_i} |x - xbar_i|^2.
+__global__ void k_mu_moments(const double* __restrict__ mu, int N2, int s, int n2, int I,
+                             double* __restrict__ xbar, double* __restrict__ var) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= I) return;
+  const int i1 = i / n2, i2 = i - i1 * n2;
+  double m = 0, a = 0, b = 0;
+  for (int r = 0; r < s; ++r)
+    for (int c = 0; c < s; ++c) {
+      const double v = mu[(long long)(i1 * s + r) * N2 + i2 * s + c];
+      m += v;
+      a += v * (i1 * s + r);
+      b += v * (i2 * s + c);
+    }
+  a /= m;
+  b /= m;
+  double vv = 0;
+  for (int r = 0; r < s; ++r)
+    for (int c = 0; c < s; ++c) {
+      const double v = mu[(long long)(i1 * s + r) * N2 + i2 * s + c];
+      const double d1 = i1 * s + r - a, d2 = i2 * s + c - b;
+      vv += v * (d1 * d1 + d2 * d2);
+    }
+  xbar[2 * i] = a;
+  xbar[2 * i + 1] = b;
+  var[i] = vv / m;
+}
+
+__global__ void k_flow_costs(const double* __restrict__ mom, const double* __restrict__ xbar,
+                             const double* __restrict__ var, const double* __restrict__ m, int n1, int n2, int s,
+                             double* __restrict__ cbar, long long* __restrict__ C) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n1 * n2) return;
+  const int i1 = i / n2, i2 = i - i1 * n2;
+  const double z1 = i1 * s + 0.5 * (s - 1), z2 = i2 * s + 0.5 * (s - 1);
+  const double M0 = mom[6 * i], M1a = mom[6 * i + 1], M1b = mom[6 * i + 2];
+  const double G0 = mom[6 * i + 3], G1 = mom[6 * i + 4];
+  cbar[5 * i] = 0.0;
+  C[5 * i] = 0;
+  for (int a = 1; a < 5; ++a) {
+    const int j = nbr_cell(i, a, n1, n2);
+    if (j < 0) {
+      cbar[5 * i + a] = nan("");
+      C[5 * i + a] = 0;
+      continue;
+    }
+    const double x1 = xbar[2 * j] - z1, x2 = xbar[2 * j + 1] - z2;
+    const double W = var[j] + x1 * x1 + x2 * x2;
+    const double cb = (M0 * W - G0 - 2.0 * (M1a * x1 + M1b * x2) + 2.0 * G1) / m[i];
+    cbar[5 * i + a] = cb;
+    C[5 * i + a] = __double2ll_rn(cb * 1024.0);   // reading R11: round half even
+  }
+}
+
+// F3: one CTA per target cell j.  Writes the new box of every changed cell
+// into the spare buffer; k_copy_back then moves it into the live buffer.
+__global__ void k_apply_flow(const long long* __restrict__ w, const long long* __restrict__ q, int n1, int n2,
+                             const double* __restrict__ pool, const int* __restrict__ off,
+                             const int* __restrict__ ext, double* __restrict__ pool_new, int* __restrict__ off_new,
+                             int* __restrict__ ext_new, long long slot, int cap_side, double tau,
+                             unsigned long long* __restrict__ counters, double* __restrict__ dropped) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* acc = (double*)smem;
+  __shared__ int src[5];
+  __shared__ double frac[5];
+  __shared__ int nsrc;
+  __shared__ int bnd[4];
+  __shared__ double dsum[32];
+  const int j = blockIdx.x;
+  if (w[5LL * j] == q[j]) return;   // no inflow from a neighbour: nu_j unchanged
+  if (threadIdx.x == 0) {
+    int k = 0;
+    if (w[5LL * j] > 0) { src[k] = j; frac[k] = (double)w[5LL * j] / (double)q[j]; ++k; }
+    // from up (its 'down' arc 2), down ('up' 1), left ('right' 4), right ('left' 3)
+    const int srcs[4] = {nbr_cell(j, 1, n1, n2), nbr_cell(j, 2, n1, n2), nbr_cell(j, 3, n1, n2),
+                         nbr_cell(j, 4, n1, n2)};
+    const int arcs[4] = {2, 1, 4, 3};
+    for (int t = 0; t < 4; ++t) {
+      const int i = srcs[t];
+      if (i < 0) continue;
+      const long long wij = w[5LL * i + arcs[t]];
+      if (wij > 0) { src[k] = i; frac[k] = (double)wij / (double)q[i]; ++k; }
+    }
+    nsrc = k;
+    int L1 = 1 << 30, L2 = 1 << 30, U1 = -1, U2 = -1;
+    for (int t = 0; t < k; ++t) {
+      const int i = src[t];
+      L1 = min(L1, off[2 * i]);
+      L2 = min(L2, off[2 * i + 1]);
+      U1 = max(U1, off[2 * i] + ext[2 * i]);
+      U2 = max(U2, off[2 * i + 1] + ext[2 * i + 1]);
+    }
+    bnd[0] = L1; bnd[1] = L2; bnd[2] = U1 - L1; bnd[3] = U2 - L2;
+  }
+  __syncthreads();
+  const int L1 = bnd[0], L2 = bnd[1], b1 = bnd[2], b2 = bnd[3];
+  if (b1 > cap_side || b2 > cap_side) {
+    if (threadIdx.x == 0) atomicAdd(&counters[1], 1ull);
+    return;
+  }
+  for (int t = threadIdx.x; t < b1 * b2; t += blockDim.x) acc[t] = 0.0;
+  __syncthreads();
+  for (int k = 0; k < nsrc; ++k) {
+    const int i = src[k];
+    const double f = frac[k];
+    const int r0 = off[2 * i] - L1, c0 = off[2 * i + 1] - L2, e1 = ext[2 * i], e2 = ext[2 * i + 1];
+    const double* d = pool + (long long)i * slot;
+    for (int t = threadIdx.x; t < e1 * e2; t += blockDim.x) {
+      const int r = t / e2, c = t - r * e2;
+      double* a = &acc[(r0 + r) * b2 + c0 + c];
+      *a = __dadd_rn(*a, __dmul_rn(f, d[t]));
+    }
+    __syncthreads();
+  }
+  __shared__ int mm[4];
+  if (threadIdx.x == 0) { mm[0] = 1 << 30; mm[1] = -1; mm[2] = 1 << 30; mm[3] = -1; }
+  __syncthreads();
+  double dr = 0.0;
+  for (int t = threadIdx.x; t < b1 * b2; t += blockDim.x) {
+    const double v = acc[t];
+    const int r = t / b2, c = t - r * b2;
+    if (v >= tau) {
+      atomicMin(&mm[0], r); atomicMax(&mm[1], r); atomicMin(&mm[2], c); atomicMax(&mm[3], c);
+    } else if (v > 0.0) {
+      dr += v;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) dr += __shfl_xor_sync(0xffffffffu, dr, o);
+  if ((threadIdx.x & 31) == 0) dsum[threadIdx.x >> 5] = dr;
+  __syncthreads();
+  const int e1 = mm[1] - mm[0] + 1, e2 = mm[3] - mm[2] + 1;
+  if (mm[1] < mm[0] || (long long)e1 * e2 > slot) {
+    if (threadIdx.x == 0) atomicAdd(&counters[1], 1ull);
+    return;
+  }
+  double* dst = pool_new + (long long)j * slot;
+  for (int t = threadIdx.x; t < e1 * e2; t += blockDim.x) {
+    const int r = t / e2, c = t - r * e2;
+    const double v = acc[(mm[0] + r) * b2 + mm[2] + c];
+    dst[t] = v >= tau ? v : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    off_new[2 * j] = L1 + mm[0];
+    off_new[2 * j + 1] = L2 + mm[2];
+    ext_new[2 * j] = e1;
+    ext_new[2 * j + 1] = e2;
+    double s = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += dsum[k];
+    atomicAdd(dropped, s);
+    atomicAdd(&counters[0], 1ull);
+  }
+}
+
+__global__ void k_copy_back(const long long* __restrict__ w, const long long* __restrict__ q,
+                            const double* __restrict__ pool_new, const int* __restrict__ off_new,
+                            const int* __restrict__ ext_new, double* __restrict__ pool, int* __restrict__ off,
+                            int* __restrict__ ext, long long slot, const unsigned long long* __restrict__ counters) {
+  const int j = blockIdx.x;
+  if (w[5LL * j] == q[j]) return;
+  if (counters[1] != 0) return;   // some cell failed: keep the old state everywhere
+  const int e1 = ext_new[2 * j], e2 = ext_new[2 * j + 1];
+  const double* s = pool_new + (long long)j * slot;
+  double* d = pool + (long long)j * slot;
+  for (int t = threadIdx.x; t < e1 * e2; t += blockDim.x) d[t] = s[t];
+  if (threadIdx.x == 0) {
+    off[2 * j] = off_new[2 * j];
+    off[2 * j + 1] = off_new[2 * j + 1];
+    ext[2 * j] = e1;
+    ext[2 * j + 1] = e2;
+  }
+}
+
+__global__ void k_check_flow(const long long* __restrict__ w, const long long* __restrict__ q, int n1, int n2,
+                             unsigned long long* __restrict__ bad) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n1 * n2) return;
+  long long out = 0, in = 0;
+  for (int a = 0; a < 5; ++a) {
+    const long long v = w[5LL * j + a];
+    if (v < 0) atomicAdd(bad, 1ull);
+    if (nbr_cell(j, a, n1, n2) < 0 && v != 0) atomicAdd(bad, 1ull);
+    out += v;
+  }
+  in += w[5LL * j];
+  const int srcs[4] = {nbr_cell(j, 1, n1, n2), nbr_cell(j, 2, n1, n2), nbr_cell(j, 3, n1, n2), nbr_cell(j, 4, n1, n2)};
+  const int arcs[4] = {2, 1, 4, 3};
+  for (int t = 0; t < 4; ++t)
+    if (srcs[t] >= 0) in += w[5LL * srcs[t] + arcs[t]];
+  if (out != q[j] || in != q[j]) atomicAdd(bad, 1ull);
+}
+
+}  // namespace
+
+dd_status flow_init_static(dd_ctx* c) {
+  const int I = c->I;
+  auto alloc = [&](void** p, size_t bytes) -> dd_status {
+    cudaError_t e = cudaMalloc(p, bytes + 16);
+    if (e != cudaSuccess) {
+      c->err = std::string("cudaMalloc: ") + cudaGetErrorString(e);
+      return DD_ERR_OOM;
+    }
+    return DD_OK;
+  };
+  dd_status s;
+  if ((s = alloc((void**)&c->d_xbar, (size_t)I * 16))) return s;
+  if ((s = alloc((void**)&c->d_var, (size_t)I * 8))) return s;
+  if ((s = alloc((void**)&c->d_cbar, (size_t)I * 40))) return s;
+  if ((s = alloc((void**)&c->d_C, (size_t)I * 40))) return s;
+  if ((s = alloc((void**)&c->d_w, (size_t)I * 40))) return s;
+  if ((s = alloc((void**)&c->d_flow_info, 64 * 8))) return s;
+  // d_scratch still holds mu (fp64) from init
+  k_mu_moments<<<(I + 127) / 128, 128, 0, c->stream>>>(c->d_scratch, c->N2, c->s, c->n2, I, c->d_xbar, c->d_var);
+  DD_CUDA(cudaGetLastError());
+  return DD_OK;
+}
+
+static dd_status apply_w(dd_ctx* c, unsigned long long* d_counters, double* d_dropped) {
+  const int I = c->I;
+  const int cap_side = (int)std::min<long long>(c->ccap_big + 8, 72);
+  const size_t smem = (size_t)cap_side * cap_side * 8;
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    DD_CUDA(cudaFuncSetAttribute(k_apply_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = smem;
+  }
+  const int cur = c->cur, spare = 1 - c->cur;
+  k_apply_flow<<<I, 128, smem, c->stream>>>((const long long*)c->d_w, (const long long*)c->d_q, c->n1, c->n2,
+                                             c->d_pool[cur], c->d_off[cur], c->d_ext[cur], c->d_pool[spare],
+                                             c->d_off[spare], c->d_ext[spare], c->slot, cap_side, c->opt.trunc,
+                                             d_counters, d_dropped);
+  DD_CUDA(cudaGetLastError());
+  k_copy_back<<<I, 128, 0, c->stream>>>((const long long*)c->d_w, (const long long*)c->d_q, c->d_pool[spare],
+                                         c->d_off[spare], c->d_ext[spare], c->d_pool[cur], c->d_off[cur],
+                                         c->d_ext[cur], c->slot, d_counters);
+  DD_CUDA(cudaGetLastError());
+  return DD_OK;
+}
+
+dd_status flow_costs_impl(dd_ctx* c) {
+  k_flow_costs<<<(c->I + 127) / 128, 128, 0, c->stream>>>(c->d_mom, c->d_xbar, c->d_var, c->d_m, c->n1, c->n2, c->s,
+                                                         c->d_cbar, (long long*)c->d_C);
+  DD_CUDA(cudaGetLastError());
+  return DD_OK;
+}
+
+dd_status flow_update_impl(dd_ctx* c, dd_flow_stats* stats) {
+  ++c->n_flows;
+  dd_status s = flow_costs_impl(c);
+  if (s) return s;
+  s = mcf_solve_device(c->n1, c->n2, c->d_q, c->d_C, c->d_w, &c->d_mcf, &c->mcf_bytes, nullptr, c->stream, c->err);
+  if (s) return s;
+  unsigned long long* ctr = (unsigned long long*)c->d_flow_info;   // [0] changed, [1] failed
+  double* dropped = (double*)(c->d_flow_info + 8);
+  DD_CUDA(cudaMemsetAsync(c->d_flow_info, 0, 64 * 8, c->stream));
+  s = apply_w(c, ctr, dropped);
+  if (s) return s;
+  if (stats) {
+    long long info[16];
+    unsigned long long cnt[2];
+    DD_CUDA(cudaMemcpyAsync(info, mcf_info_ptr(c->d_mcf, c->I), sizeof(info), cudaMemcpyDeviceToHost, c->stream));
+    DD_CUDA(cudaMemcpyAsync(cnt, ctr, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
+    DD_CUDA(cudaStreamSynchronize(c->stream));
+    stats->objective = info[0];
+    stats->stationary = (int32_t)info[1];
+    stats->certificate = (int32_t)info[2];
+    stats->refines = (int32_t)info[3];
+    stats->rounds = (int32_t)info[4];
+    stats->changed_cells = (int64_t)cnt[0];
+    if (info[6]) {
+      c->err = "min-cost flow did not converge (round cap)";
+      return DD_ERR_NUMERIC;
+    }
+    if (cnt[1]) {
+      c->err = "flow apply exceeded the box capacity; state left unchanged";
+      return DD_ERR_NUMERIC;
+    }
+  }
+  return DD_OK;
+}
+
+dd_status pd_gap_impl(dd_ctx* c, double*, double*, double*, double*) {
+  c->err = "primal_dual_gap: not implemented in this build";
+  return DD_ERR_ARG;
+}
+
+}  // namespace dd
+
+using namespace dd;
+
+extern "C" {
+
+dd_status flow_edge_costs(dd_ctx* c, double* cbar, int64_t* C, int64_t* q) {
+  if (!c) return DD_ERR_ARG;
+  DD_CUDA(cudaSetDevice(c->device));
+  dd_status s = flow_costs_impl(c);
+  if (s) return s;
+  if (cbar) DD_CUDA(cudaMemcpyAsync(cbar, c->d_cbar, (size_t)c->I * 40, cudaMemcpyDeviceToHost, c->stream));
+  if (C) DD_CUDA(cudaMemcpyAsync(C, c->d_C, (size_t)c->I * 40, cudaMemcpyDeviceToHost, c->stream));
+  if (q) DD_CUDA(cudaMemcpyAsync(q, c->d_q, (size_t)c->I * 8, cudaMemcpyDeviceToHost, c->stream));
+  DD_CUDA(cudaStreamSynchronize(c->stream));
+  return DD_OK;
+}
+
+dd_status flow_apply(dd_ctx* c, const int64_t* w) {
+  if (!c || !w) return DD_ERR_ARG;
+  DD_CUDA(cudaSetDevice(c->device));
+  DD_CUDA(cudaMemcpyAsync(c->d_w, w, (size_t)c->I * 40, cudaMemcpyHostToDevice, c->stream));
+  unsigned long long* ctr = (unsigned long long*)c->d_flow_info;
+  double* dropped = (double*)(c->d_flow_info + 8);
+  DD_CUDA(cudaMemsetAsync(c->d_flow_info, 0, 64 * 8, c->stream));
+  k_check_flow<<<(c->I + 127) / 128, 128, 0, c->stream>>>((const long long*)c->d_w, (const long long*)c->d_q, c->n1,
+                                                         c->n2, ctr + 2);
+  DD_CUDA(cudaGetLastError());
+  unsigned long long bad = 0;
+  DD_CUDA(cudaMemcpyAsync(&bad, ctr + 2, 8, cudaMemcpyDeviceToHost, c->stream));
+  DD_CUDA(cudaStreamSynchronize(c->stream));
+  if (bad) {
+    c->err = "w violates the divergence constraints (PAPER.md:350-354)";
+    return DD_ERR_PRECOND;
+  }
+  dd_status s = apply_w(c, ctr, dropped);
+  if (s) return s;
+  unsigned long long cnt[2];
+  DD_CUDA(cudaMemcpyAsync(cnt, ctr, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
+  DD_CUDA(cudaStreamSynchronize(c->stream));
+  if (cnt[1]) {
+    c->err = "flow apply exceeded the box capacity; state left unchanged";
+    return DD_ERR_NUMERIC;
+  }
+  return DD_OK;
+}
+
+dd_status dd_mincost_flow(int32_t n1, int32_t n2, const int64_t* q, const int64_t* C, int64_t* w, int64_t* objective,
+                          dd_flow_stats* stats, int32_t device, void* stream) {
+  if (n1 <= 0 || n2 <= 0 || !q || !C || !w) return DD_ERR_ARG;
+  const int I = n1 * n2;
+  for (int i = 0; i < I; ++i) {
+    if (q[i] <= 0) return DD_ERR_ARG;
+    for (int a = 1; a < 5; ++a)
+      if (C[5 * i + a] >= (1LL << 40) || C[5 * i + a] <= -(1LL << 40)) return DD_ERR_ARG;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) return DD_ERR_CUDA;
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t *dq = nullptr, *dC = nullptr, *dw = nullptr;
+  void* ws = nullptr;
+  size_t wsb = 0;
+  std::string err;
+  dd_status s = DD_OK;
+  if (cudaMalloc(&dq, I * 8) || cudaMalloc(&dC, I * 40) || cudaMalloc(&dw, I * 40)) {
+    s = DD_ERR_OOM;
+  } else {
+    cudaMemcpyAsync(dq, q, I * 8, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(dC, C, I * 40, cudaMemcpyHostToDevice, st);
+    s = mcf_solve_device(n1, n2, dq, dC, dw, &ws, &wsb, nullptr, st, err);
+    if (s == DD_OK) {
+      long long info[16];
+      cudaMemcpyAsync(w, dw, I * 40, cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(info, mcf_info_ptr(ws, I), sizeof(info), cudaMemcpyDeviceToHost, st);
+      if (cudaStreamSynchronize(st) != cudaSuccess) {
+        s = DD_ERR_CUDA;
+      } else {
+        if (objective) *objective = info[0];
+        if (stats) {
+          stats->objective = info[0];
+          stats->stationary = (int32_t)info[1];
+          stats->certificate = (int32_t)info[2];
+          stats->refines = (int32_t)info[3];
+          stats->rounds = (int32_t)info[4];
+          stats->changed_cells = 0;
+        }
+        if (info[6]) s = DD_ERR_NUMERIC;
+      }
+    }
+  }
+  if (dq) cudaFree(dq);
+  if (dC) cudaFree(dC);
+  if (dw) cudaFree(dw);
+  if (ws) cudaFree(ws);
+  return s;
+}
+
+}  // extern "C"

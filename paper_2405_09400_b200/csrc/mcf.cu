@@ -1,0 +1,473 @@
+// mcf.cu — exact min-cost flow on the basic-cell grid graph (flow update
+// step 2, §5.1; Eq. MinCostFlow PAPER.md:378-381 with the
+// divergence constraints PAPER.md:350-354).
+//
+// The LP is a transportation problem: sources S_i with supply q_i, sinks T_j
+// with demand q_j, arcs S_i -> T_j for j in N(i) (self + 4 neighbours) with
+// integer cost C_ij (reading R11).  It is solved exactly on the GPU by
+// Goldberg-Tarjan cost scaling with synchronous push/relabel rounds inside ONE
+// cooperative persistent kernel (grid-wide barriers, no host round trips):
+//   * costs are scaled by SC = 2I + 1 (> number of nodes), so an eps-optimal
+//     flow with eps = 1 is optimal;
+//   * refine(eps): saturate every residual arc with negative reduced cost,
+//     then rounds of {push (prices frozen; each arc pair is touched by at most
+//     one endpoint because admissibility is antisymmetric), merge excess,
+//     relabel (p(v) = max over residual arcs of p(u) - c(v,u) - eps, computed
+//     from the previous round's prices: simultaneous relabels only lower
+//     prices and keep eps-optimality)} until no node has excess;
+//   * before scaling, a Bellman-Ford negative-cycle test on (I, 4-nbr arcs, C)
+//     certifies stationarity (no negative cycle <=> the stationary flow is
+//     optimal); near the optimum it passes
+//     in one round.
+// Every decision depends only on the previous round's state and integer
+// atomics commute, so the result is deterministic.
+#include <cooperative_groups.h>
+
+#include <string>
+
+#include "../../include/domdec.h"
+#include "internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace dd {
+
+struct McfArgs {
+  int n1, n2, I;
+  const long long* q;     // [I]
+  const long long* C;     // [I][5] original integer costs
+  long long* w;           // [I][5] flow (output)
+  long long* cs;          // [I][5] scaled costs
+  long long* eS;          // [I] excess of sources
+  long long* eT;          // [I] excess of sinks
+  unsigned long long* addS;   // [I] incoming excess of this round (two's complement adds)
+  unsigned long long* addT;
+  long long* pS[2];       // prices, double-buffered by round parity
+  long long* pT[2];
+  long long* dist[2];     // Bellman-Ford labels (certificate) / source labels (price update)
+  long long* distT[2];    // sink labels (price update)
+  unsigned long long* ctr;  // [16] counters
+  long long* info;        // [16] results: 0 objective, 1 stationary, 2 certificate, 3 refines, 4 rounds, 6 error
+  int bf_rounds;
+  int max_rounds;
+};
+
+__device__ __forceinline__ int nbr(int i, int a, int n1, int n2) {
+  const int i1 = i / n2, i2 = i - (i / n2) * n2;
+  switch (a) {
+    case 0: return i;
+    case 1: return i1 > 0 ? i - n2 : -1;
+    case 2: return i1 + 1 < n1 ? i + n2 : -1;
+    case 3: return i2 > 0 ? i - 1 : -1;
+    default: return i2 + 1 < n2 ? i + 1 : -1;
+  }
+}
+
+// incoming arc k (0..4) of sink T_j: source index and its arc number
+__device__ __forceinline__ int in_arc(int j, int k, int n1, int n2, int* a_out) {
+  const int j1 = j / n2, j2 = j - (j / n2) * n2;
+  switch (k) {
+    case 0: *a_out = 0; return j;
+    case 1: *a_out = 2; return j1 > 0 ? j - n2 : -1;       // from up, its 'down' arc
+    case 2: *a_out = 1; return j1 + 1 < n1 ? j + n2 : -1;  // from down, its 'up' arc
+    case 3: *a_out = 4; return j2 > 0 ? j - 1 : -1;        // from left, its 'right' arc
+    default: *a_out = 3; return j2 + 1 < n2 ? j + 1 : -1;  // from right, its 'left' arc
+  }
+}
+
+constexpr long long kInf = (1LL << 60);
+
+__device__ __forceinline__ long long floor_div(long long a, long long b) {   // b > 0
+  long long q = a / b;
+  if ((a % b != 0) && (a < 0)) --q;
+  return q;
+}
+
+// Global price update (Goldberg's set-relabel, parallel Bellman-Ford): d(v) =
+// length of the shortest residual path from v to a deficit node with arc
+// lengths l(v,u) = floor(c_p(v,u)/eps) + 1; then p(v) -= eps * d(v).  Keeps
+// eps-optimality and makes every shortest path admissible.  Applied only if
+// the labels converged within the round cap.  Uniform control flow.
+__device__ void price_update(const McfArgs& A, cg::grid_group& grid, int par, long long eps, long long gt,
+                             long long gs, int cap_rounds) {
+  const int n1 = A.n1, n2 = A.n2, I = A.I;
+  long long* pS = A.pS[par];
+  long long* pT = A.pT[par];
+  for (long long i = gt; i < I; i += gs) {
+    A.dist[0][i] = A.eS[i] < 0 ? 0 : kInf;
+    A.distT[0][i] = A.eT[i] < 0 ? 0 : kInf;
+  }
+  if (gt == 0) { A.ctr[10] = 0; A.ctr[11] = 0; A.ctr[12] = 0; }
+  grid.sync();
+  int r = 0;
+  bool conv = false;
+  for (; r < cap_rounds; ++r) {
+    const long long* dS0 = A.dist[r & 1];
+    const long long* dT0 = A.distT[r & 1];
+    long long* dS1 = A.dist[(r + 1) & 1];
+    long long* dT1 = A.distT[(r + 1) & 1];
+    for (long long i = gt; i < I; i += gs) {
+      long long best = dS0[i];
+      if (best > 0) {
+        for (int a = 0; a < 5; ++a) {
+          const int j = nbr((int)i, a, n1, n2);
+          if (j < 0 || A.q[i] - A.w[5 * i + a] <= 0) continue;
+          const long long du = dT0[j];
+          if (du >= kInf) continue;
+          long long l = floor_div(A.cs[5 * i + a] + pS[i] - pT[j], eps) + 1;
+          if (l < 0) l = 0;
+          if (l > (1LL << 40)) l = (1LL << 40);
+          if (du + l < best) best = du + l;
+        }
+      }
+      dS1[i] = best;
+      long long bt = dT0[i];
+      if (bt > 0) {
+        for (int k = 0; k < 5; ++k) {
+          int a;
+          const int src = in_arc((int)i, k, n1, n2, &a);
+          if (src < 0 || A.w[5LL * src + a] <= 0) continue;
+          const long long du = dS0[src];
+          if (du >= kInf) continue;
+          long long l = floor_div(-(A.cs[5LL * src + a] + pS[src] - pT[i]), eps) + 1;
+          if (l < 0) l = 0;
+          if (l > (1LL << 40)) l = (1LL << 40);
+          if (du + l < bt) bt = du + l;
+        }
+      }
+      dT1[i] = bt;
+      if (best != dS0[i] || bt != dT0[i]) atomicAdd(&A.ctr[10 + (r & 1)], 1ull);
+    }
+    grid.sync();
+    const unsigned long long ch = A.ctr[10 + (r & 1)];
+    grid.sync();
+    if (gt == 0) A.ctr[10 + ((r + 1) & 1)] = 0;
+    if (ch == 0) { conv = true; ++r; break; }
+  }
+  grid.sync();
+  if (!conv) return;
+  const long long* dS = A.dist[r & 1];
+  const long long* dT = A.distT[r & 1];
+  for (long long i = gt; i < I; i += gs) {
+    if (dS[i] < kInf) atomicMax(&A.ctr[12], (unsigned long long)dS[i]);
+    if (dT[i] < kInf) atomicMax(&A.ctr[12], (unsigned long long)dT[i]);
+  }
+  grid.sync();
+  const long long Dmax = (long long)A.ctr[12];
+  for (long long i = gt; i < I; i += gs) {
+    const long long a = dS[i] < kInf ? dS[i] : Dmax;
+    const long long b = dT[i] < kInf ? dT[i] : Dmax;
+    pS[i] -= eps * a;
+    pT[i] -= eps * b;
+  }
+  grid.sync();
+}
+
+__global__ void mcf_kernel(McfArgs A) {
+  cg::grid_group grid = cg::this_grid();
+  const int n1 = A.n1, n2 = A.n2, I = A.I;
+  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long gs = (long long)gridDim.x * blockDim.x;
+  const long long SC = 2LL * I + 1;
+
+  // ---- init: stationary flow, scaled costs, max |C| -------------------------
+  for (long long i = gt; i < I; i += gs) {
+    for (int a = 0; a < 5; ++a) {
+      const int j = nbr((int)i, a, n1, n2);
+      A.w[5 * i + a] = (a == 0) ? A.q[i] : 0;
+      const long long c = (j >= 0 && a > 0) ? A.C[5 * i + a] : 0;
+      A.cs[5 * i + a] = c * SC;
+      if (j >= 0 && a > 0) {
+        const unsigned long long ab = (unsigned long long)(c < 0 ? -c : c);
+        atomicMax(&A.ctr[0], ab);
+        if (c < 0) atomicAdd(&A.ctr[1], 1ull);
+      }
+    }
+    A.dist[0][i] = 0;
+    A.pS[0][i] = 0;
+    A.pT[0][i] = 0;
+    A.eS[i] = 0;
+    A.eT[i] = 0;
+    A.addS[i] = 0;
+    A.addT[i] = 0;
+  }
+  grid.sync();
+  const bool any_negative = A.ctr[1] > 0;
+  if (!any_negative) {
+    if (gt == 0) {
+      A.info[0] = 0; A.info[1] = 1; A.info[2] = 1; A.info[3] = 0; A.info[4] = 0;
+    }
+    return;
+  }
+  // ---- Bellman-Ford certificate on (I, 4-nbr arcs, C) -----------------------
+  int cert = 0;
+  for (int r = 0; r < A.bf_rounds; ++r) {
+    const long long* d0 = A.dist[r & 1];
+    long long* d1 = A.dist[(r + 1) & 1];
+    for (long long j = gt; j < I; j += gs) {
+      long long best = d0[j];
+      for (int k = 1; k < 5; ++k) {
+        int a;
+        const int i = in_arc((int)j, k, n1, n2, &a);
+        if (i < 0) continue;
+        const long long cand = d0[i] + A.C[5LL * i + a];
+        if (cand < best) best = cand;
+      }
+      d1[j] = best;
+      if (best != d0[j]) atomicAdd(&A.ctr[2 + (r & 1)], 1ull);
+    }
+    grid.sync();
+    const unsigned long long changed = A.ctr[2 + (r & 1)];
+    grid.sync();
+    if (gt == 0) A.ctr[2 + ((r + 1) & 1)] = 0;
+    grid.sync();
+    if (changed == 0) { cert = 1; break; }
+  }
+  if (cert) {
+    if (gt == 0) { A.info[0] = 0; A.info[1] = 1; A.info[2] = 1; A.info[3] = 0; A.info[4] = 0; }
+    return;
+  }
+  // ---- cost scaling -----------------------------------------------------------
+  long long eps = (long long)A.ctr[0] * SC;
+  int refines = 0, rounds = 0, par = 0;
+  bool failed = false;
+  while (eps >= 1 && !failed) {
+    eps = (eps + 15) / 16;   // alpha = 16
+    if (eps < 1) eps = 1;
+    ++refines;
+    const long long* pSo = A.pS[par];
+    const long long* pTo = A.pT[par];
+    // saturate arcs with negative reduced cost (both directions)
+    for (long long i = gt; i < I; i += gs) {
+      for (int a = 0; a < 5; ++a) {
+        const int j = nbr((int)i, a, n1, n2);
+        if (j < 0) continue;
+        const long long cp = A.cs[5 * i + a] + pSo[i] - pTo[j];
+        if (cp < 0) A.w[5 * i + a] = A.q[i];
+        else if (cp > 0) A.w[5 * i + a] = 0;
+      }
+    }
+    grid.sync();
+    for (long long i = gt; i < I; i += gs) {
+      long long out = 0;
+      for (int a = 0; a < 5; ++a) out += A.w[5 * i + a];
+      A.eS[i] = A.q[i] - out;
+      long long in = 0;
+      for (int k = 0; k < 5; ++k) {
+        int a;
+        const int src = in_arc((int)i, k, n1, n2, &a);
+        if (src >= 0) in += A.w[5LL * src + a];
+      }
+      A.eT[i] = in - A.q[i];
+    }
+    grid.sync();
+    const int gu_every = 2 * (n1 + n2) + 32;
+    const int gu_cap = 8 * (n1 + n2) + 256;
+    price_update(A, grid, par, eps, gt, gs, gu_cap);
+    int since_gu = 0;
+    for (;;) {
+      if (rounds >= A.max_rounds) { failed = true; break; }
+      ++rounds;
+      if (++since_gu >= gu_every) {
+        since_gu = 0;
+        price_update(A, grid, par, eps, gt, gs, gu_cap);
+      }
+      const long long* pS = A.pS[par];
+      const long long* pT = A.pT[par];
+      // push phase (prices frozen)
+      for (long long i = gt; i < I; i += gs) {
+        long long e = A.eS[i];
+        if (e > 0) {
+          for (int a = 0; a < 5 && e > 0; ++a) {
+            const int j = nbr((int)i, a, n1, n2);
+            if (j < 0) continue;
+            const long long r = A.q[i] - A.w[5 * i + a];
+            if (r <= 0) continue;
+            if (A.cs[5 * i + a] + pS[i] - pT[j] < 0) {
+              const long long d = e < r ? e : r;
+              A.w[5 * i + a] += d;
+              e -= d;
+              atomicAdd(&A.addT[j], (unsigned long long)d);
+            }
+          }
+          A.eS[i] = e;
+        }
+        long long f = A.eT[i];
+        if (f > 0) {
+          for (int k = 0; k < 5 && f > 0; ++k) {
+            int a;
+            const int src = in_arc((int)i, k, n1, n2, &a);
+            if (src < 0) continue;
+            const long long r = A.w[5LL * src + a];
+            if (r <= 0) continue;
+            if (A.cs[5LL * src + a] + pS[src] - pT[i] > 0) {   // reverse arc has negative reduced cost
+              const long long d = f < r ? f : r;
+              A.w[5LL * src + a] -= d;
+              f -= d;
+              atomicAdd(&A.addS[src], (unsigned long long)d);
+            }
+          }
+          A.eT[i] = f;
+        }
+      }
+      grid.sync();
+      // merge incoming excess, count active nodes
+      for (long long i = gt; i < I; i += gs) {
+        const long long es = A.eS[i] + (long long)A.addS[i];
+        const long long et = A.eT[i] + (long long)A.addT[i];
+        A.addS[i] = 0;
+        A.addT[i] = 0;
+        A.eS[i] = es;
+        A.eT[i] = et;
+        if (es > 0) atomicAdd(&A.ctr[4 + (rounds & 1)], 1ull);
+        if (et > 0) atomicAdd(&A.ctr[4 + (rounds & 1)], 1ull);
+      }
+      grid.sync();
+      const unsigned long long active = A.ctr[4 + (rounds & 1)];
+      if (gt == 0) A.ctr[4 + ((rounds + 1) & 1)] = 0;
+      if (active == 0) {
+        grid.sync();
+        break;
+      }
+      // relabel phase: new prices from the frozen ones
+      long long* pSn = A.pS[par ^ 1];
+      long long* pTn = A.pT[par ^ 1];
+      for (long long i = gt; i < I; i += gs) {
+        long long ps = pS[i];
+        if (A.eS[i] > 0) {
+          bool adm = false;
+          long long best = LLONG_MIN;
+          for (int a = 0; a < 5; ++a) {
+            const int j = nbr((int)i, a, n1, n2);
+            if (j < 0) continue;
+            if (A.q[i] - A.w[5 * i + a] <= 0) continue;
+            const long long cp = A.cs[5 * i + a] + pS[i] - pT[j];
+            if (cp < 0) { adm = true; break; }
+            const long long cand = pT[j] - A.cs[5 * i + a];
+            if (cand > best) best = cand;
+          }
+          if (!adm && best != LLONG_MIN) ps = best - eps;
+        }
+        pSn[i] = ps;
+        long long pt = pT[i];
+        if (A.eT[i] > 0) {
+          bool adm = false;
+          long long best = LLONG_MIN;
+          for (int k = 0; k < 5; ++k) {
+            int a;
+            const int src = in_arc((int)i, k, n1, n2, &a);
+            if (src < 0) continue;
+            if (A.w[5LL * src + a] <= 0) continue;
+            const long long cp = A.cs[5LL * src + a] + pS[src] - pT[i];
+            if (cp > 0) { adm = true; break; }
+            const long long cand = pS[src] + A.cs[5LL * src + a];
+            if (cand > best) best = cand;
+          }
+          if (!adm && best != LLONG_MIN) pt = best - eps;
+        }
+        pTn[i] = pt;
+      }
+      grid.sync();
+      par ^= 1;
+    }
+    if (eps == 1) break;
+  }
+  // ---- objective (original integer costs) -------------------------------------
+  if (gt == 0) A.ctr[8] = 0;
+  grid.sync();
+  for (long long i = gt; i < I; i += gs) {
+    long long acc = 0;
+    for (int a = 1; a < 5; ++a)
+      if (nbr((int)i, a, n1, n2) >= 0) acc += A.w[5 * i + a] * A.C[5 * i + a];
+    atomicAdd(&A.ctr[8], (unsigned long long)acc);
+  }
+  grid.sync();
+  const long long obj = (long long)A.ctr[8];
+  if (obj >= 0 && !failed) {   // stationary flow is optimal: keep it exactly
+    for (long long i = gt; i < I; i += gs)
+      for (int a = 0; a < 5; ++a) A.w[5 * i + a] = (a == 0) ? A.q[i] : 0;
+  }
+  if (gt == 0) {
+    A.info[0] = obj >= 0 ? 0 : obj;
+    A.info[1] = obj >= 0 ? 1 : 0;
+    A.info[2] = 0;
+    A.info[3] = refines;
+    A.info[4] = rounds;
+    A.info[6] = failed ? 1 : 0;
+  }
+  if (failed) {
+    for (long long i = gt; i < I; i += gs)
+      for (int a = 0; a < 5; ++a) A.w[5 * i + a] = (a == 0) ? A.q[i] : 0;
+  }
+}
+
+static size_t ws_size(int I) {
+  // cs, w handled by caller for w; workspace: cs[5I] eS eT addS addT pS0 pS1 pT0 pT1 d0 d1 ctr[16]
+  return sizeof(long long) * (5ull * I + 12ull * I) + 16 * sizeof(unsigned long long) + 256;
+}
+
+dd_status mcf_solve_device(int n1, int n2, const int64_t* d_q, const int64_t* d_C, int64_t* d_w, void** d_ws,
+                           size_t* ws_bytes, int* d_info_unused, cudaStream_t st, std::string& err) {
+  (void)d_info_unused;
+  const int I = n1 * n2;
+  const size_t need = ws_size(I) + 16 * sizeof(long long);
+  if (*ws_bytes < need) {
+    if (*d_ws) cudaFree(*d_ws);
+    *d_ws = nullptr;
+    if (cudaMalloc(d_ws, need) != cudaSuccess) {
+      err = "mcf workspace allocation failed";
+      return DD_ERR_OOM;
+    }
+    *ws_bytes = need;
+  }
+  char* base = (char*)*d_ws;
+  McfArgs A;
+  A.n1 = n1;
+  A.n2 = n2;
+  A.I = I;
+  A.q = (const long long*)d_q;
+  A.C = (const long long*)d_C;
+  A.w = (long long*)d_w;
+  long long* p = (long long*)base;
+  A.cs = p; p += 5LL * I;
+  A.eS = p; p += I;
+  A.eT = p; p += I;
+  A.addS = (unsigned long long*)p; p += I;
+  A.addT = (unsigned long long*)p; p += I;
+  A.pS[0] = p; p += I;
+  A.pS[1] = p; p += I;
+  A.pT[0] = p; p += I;
+  A.pT[1] = p; p += I;
+  A.dist[0] = p; p += I;
+  A.dist[1] = p; p += I;
+  A.distT[0] = p; p += I;
+  A.distT[1] = p; p += I;
+  A.ctr = (unsigned long long*)p; p += 16;
+  A.info = p;
+  A.bf_rounds = 2 * (n1 + n2) + 8;
+  A.max_rounds = 2000000;
+  cudaError_t e = cudaMemsetAsync(A.ctr, 0, 32 * sizeof(long long), st);
+  if (e != cudaSuccess) { err = cudaGetErrorString(e); return DD_ERR_CUDA; }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int nsm = 0, per = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int threads = 256;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mcf_kernel, threads, 0);
+  if (per <= 0) { err = "mcf kernel cannot be resident"; return DD_ERR_CUDA; }
+  long long want = (I + threads - 1) / threads;
+  long long blocks = (long long)nsm * per;
+  if (want < blocks) blocks = want;
+  if (blocks < 1) blocks = 1;
+  void* args[] = {&A};
+  e = cudaLaunchCooperativeKernel((void*)mcf_kernel, dim3((unsigned)blocks), dim3(threads), args, 0, st);
+  if (e != cudaSuccess) { err = std::string("mcf launch: ") + cudaGetErrorString(e); return DD_ERR_CUDA; }
+  return DD_OK;
+}
+
+long long* mcf_info_ptr(void* ws, int I) {
+  char* base = (char*)ws;
+  return (long long*)(base + sizeof(long long) * (17ull * I) + 16 * sizeof(unsigned long long));
+}
+
+}  // namespace dd

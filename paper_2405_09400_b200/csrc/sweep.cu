@@ -1,0 +1,720 @@
+// sweep.cu — the fused domain-decomposition sweep kernel (sm_100a).
+//
+// One CTA per composite cell J of the partition (batched over all cells, as
+// the batched SinkhornGPU of App. A.1).  Per cell, in one
+// launch and without leaving the SM:
+//   a1 BasicToComposite   nu_J = sum_{i in J} nu_i on the hull box
+//                         (Eq. get-composite-cell-marginal PAPER.md:1128-1133)
+//   a2 log-domain separable Sinkhorn on X_J x box(nu_J),
+//      fp32, base-2, in a per-cell local gauge,
+//      stopping rule = L1 X-marginal error after the Y-update <= Err mu(X_J)
+//      (per-cell reading R6), warm start from the previous
+//      sweep on the same partition (reading R7)
+//   a3 CompositeToBasic   nu_i = nu_J * exp(S_i - LSE_i' S_i') (share form of
+//                         PAPER.md:1151-1193), plus
+//                         the plan cost <c, pi_i> for the flow update (R13)
+//   a4 Balance            proportional pooling (Alg. 4 l.6 PAPER.md:1231, R8)
+//   a5 Truncate + minimal box (Alg. 4 l.7 PAPER.md:1233, tau PAPER.md:1265)
+//   a6 per-cell stats for the sweep reductions.
+// The linear-domain marginals (pool, nu_J, shares, balance) are fp64 so that
+// the global Y-marginal is preserved to fp64 rounding.
+#include "internal.cuh"
+
+namespace dd {
+
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2f(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// 2^x - 1 with relative accuracy near 0 (X-error of a nearly converged cell).
+__device__ __forceinline__ float exp2m1f(float x) {
+  if (fabsf(x) < 0.0625f) {
+    const float t = x * 0.69314718055994531f;
+    return t * (1.0f + t * (0.5f + t * (0.16666667f + t * 0.041666668f)));
+  }
+  return ex2f(x) - 1.0f;
+}
+
+// Deterministic block reductions (fixed thread->data map, fixed tree).
+template <int NV>
+__device__ __forceinline__ void block_sum_d(double (&v)[NV], double* scratch) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  }
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) scratch[wid * NV + k] = v[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double t = 0.0;
+    for (int w = 0; w < nw; ++w) t += scratch[w * NV + k];
+    v[k] = t;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ float block_max_f(float v, float* scratch) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if (lane == 0) scratch[wid] = v;
+  __syncthreads();
+  float t = scratch[0];
+  for (int w = 1; w < nw; ++w) t = fmaxf(t, scratch[w]);
+  __syncthreads();
+  return t;
+}
+
+__device__ __forceinline__ float block_sum_f(float v, float* scratch) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) scratch[wid] = v;
+  __syncthreads();
+  float t = 0.f;
+  for (int w = 0; w < nw; ++w) t += scratch[w];
+  __syncthreads();
+  return t;
+}
+
+struct SmemLayout {
+  size_t nuJ, red, P0, P1, P2, P3, U, R, V, A2, A2n, LM, MU, AL, fred, ints, total;
+};
+
+__host__ __device__ inline SmemLayout smem_layout(int ccap, int s) {
+  SmemLayout L;
+  const size_t BB = (size_t)ccap * ccap, NX = 2 * (size_t)s;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 15) & ~size_t(15); return r; };
+  L.nuJ = take(BB * 8);
+  L.red = take(256 * 8);
+  L.P0 = take(BB * 4);
+  L.P1 = take(BB * 4);
+  L.P2 = take(BB * 4);
+  L.P3 = take(BB * 4);
+  L.U = take(2 * NX * ccap * 4);
+  L.R = take(4 * NX * ccap * 4);
+  L.V = take(NX * ccap * 4);
+  L.A2 = take(NX * NX * 4);
+  L.A2n = take(NX * NX * 4);
+  L.LM = take(NX * NX * 4);
+  L.MU = take(NX * NX * 4);
+  L.AL = take(NX * NX * 4);
+  L.fred = take(64 * 4);
+  L.ints = take(64 * 4);
+  L.total = o;
+  return L;
+}
+
+size_t sweep_smem_bytes(int ccap, int s) { return smem_layout(ccap, s).total; }
+
+// Final (balanced) value of every member at one box entry.  Explicit _rn
+// intrinsics: bitwise identical in the truncation and the write pass.
+// Balance (reading R8): overlap-weighted transfer
+//   v_k = parts_k + parts_k * sum_j s_kj parts_j / nu_J      (mode 1)
+// with s_dr = -f_dr/T_dr (donor d), s_rd = +f_dr/T_dr (receiver r); exact
+// fallback (mode 2) = donors scaled by f_k, pooled mass shared by g_k.
+struct BalanceCoef {
+  int mode;      // 0 identity, 1 overlap transfer, 2 proportional pooling
+  double s[4][4];
+  double f[4];
+  double g[4];
+  double c[4];
+};
+
+__device__ __noinline__ void member_values(double nuj, const float* p, int nmem,
+                                           const BalanceCoef& bc, double* out) {
+  int am = 0;
+  for (int k = 1; k < nmem; ++k)
+    if (p[k] > p[am]) am = k;
+  double parts[4];
+  double rest = 0.0;
+  for (int k = 0; k < nmem; ++k) {
+    if (k == am) continue;
+    parts[k] = __dmul_rn(nuj, (double)p[k]);
+    rest = __dadd_rn(rest, parts[k]);
+  }
+  double pa = __dsub_rn(nuj, rest);
+  parts[am] = pa > 0.0 ? pa : 0.0;
+  if (bc.mode == 1 && nuj > 0.0) {
+    for (int k = 0; k < nmem; ++k) {
+      double t = 0.0;
+      for (int j = 0; j < nmem; ++j) t = __dadd_rn(t, __dmul_rn(bc.s[k][j], parts[j]));
+      out[k] = __dadd_rn(parts[k], __dmul_rn(parts[k], __ddiv_rn(t, nuj)));
+    }
+  } else if (bc.mode == 2) {
+    double pool = 0.0;
+    for (int k = 0; k < nmem; ++k) pool = __dadd_rn(pool, __dmul_rn(bc.c[k], parts[k]));
+    for (int k = 0; k < nmem; ++k) out[k] = __dadd_rn(__dmul_rn(bc.f[k], parts[k]), __dmul_rn(bc.g[k], pool));
+  } else {
+    for (int k = 0; k < nmem; ++k) out[k] = parts[k];
+  }
+}
+
+__device__ __forceinline__ int pair_id(int a, int b) {   // a < b, 4 members -> 6 pairs
+  return a == 0 ? b - 1 : (a == 1 ? b + 1 : 5);
+}
+
+__device__ void sweep_cell(const SweepParams& p, const int J, unsigned char* smem) {
+  const int tid = threadIdx.x, T = blockDim.x;
+  const SmemLayout Ls = smem_layout(p.ccap, p.s);
+  double* nuJ = (double*)(smem + Ls.nuJ);
+  double* red = (double*)(smem + Ls.red);
+  float* P0 = (float*)(smem + Ls.P0);
+  float* P1 = (float*)(smem + Ls.P1);
+  float* P2 = (float*)(smem + Ls.P2);
+  float* P3 = (float*)(smem + Ls.P3);
+  float* Ub = (float*)(smem + Ls.U);
+  float* Rb = (float*)(smem + Ls.R);
+  float* Vb = (float*)(smem + Ls.V);
+  float* A2 = (float*)(smem + Ls.A2);
+  float* A2n = (float*)(smem + Ls.A2n);
+  float* LM = (float*)(smem + Ls.LM);
+  float* MU = (float*)(smem + Ls.MU);
+  float* AL = (float*)(smem + Ls.AL);
+  float* fred = (float*)(smem + Ls.fred);
+  int* ints = (int*)(smem + Ls.ints);
+
+  const CompCell cc = p.cells[J];
+  const int nmem = cc.nmem, n1 = cc.n1, n2 = cc.n2, s = p.s;
+  const float w = p.w;
+  const long long slot = p.slot;
+
+  // ---- member boxes and hull (a1) -------------------------------------
+  if (tid < nmem) {
+    const int i = cc.mem[tid];
+    ints[tid] = p.off_in[2 * i];
+    ints[4 + tid] = p.off_in[2 * i + 1];
+    ints[8 + tid] = p.ext_in[2 * i];
+    ints[12 + tid] = p.ext_in[2 * i + 1];
+  }
+  __syncthreads();
+  int L1 = ints[0], L2 = ints[4], U1 = ints[0] + ints[8], U2 = ints[4] + ints[12];
+  for (int k = 1; k < nmem; ++k) {
+    L1 = min(L1, ints[k]);
+    L2 = min(L2, ints[4 + k]);
+    U1 = max(U1, ints[k] + ints[8 + k]);
+    U2 = max(U2, ints[4 + k] + ints[12 + k]);
+  }
+  const int b1 = U1 - L1, b2 = U2 - L2, BB = b1 * b2;
+  // gauge origin G = L + o, o = floor((b - n)/2)
+  const int o1 = (b1 - n1) >> 1, o2 = (b2 - n2) >> 1;
+  const int G1 = L1 + o1, G2 = L2 + o2;
+
+  auto copy_unchanged = [&](int reason) {
+    for (int k = 0; k < nmem; ++k) {
+      const int i = cc.mem[k];
+      const long long len = (long long)ints[8 + k] * ints[12 + k];
+      const double* src = p.pool_in + (long long)i * slot;
+      double* dst = p.pool_out + (long long)i * slot;
+      for (long long t = tid; t < len; t += T) dst[t] = src[t];
+      if (tid == 0) {
+        p.off_out[2 * i] = ints[k];
+        p.off_out[2 * i + 1] = ints[4 + k];
+        p.ext_out[2 * i] = ints[8 + k];
+        p.ext_out[2 * i + 1] = ints[12 + k];
+      }
+    }
+    if (tid == 0) {
+      CellStats st;
+      st.iters = 0;
+      st.overflow = reason;
+      st.e0 = 0.f;
+      st.e = 0.f;
+      st.dropped = 0.0;
+      p.stats[J] = st;
+      atomicAdd(&p.totals->overflow, 1ull);
+      atomicAdd(&p.totals->cells, 1ull);
+    }
+  };
+
+  if (b1 > p.ccap || b2 > p.ccap) {
+    if (p.mode == 0) {   // defer to the large size class (second launch)
+      if (tid == 0) p.ovf_list[atomicAdd(p.ovf_count, 1)] = J;
+    } else {
+      copy_unchanged(1);
+    }
+    return;
+  }
+
+  // ---- assemble nu_J (fp64, member order) -------------------------------
+  for (int t = tid; t < BB; t += T) nuJ[t] = 0.0;
+  __syncthreads();
+  for (int k = 0; k < nmem; ++k) {
+    const int i = cc.mem[k];
+    const int e1 = ints[8 + k], e2 = ints[12 + k];
+    const int d1 = ints[k] - L1, d2 = ints[4 + k] - L2;
+    const double* src = p.pool_in + (long long)i * slot;
+    for (int t = tid; t < e1 * e2; t += T) {
+      const int r = t / e2, c = t - r * e2;
+      nuJ[(d1 + r) * b2 + d2 + c] += src[t];
+    }
+    __syncthreads();
+  }
+  double massJ_v[1] = {0.0};
+  for (int t = tid; t < BB; t += T) {
+    const double v = nuJ[t];
+    P1[t] = v > 0.0 ? (float)log2(v) : kNeg;   // log2 nu_J (zeros -> kNeg, R19)
+    massJ_v[0] += v;
+  }
+  // ---- X-block data, warm start (R7) and re-gauge ------------------------
+  const int NN = n1 * n2;
+  float amax = kNeg;
+  for (int t = tid; t < NN; t += T) {
+    const int k1 = t / n2, k2 = t - k1 * n2;
+    const long long pix = (long long)(cc.r0 + k1) * p.N2 + cc.c0 + k2;
+    float a;
+    if (p.alpha_valid) {
+      const int g1 = p.gauge[2 * J], g2 = p.gauge[2 * J + 1];
+      a = p.alpha[pix] + 2.f * w * ((float)(G1 - g1) * k1 + (float)(G2 - g2) * k2);
+    } else {
+      // first sweep: a = 0 in the global gauge (R7), i.e. A = -2 w D.kappa, D = K - G
+      a = -2.f * w * ((float)(cc.r0 - G1) * k1 + (float)(cc.c0 - G2) * k2);
+    }
+    A2[t] = a;
+    LM[t] = p.log2mu[pix];
+    MU[t] = p.mu[pix];
+    amax = fmaxf(amax, a);
+  }
+  block_sum_d<1>(massJ_v, red);
+  const double massJ = massJ_v[0];
+  amax = block_max_f(amax, fred);
+  for (int t = tid; t < NN; t += T) A2[t] -= amax;
+  double muXJ = 0.0;
+  for (int k = 0; k < nmem; ++k) muXJ += p.m[cc.mem[k]];
+  const float tolJ = (float)(p.tol * muXJ);
+  __syncthreads();
+
+  // ---- a2: separable log-domain Sinkhorn ---------------------------------
+  int it = 0;
+  float e0 = 0.f, e = 0.f;
+  bool first = true;
+  const float fo1 = (float)o1, fo2 = (float)o2;
+  for (;;) {
+    ++it;
+    for (int t = tid; t < NN; t += T) AL[t] = A2[t] + LM[t];
+    __syncthreads();
+    // Y-half stage 1: U(k1, l2) = LSE_k2 [A + log mu - w (k2 - l2~)^2]
+    for (int o = tid; o < n1 * b2; o += T) {
+      const int k1 = o / b2, l2 = o - k1 * b2;
+      const float lt = (float)l2 - fo2;
+      const float* ar = AL + k1 * n2;
+      float sh;
+      if (first) {
+        sh = kNeg;
+        for (int k2 = 0; k2 < n2; ++k2) { const float d = (float)k2 - lt; sh = fmaxf(sh, ar[k2] - w * d * d); }
+      } else {
+        sh = Ub[o];
+      }
+      float sum = 0.f;
+      for (int k2 = 0; k2 < n2; ++k2) { const float d = (float)k2 - lt; sum += ex2f(ar[k2] - w * d * d - sh); }
+      if (!(sum > 0x1p-60f && sum < 0x1p60f)) {
+        sh = kNeg;
+        for (int k2 = 0; k2 < n2; ++k2) { const float d = (float)k2 - lt; sh = fmaxf(sh, ar[k2] - w * d * d); }
+        sum = 0.f;
+        for (int k2 = 0; k2 < n2; ++k2) { const float d = (float)k2 - lt; sum += ex2f(ar[k2] - w * d * d - sh); }
+      }
+      Ub[o] = sh + lg2f(sum);
+    }
+    __syncthreads();
+    // Y-half stage 2: B(l1, l2) = -LSE_k1 [U(k1, l2) - w (k1 - l1~)^2]
+    for (int o = tid; o < BB; o += T) {
+      const int l1 = o / b2, l2 = o - l1 * b2;
+      const float lt = (float)l1 - fo1;
+      float sh;
+      if (first) {
+        sh = kNeg;
+        for (int k1 = 0; k1 < n1; ++k1) { const float d = (float)k1 - lt; sh = fmaxf(sh, Ub[k1 * b2 + l2] - w * d * d); }
+      } else {
+        sh = -P0[o];
+      }
+      float sum = 0.f;
+      for (int k1 = 0; k1 < n1; ++k1) { const float d = (float)k1 - lt; sum += ex2f(Ub[k1 * b2 + l2] - w * d * d - sh); }
+      if (!(sum > 0x1p-60f && sum < 0x1p60f)) {
+        sh = kNeg;
+        for (int k1 = 0; k1 < n1; ++k1) { const float d = (float)k1 - lt; sh = fmaxf(sh, Ub[k1 * b2 + l2] - w * d * d); }
+        sum = 0.f;
+        for (int k1 = 0; k1 < n1; ++k1) { const float d = (float)k1 - lt; sum += ex2f(Ub[k1 * b2 + l2] - w * d * d - sh); }
+      }
+      P0[o] = -(sh + lg2f(sum));
+    }
+    __syncthreads();
+    // X-half stage 1: V(l1, k2) = LSE_l2 [B + log nu_J - w (k2 - l2~)^2]
+    for (int o = tid; o < b1 * n2; o += T) {
+      const int l1 = o / n2, k2 = o - l1 * n2;
+      const float kt = (float)k2 + fo2;   // k2 - l2~ = (k2 + o2) - l2
+      const float* br = P0 + l1 * b2;
+      const float* nr = P1 + l1 * b2;
+      float sh;
+      if (first) {
+        sh = kNeg;
+        for (int l2 = 0; l2 < b2; ++l2) { const float d = kt - (float)l2; sh = fmaxf(sh, br[l2] + nr[l2] - w * d * d); }
+      } else {
+        sh = Vb[o];
+      }
+      float sum = 0.f;
+      for (int l2 = 0; l2 < b2; ++l2) { const float d = kt - (float)l2; sum += ex2f(br[l2] + nr[l2] - w * d * d - sh); }
+      if (!(sum > 0x1p-60f && sum < 0x1p60f)) {
+        sh = kNeg;
+        for (int l2 = 0; l2 < b2; ++l2) { const float d = kt - (float)l2; sh = fmaxf(sh, br[l2] + nr[l2] - w * d * d); }
+        sum = 0.f;
+        for (int l2 = 0; l2 < b2; ++l2) { const float d = kt - (float)l2; sum += ex2f(br[l2] + nr[l2] - w * d * d - sh); }
+      }
+      Vb[o] = sh + lg2f(sum);
+    }
+    __syncthreads();
+    // X-half stage 2: A'(k1, k2) = -LSE_l1 [V(l1, k2) - w (k1 - l1~)^2]
+    for (int o = tid; o < NN; o += T) {
+      const int k1 = o / n2, k2 = o - k1 * n2;
+      const float kt = (float)k1 + fo1;
+      float sh;
+      if (first) {
+        sh = kNeg;
+        for (int l1 = 0; l1 < b1; ++l1) { const float d = kt - (float)l1; sh = fmaxf(sh, Vb[l1 * n2 + k2] - w * d * d); }
+      } else {
+        sh = -A2[o];   // previous pass's A' is the current A
+      }
+      float sum = 0.f;
+      for (int l1 = 0; l1 < b1; ++l1) { const float d = kt - (float)l1; sum += ex2f(Vb[l1 * n2 + k2] - w * d * d - sh); }
+      if (!(sum > 0x1p-60f && sum < 0x1p60f)) {
+        sh = kNeg;
+        for (int l1 = 0; l1 < b1; ++l1) { const float d = kt - (float)l1; sh = fmaxf(sh, Vb[l1 * n2 + k2] - w * d * d); }
+        sum = 0.f;
+        for (int l1 = 0; l1 < b1; ++l1) { const float d = kt - (float)l1; sum += ex2f(Vb[l1 * n2 + k2] - w * d * d - sh); }
+      }
+      A2n[o] = -(sh + lg2f(sum));
+    }
+    __syncthreads();
+    // L1 X-marginal error of the plan (A, B): sum mu |1 - 2^(A - A')|
+    float part = 0.f;
+    for (int o = tid; o < NN; o += T) part += MU[o] * fabsf(exp2m1f(A2[o] - A2n[o]));
+    const float etot = block_sum_f(part, fred);
+    if (it == 1) e0 = etot;
+    e = etot;
+    const bool stop = p.fixed_iter > 0 ? (it >= p.fixed_iter) : (etot <= tolJ || it >= p.max_iter);
+    if (stop) break;
+    float* tmp = A2; A2 = A2n; A2n = tmp;   // A <- A'
+    first = false;
+  }
+  // Now A2 = plan potential, P0 = B = Y(A2), AL = A2 + log2 mu.
+
+  // ---- a3: CompositeToBasic (share form) + plan moments (R13) --------------
+  // Stage 1 split by column half h2: U_h2(k1, l2) = LSE over k2 in half h2,
+  // plus the conditional moments of x2' = x2 - (centre column of the member).
+  const int c2 = n2 / s;
+  const float cen = 0.5f * (float)(s - 1);
+  for (int o = tid; o < c2 * n1 * b2; o += T) {
+    const int h2 = o / (n1 * b2);
+    const int rem = o - h2 * n1 * b2;
+    const int k1 = rem / b2, l2 = rem - k1 * b2;
+    const float lt = (float)l2 - fo2;
+    const float* ar = AL + k1 * n2;
+    float sh = kNeg;
+    for (int k2 = h2 * s; k2 < h2 * s + s; ++k2) { const float d = (float)k2 - lt; sh = fmaxf(sh, ar[k2] - w * d * d); }
+    float sum = 0.f, m1 = 0.f, m2 = 0.f;
+    for (int k2 = h2 * s; k2 < h2 * s + s; ++k2) {
+      const float d = (float)k2 - lt;
+      const float tt = ex2f(ar[k2] - w * d * d - sh);
+      const float xq = (float)(k2 - h2 * s) - cen;
+      sum += tt;
+      m1 += tt * xq;
+      m2 += tt * xq * xq;
+    }
+    const float inv = 1.0f / sum;
+    Ub[o] = sh + lg2f(sum);
+    Rb[o] = m1 * inv;
+    Rb[c2 * n1 * b2 + o] = m2 * inv;
+  }
+  __syncthreads();
+  int mq[4];
+  for (int k = 0; k < 4; ++k) mq[k] = cc.quad[k];
+  // acc[0..3]: split masses; acc[4 + 6k + .]: M0, M1a, M1b, G0, G1, M2 of
+  // member k; acc[28 + pair]: overlaps sum parts_a parts_b / nu_J (balance)
+  double acc[34];
+  for (int k = 0; k < 34; ++k) acc[k] = 0.0;
+  for (int o = tid; o < BB; o += T) {
+    const int l1 = o / b2, l2 = o - l1 * b2;
+    const float lt = (float)l1 - fo1;
+    float S[4], Ex1[4], Ex2[4], Exx[4];
+    for (int k = 0; k < nmem; ++k) {
+      const int h1 = mq[k] >> 1, h2 = mq[k] & 1;
+      const float* ur = Ub + (h2 * n1) * b2 + l2;
+      const float* r1 = Rb + (h2 * n1) * b2 + l2;
+      const float* r2 = Rb + c2 * n1 * b2 + (h2 * n1) * b2 + l2;
+      float sh = kNeg;
+      for (int k1 = h1 * s; k1 < h1 * s + s; ++k1) { const float d = (float)k1 - lt; sh = fmaxf(sh, ur[k1 * b2] - w * d * d); }
+      float sum = 0.f, a1 = 0.f, a2 = 0.f, aq = 0.f;
+      for (int k1 = h1 * s; k1 < h1 * s + s; ++k1) {
+        const float d = (float)k1 - lt;
+        const float tt = ex2f(ur[k1 * b2] - w * d * d - sh);
+        const float xq = (float)(k1 - h1 * s) - cen;
+        sum += tt;
+        a1 += tt * xq;
+        a2 += tt * r1[k1 * b2];
+        aq += tt * (xq * xq + r2[k1 * b2]);
+      }
+      const float inv = 1.0f / sum;
+      S[k] = sh + lg2f(sum);
+      Ex1[k] = a1 * inv;
+      Ex2[k] = a2 * inv;
+      Exx[k] = aq * inv;
+    }
+    float mx = S[0];
+    for (int k = 1; k < nmem; ++k) mx = fmaxf(mx, S[k]);
+    float es[4], tot = 0.f;
+    for (int k = 0; k < nmem; ++k) { es[k] = ex2f(S[k] - mx); tot += es[k]; }
+    const float inv = 1.0f / tot;
+    float pk[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int k = 0; k < nmem; ++k) pk[k] = es[k] * inv;
+    P0[o] = pk[0];
+    P1[o] = pk[1];
+    P2[o] = pk[2];
+    P3[o] = pk[3];
+    // plan moments of the pre-balance marginals nu_k^pre = nu_J p_k (R13)
+    const double nj = nuJ[o];
+    if (nj > 0.0) {
+      for (int k = 0; k < nmem; ++k) {
+        const int h1 = mq[k] >> 1, h2 = mq[k] & 1;
+        const double v = nj * (double)pk[k];
+        const double y1 = (double)(L1 + l1 - cc.r0 - h1 * s) - (double)cen;
+        const double y2 = (double)(L2 + l2 - cc.c0 - h2 * s) - (double)cen;
+        double* a = acc + 4 + 6 * k;
+        a[0] += v;
+        a[1] += v * y1;
+        a[2] += v * y2;
+        a[3] += v * (double)Exx[k];
+        a[4] += v * (y1 * (double)Ex1[k] + y2 * (double)Ex2[k]);
+        a[5] += v * (y1 * y1 + y2 * y2);
+      }
+    }
+  }
+  __syncthreads();
+  // member masses and pairwise overlaps of the split (fp64)
+  {
+    BalanceCoef id;
+    id.mode = 0;
+    for (int o = tid; o < BB; o += T) {
+      const float pk[4] = {P0[o], P1[o], P2[o], P3[o]};
+      double v[4];
+      const double nj = nuJ[o];
+      member_values(nj, pk, nmem, id, v);
+      for (int k = 0; k < nmem; ++k) acc[k] += v[k];
+      if (nj > 0.0)
+        for (int a = 0; a < nmem; ++a)
+          for (int b = a + 1; b < nmem; ++b) acc[28 + pair_id(a, b)] += v[a] * v[b] / nj;
+    }
+  }
+  block_sum_d<34>(acc, red);
+  // ---- a4: balance coefficients (reading R8) ------------------------------
+  BalanceCoef bc;
+  {
+    double delta[4], Dsum = 0.0;
+    bool any_d = false, any_r = false;
+    bc.mode = 0;
+    for (int a = 0; a < 4; ++a) {
+      bc.f[a] = 1.0; bc.g[a] = 0.0; bc.c[a] = 0.0; delta[a] = 0.0;
+      for (int b = 0; b < 4; ++b) bc.s[a][b] = 0.0;
+    }
+    for (int k = 0; k < nmem; ++k) {
+      const double t = p.m[cc.mem[k]] * massJ / muXJ;
+      delta[k] = acc[k] - t;
+      if (delta[k] > 0) { any_d = true; Dsum += delta[k]; }
+      if (delta[k] < 0) any_r = true;
+    }
+    if (any_d && any_r) {
+      bool ok = true;
+      for (int d = 0; d < nmem && ok; ++d) {
+        if (!(delta[d] > 0)) continue;
+        double load = 0.0;
+        for (int r = 0; r < nmem; ++r) {
+          if (!(delta[r] < 0)) continue;
+          const double T = acc[28 + (d < r ? pair_id(d, r) : pair_id(r, d))];
+          const double f = delta[d] * (-delta[r]) / Dsum;
+          if (!(T > 0.0)) { ok = false; break; }
+          bc.s[d][r] = -f / T;
+          bc.s[r][d] = f / T;
+          load += f / T;
+        }
+        if (load > 1.0) ok = false;
+      }
+      if (ok) {
+        bc.mode = 1;
+      } else {
+        bc.mode = 2;
+        for (int a = 0; a < nmem; ++a) {
+          if (delta[a] > 0) { bc.f[a] = 1.0 - delta[a] / acc[a]; bc.c[a] = delta[a] / acc[a]; }
+          else if (delta[a] < 0) { bc.g[a] = -delta[a] / Dsum; }
+        }
+      }
+    }
+  }
+  // ---- a5: truncate + minimal box -----------------------------------------
+  // layout: ints[16 + 4k + 0] = min row, +1 = max row, +2 = min col, +3 = max col
+  if (tid < 4) {
+    ints[16 + 4 * tid + 0] = 1 << 30;
+    ints[16 + 4 * tid + 1] = -1;
+    ints[16 + 4 * tid + 2] = 1 << 30;
+    ints[16 + 4 * tid + 3] = -1;
+  }
+  __syncthreads();
+  double drop[1] = {0.0};
+  for (int o = tid; o < BB; o += T) {
+    const int l1 = o / b2, l2 = o - l1 * b2;
+    const float pk[4] = {P0[o], P1[o], P2[o], P3[o]};
+    double v[4];
+    member_values(nuJ[o], pk, nmem, bc, v);
+    for (int k = 0; k < nmem; ++k) {
+      if (v[k] >= p.tau) {
+        atomicMin(&ints[16 + 4 * k + 0], l1);
+        atomicMax(&ints[16 + 4 * k + 1], l1);
+        atomicMin(&ints[16 + 4 * k + 2], l2);
+        atomicMax(&ints[16 + 4 * k + 3], l2);
+      } else if (v[k] > 0.0) {
+        drop[0] += v[k];
+      }
+    }
+  }
+  block_sum_d<1>(drop, red);
+  // capacity check (uniform)
+  bool ok = true;
+  for (int k = 0; k < nmem; ++k) {
+    const int mn1 = ints[16 + 4 * k], mx1 = ints[16 + 4 * k + 1];
+    const int mn2 = ints[16 + 4 * k + 2], mx2 = ints[16 + 4 * k + 3];
+    if (mx1 < mn1 || mx2 < mn2) { ok = false; break; }   // annihilated cell
+    if ((long long)(mx1 - mn1 + 1) * (mx2 - mn2 + 1) > slot) { ok = false; break; }
+  }
+  if (!ok) {
+    copy_unchanged(2);
+    return;
+  }
+  // ---- write the new boxes -------------------------------------------------
+  unsigned long long wbytes = 0;
+  for (int k = 0; k < nmem; ++k) {
+    const int i = cc.mem[k];
+    const int mn1 = ints[16 + 4 * k], mx1 = ints[16 + 4 * k + 1];
+    const int mn2 = ints[16 + 4 * k + 2], mx2 = ints[16 + 4 * k + 3];
+    const int e1 = mx1 - mn1 + 1, e2 = mx2 - mn2 + 1;
+    double* dst = p.pool_out + (long long)i * slot;
+    for (int t = tid; t < e1 * e2; t += T) {
+      const int r = t / e2, c = t - r * e2;
+      const int o = (mn1 + r) * b2 + mn2 + c;
+      const float pk[4] = {P0[o], P1[o], P2[o], P3[o]};
+      double v[4];
+      member_values(nuJ[o], pk, nmem, bc, v);
+      dst[t] = v[k] >= p.tau ? v[k] : 0.0;
+    }
+    if (tid == 0) {
+      p.off_out[2 * i] = L1 + mn1;
+      p.off_out[2 * i + 1] = L2 + mn2;
+      p.ext_out[2 * i] = e1;
+      p.ext_out[2 * i + 1] = e2;
+      for (int q = 0; q < 6; ++q) p.mom[6 * i + q] = acc[4 + 6 * k + q];
+    }
+    wbytes += (unsigned long long)e1 * e2 * 8ull;
+  }
+  // ---- warm start store (R7) ---------------------------------------------
+  for (int t = tid; t < NN; t += T) {
+    const int k1 = t / n2, k2 = t - k1 * n2;
+    p.alpha[(long long)(cc.r0 + k1) * p.N2 + cc.c0 + k2] = A2[t];
+  }
+  if (tid == 0) {
+    p.gauge[2 * J] = G1;
+    p.gauge[2 * J + 1] = G2;
+    CellStats st;
+    st.iters = it;
+    st.overflow = 0;
+    st.e0 = e0;
+    st.e = e;
+    st.dropped = drop[0];
+    p.stats[J] = st;
+    // algorithmic MUFU count: per pass E_it + L_it (+ NN for the error)
+    const unsigned long long E_it = (unsigned long long)n1 * n2 * b2 + (unsigned long long)b1 * b2 * n1 +
+                                    (unsigned long long)b1 * n2 * b2 + (unsigned long long)n1 * n2 * b1;
+    const unsigned long long L_it = (unsigned long long)n1 * b2 + BB + (unsigned long long)b1 * n2 + NN;
+    const unsigned long long E_c2b = (unsigned long long)n1 * n2 * b2 + (unsigned long long)nmem * s * BB +
+                                     3ull * nmem * BB;
+    const unsigned long long L_c2b = (unsigned long long)c2 * n1 * b2 + (unsigned long long)nmem * BB + BB;
+    const unsigned long long mufu = (unsigned long long)it * (E_it + L_it + NN) + E_c2b + L_c2b;
+    atomicAdd(&p.totals->mufu, mufu);
+    atomicAdd(&p.cum->mufu, mufu);
+    atomicAdd(&p.cum->iters, (unsigned long long)it);
+    atomicAdd(&p.cum->cells, 1ull);
+    unsigned long long rbytes = 0;
+    for (int k = 0; k < nmem; ++k) rbytes += (unsigned long long)ints[8 + k] * ints[12 + k] * 8ull;
+    const unsigned long long byts = rbytes + wbytes + 16ull * nmem * 2 + (unsigned long long)NN * 16ull + 48ull * nmem;
+    atomicAdd(&p.totals->bytes, byts);
+    atomicAdd(&p.cum->bytes, byts);
+    atomicAdd(&p.totals->iters, (unsigned long long)it);
+    atomicAdd(&p.totals->cells, 1ull);
+    if (p.fixed_iter <= 0 && it >= p.max_iter && e > tolJ) atomicAdd(&p.totals->nonconv, 1ull);
+    atomicMax(&p.totals->iters_max, it);
+    atomicAdd(&p.totals->e0, (double)e0);
+    atomicAdd(&p.totals->e, (double)e);
+    atomicAdd(&p.totals->dropped, drop[0]);
+  }
+}
+
+__global__ void __launch_bounds__(kSweepThreads) sweep_kernel(SweepParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  if (p.mode == 0) {
+    const int J = blockIdx.x;
+    if (J < p.ncells) sweep_cell(p, J, smem);
+  } else {
+    const int n = *p.ovf_count;
+    for (int k = blockIdx.x; k < n; k += gridDim.x) {
+      sweep_cell(p, p.ovf_list[k], smem);
+      __syncthreads();
+    }
+  }
+}
+
+// Two size classes (the device-side analogue of the paper's clustering by
+// box size): pass 0 runs one CTA per composite cell with
+// shared memory for hulls <= ccap_small and queues larger cells; pass 1 runs
+// persistent CTAs with shared memory for hulls <= ccap_big over the queue.
+// No host synchronisation between the passes.
+cudaError_t launch_sweep(SweepParams p, int ccap_small, int ccap_big, cudaStream_t st) {
+  static size_t configured = 0;
+  const size_t smem0 = sweep_smem_bytes(ccap_small, p.s);
+  const size_t smem1 = sweep_smem_bytes(ccap_big, p.s);
+  const size_t need = smem0 > smem1 ? smem0 : smem1;
+  if (need > 48 * 1024 && need > configured) {
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);
+    if (e != cudaSuccess) return e;
+    configured = need;
+  }
+  cudaError_t e = cudaMemsetAsync(p.ovf_count, 0, sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  p.mode = 0;
+  p.ccap = ccap_small;
+  sweep_kernel<<<p.ncells, kSweepThreads, smem0, st>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (ccap_big > ccap_small) {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    p.mode = 1;
+    p.ccap = ccap_big;
+    sweep_kernel<<<nsm, kSweepThreads, smem1, st>>>(p);
+    e = cudaGetLastError();
+  }
+  return e;
+}
+
+}  // namespace dd

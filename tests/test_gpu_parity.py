@@ -1,0 +1,227 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the fp64 oracle on
+identical seeded inputs.  All tests need a B200."""
+import numpy as np
+import pytest
+
+import oracle as O
+from oracle.flow import check_flow
+from parity import (CONFIGS, compare_states, gpu_ctx, gpu_transport_cost, oracle_state, rel_tols)
+from synth import make_problem, random_flow, random_mcf_instance
+
+gpu = pytest.mark.gpu
+
+
+@gpu
+@pytest.mark.parametrize("cfg", ["cfg1_gm", "cfg1_gm1", "cfg1_bumps_small_eps", "cfg2_gm", "cfg2_bumps"])
+@pytest.mark.parametrize("part", ["A", "B"])
+def test_first_sweep_parity_fixed_iterations(cfg, part):
+    """One sweep from the generated coupling (identical inputs: nu_I^0 exact,
+    alpha = 0), exactly K Sinkhorn passes per cell on both sides: boxes
+    bit-exact outside the guard band, values within the fp32 tolerance."""
+    p = CONFIGS[cfg]()
+    K = 25
+    st = oracle_state(p)
+    ost = O.domdec_sweep(st, part, fixed_iter=K)
+    dd = gpu_ctx(p, fixed_iter=K)
+    gst = dd.sweep(part, stats=True)
+    assert gst["cells"] == len(ost["iters"]) and gst["iters_total"] == K * gst["cells"]
+    assert gst["overflow"] == 0
+    cmp = compare_states(dd.boxes(), st.boxes)
+    assert cmp["unexplained"] == 0, cmp
+    rb, rt = rel_tols(p.eps_prime)
+    assert cmp["rel_bulk"] < rb and cmp["rel_tail"] < rt, cmp
+    # L1 X-error of the plans and entry error (a6) agree
+    assert abs(gst["l1x_final"] - ost["e_sum"]) < 1e-6
+    assert abs(gst["l1x_entry"] - ost["e0_sum"]) < 1e-6 + 1e-4 * ost["e0_sum"]
+    ex, ey = dd.marginal_error()
+    oex, oey = O.marginal_errors(st)
+    assert abs(ex - oex) < 1e-6 and ey < 1e-12 and oey < 1e-12
+    # plan cost <c, pi> (R13) and warm-start potentials (up to constants per cell)
+    assert abs(gpu_transport_cost(dd, p.h) - O.transport_cost(st)) < 1e-5 * O.transport_cost(st)
+    a = dd.export_alpha(part)
+    comp = O.composite_partition(st.n1, st.n2, part)
+    from oracle.domdec import composite_geometry
+    for J in comp:
+        R, Cc, _ = composite_geometry(st, J)
+        oa = st.alpha[part][R, Cc]
+        oa = oa - np.sum(oa * p.mu[R, Cc]) / np.sum(p.mu[R, Cc])
+        assert np.max(np.abs(a[R, Cc] - oa)) < 2e-3
+
+
+@gpu
+@pytest.mark.parametrize("cfg,sweeps", [("cfg1_gm", 16), ("cfg2_bumps", 8), ("cfg2_gm", 8)])
+def test_pure_domdec_trajectory_parity(cfg, sweeps):
+    """Alg. 2 (A/B alternation) in parity mode: after every sweep the
+    transport cost agrees within 1e-5 relative and the L1 marginal errors
+    within 1e-6 absolute (BASELINE.json north star tolerances)."""
+    p = CONFIGS[cfg]()
+    K = 20
+    st = oracle_state(p)
+    dd = gpu_ctx(p, fixed_iter=K)
+    for k in range(sweeps):
+        part = "AB"[k % 2]
+        O.domdec_sweep(st, part, fixed_iter=K)
+        gs = dd.sweep(part, stats=True)
+        assert gs["overflow"] == 0
+        oc = O.transport_cost(st)
+        gc = gpu_transport_cost(dd, p.h)
+        assert abs(gc - oc) < 1e-5 * oc, (k, gc, oc)
+        ex, ey = dd.marginal_error()
+        oex, oey = O.marginal_errors(st)
+        assert abs(ex - oex) < 1e-6 and abs(ey - oey) < 1e-6, (k, ex, oex, ey, oey)
+    cmp = compare_states(dd.boxes(), st.boxes)
+    assert cmp["unexplained"] == 0, cmp
+
+
+@gpu
+@pytest.mark.parametrize("cfg", ["cfg1_gm", "cfg2_bumps"])
+def test_edge_costs_parity(cfg):
+    """Flow update step 1 (Eq. edge-cost, reading R13): the
+    GPU's moment form equals the oracle's direct double sums on the plans of
+    the same (parity-mode) sweep."""
+    p = CONFIGS[cfg]()
+    K = 25
+    st = oracle_state(p)
+    O.domdec_sweep(st, "A", fixed_iter=K)
+    dd = gpu_ctx(p, fixed_iter=K)
+    dd.sweep("A")
+    cbar, C, q = dd.edge_costs()
+    ocbar = O.edge_costs(st)
+    valid = ~np.isnan(ocbar)
+    assert np.array_equal(valid, ~np.isnan(cbar))
+    assert np.array_equal(q, p.supplies())
+    Q = st.last["Q"]
+    scale = 1.0 + np.abs(Q)[:, None] * np.ones((1, 5))
+    err = np.abs(cbar[valid] - ocbar[valid]) / scale[valid]
+    assert err.max() < 5e-5, err.max()
+
+
+@gpu
+@pytest.mark.parametrize("shape", [(1, 2), (2, 2), (2, 3), (3, 3), (5, 7), (8, 8), (16, 16), (32, 32), (64, 48)])
+@pytest.mark.parametrize("seed", range(3))
+def test_mincost_flow_exact(shape, seed):
+    """Flow update step 2: the GPU solver's optimal objective equals the exact
+    LP optimum (oracle) on the same integer instance, and its flow satisfies
+    both divergence constraints exactly."""
+    from paper_2405_09400_b200 import mincost_flow
+    n1, n2 = shape
+    q, C = random_mcf_instance(n1, n2, seed=1000 * seed + n1 * 31 + n2, qmax=5000, cmax=3000)
+    w, obj, st = mincost_flow(n1, n2, q, C)
+    assert check_flow(w, q, n1, n2)
+    ow, oobj = O.min_cost_flow(q, C, n1, n2)
+    assert obj == oobj == O.flow_objective(w, C)
+
+
+@gpu
+def test_mincost_flow_golden_two_node(golden):
+    from paper_2405_09400_b200 import mincost_flow
+    g = golden("mcf_2node.json")
+    w, obj, st = mincost_flow(g["n1"], g["n2"], np.array(g["q"]), np.array(g["C"]))
+    assert obj == g["objective"] and np.array_equal(w, np.array(g["w"]))
+
+
+@gpu
+def test_mincost_flow_stationary_certificate():
+    """All costs >= 0 or no negative cycle: the stationary flow is returned
+    and certified."""
+    from paper_2405_09400_b200 import mincost_flow
+    n1, n2 = 16, 16
+    q, C = random_mcf_instance(n1, n2, seed=5, qmax=100, cmax=100)
+    # potential differences + positive noise: no negative cycle, some negative arcs
+    f = np.arange(n1 * n2) % 7 * 50
+    from oracle.flow import neighbour
+    for i in range(n1 * n2):
+        for a in range(1, 5):
+            j = neighbour(i, a, n1, n2)
+            C[i, a] = (f[j] - f[i] + abs(C[i, a]) % 3) if j >= 0 else 0
+    w, obj, st = mincost_flow(n1, n2, q, C)
+    assert obj == 0 and st["stationary"] == 1 and st["certificate"] == 1
+    assert np.array_equal(w[:, 0], q) and not w[:, 1:].any()
+
+
+@gpu
+@pytest.mark.parametrize("cfg", ["cfg1_gm", "cfg2_gm", "cfg2_bumps"])
+def test_flow_apply_bit_exact(cfg):
+    """Flow update step 3 (Eq. flow-update-cell-marginals PAPER.md:453-456)
+    with a generator-made feasible flow on the generated state (identical
+    inputs): boxes bit-exact and values identical (same fp64 operation order)."""
+    p = CONFIGS[cfg]()
+    st = oracle_state(p)
+    q = p.supplies()
+    w = random_flow(q, p.n, p.n, seed=11, n_cycles=40 * p.n)
+    assert check_flow(w, q, p.n, p.n)
+    O.apply_flow(st, w, q)
+    dd = gpu_ctx(p)
+    dd.apply_flow(w)
+    gb = dd.boxes()
+    for i in range(p.n * p.n):
+        assert gb[i][0] == st.boxes[i][0] and gb[i][1] == st.boxes[i][1]
+        assert gb[i][2].shape == st.boxes[i][2].shape
+        np.testing.assert_array_max_ulp(gb[i][2], st.boxes[i][2], maxulp=4)
+
+
+@gpu
+def test_hybrid_converges_like_oracle():
+    """Alg. 3 in tolerance mode on config 1: both reach the same converged
+    transport cost (1e-5 relative) and marginal-error level (1e-6 absolute),
+    and both are within 1e-4 of the dense global optimum."""
+    p = CONFIGS["cfg1_gm"]()
+    st = oracle_state(p)
+    q = p.supplies()
+    O.run(st, q, 40, hybrid=True, err=1e-5)
+    dd = gpu_ctx(p, err=1e-5)
+    for _ in range(40):
+        dd.sweep("A")
+        dd.sweep("B")
+        dd.flow_update()
+    oc, gc = O.transport_cost(st), gpu_transport_cost(dd, p.h)
+    assert abs(gc - oc) < 1e-5 * oc
+    ex, ey = dd.marginal_error()
+    oex, oey = O.marginal_errors(st)
+    assert abs(ex - oex) < 1e-6 and abs(ey - oey) < 1e-6
+    plan, a, b, xs, ys = O.dense_sinkhorn(p.mu, p.nu, p.eps_prime, tol=1e-13)
+    N = p.N
+    from oracle.sinkhorn import sqdist
+    cstar = float(np.sum(sqdist(np.stack([xs // N, xs % N], 1), np.stack([ys // N, ys % N], 1)) * plan)) * p.h ** 2
+    assert abs(gc - cstar) < 1e-4 * cstar
+
+
+@gpu
+def test_hybrid_flow_updates_move_mass_then_stop():
+    """Four bumps with the T0 rotation (§5.2): the first flow update moves
+    mass (negative objective), later ones become stationary."""
+    p = make_problem("bumps", 32, 2, eps_factor=0.5)
+    dd = gpu_ctx(p)
+    objs = []
+    for _ in range(30):
+        dd.sweep("A")
+        dd.sweep("B")
+        objs.append(dd.flow_update(stats=True))
+    assert objs[0]["objective"] < 0 and objs[0]["changed_cells"] > 0
+    assert all(o["stationary"] for o in objs[-5:])
+
+
+@gpu
+@pytest.mark.parametrize("part", ["A", "B"])
+def test_full_size_sampled_first_sweep(part):
+    """BASELINE.json configs[3] (1024^2, s = 4, eps = (2h)^2) in the launch
+    configuration bench.py times (tolerance mode, Err = 1e-4): the GPU sweeps
+    all composite cells; the oracle recomputes a sample of cells one by one on
+    identical inputs.  Cells whose iteration count matches are compared at the
+    fp32 tolerance; the rest must agree to the Sinkhorn tolerance."""
+    p = make_problem("gm", 1024, 4, eps_factor=2.0, theta_deg=20, seed=0)
+    st = oracle_state(p)
+    comp = O.composite_partition(st.n1, st.n2, part)
+    rng = np.random.default_rng(7)
+    sample = sorted(set([0, len(comp) - 1, len(comp) // 2] + list(rng.choice(len(comp), 20, replace=False))))
+    res = O.domdec_sweep(st, part, err=1e-4, cells=sample)
+    dd = gpu_ctx(p)
+    dd.sweep(part)
+    gb = dd.boxes()
+    for k in sample:
+        r = res[k]
+        for i, ob in r["boxes"].items():
+            from parity import compare_cell
+            c = compare_cell(gb[i], ob)
+            assert c["box_equal"] or c["guard_ok"], (k, i, c)
+            assert c["rel_bulk"] < 5e-3, (k, i, c)

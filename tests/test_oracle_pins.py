@@ -163,12 +163,21 @@ def test_balance_identities():
     same = O.balance(parts, [p.sum() for p in parts])
     for a, b in zip(same, parts):
         assert np.array_equal(a, b)
-    # hand example: masses (0.6, 0.4) -> (0.5, 0.5): 0.1 moves.
+    # hand example: masses (0.6, 0.4) -> (0.5, 0.5): 0.1 moves
+    # from cell 0 to cell 1 at their shared support point.
     p0 = np.array([[0.3, 0.3]])
     p1 = np.array([[0.4, 0.0]])
     o0, o1 = O.balance([p0, p1], [0.5, 0.5])
-    np.testing.assert_allclose(o0, [[0.25, 0.25]])
-    np.testing.assert_allclose(o1, [[0.45, 0.05]])
+    np.testing.assert_allclose(o0, [[0.2, 0.3]])
+    np.testing.assert_allclose(o1, [[0.5, 0.0]])
+    # disjoint supports cannot exchange mass pointwise: the exact fallback
+    # (proportional pooling) is used
+    q0 = np.array([[0.6, 0.0]])
+    q1 = np.array([[0.0, 0.4]])
+    r0, r1 = O.balance([q0, q1], [0.5, 0.5])
+    np.testing.assert_allclose(r0 + r1, q0 + q1)
+    np.testing.assert_allclose([r0.sum(), r1.sum()], [0.5, 0.5])
+    assert (r0 >= 0).all() and (r1 >= 0).all()
 
 
 def test_truncate_box():
@@ -285,15 +294,15 @@ def test_singleton_edge_costs_reduce_to_simple_formula():
 
 def _materialise_flow_plan(st, w, q):
     """pi_hat = sum_j sum_i w_ij pi_hat_ij (Eq. flow-update-new-plan,
-    PAPER.md:425-434) with the product candidate for i != j and
-    pi_hat_ii = pi_i/m_i, as a dense matrix."""
+    PAPER.md:425-434) with the product candidate mu_j/m_j (x) nu_i/m_i,
+    nu_i = P_Y pi_i, for i != j and pi_hat_ii = pi_i/m_i, as a dense matrix."""
     N, s, n = st.N1, st.s, st.n1
     P = O.dense_state_plan(st)
     out = np.zeros_like(P)
     for i in range(n * n):
         i1, i2 = divmod(i, n)
         xi = np.array([(r) * N + c for r in range(i1 * s, (i1 + 1) * s) for c in range(i2 * s, (i2 + 1) * s)])
-        r0, c0, d = st.boxes[i]
+        r0, c0, d = st.last["nu_pre"][i]
         nu_i = np.zeros(N * N)
         nu_i[(np.arange(r0, r0 + d.shape[0])[:, None] * N + np.arange(c0, c0 + d.shape[1])[None, :]).ravel()] = d.ravel()
         for a in range(5):
