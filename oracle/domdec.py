@@ -68,17 +68,21 @@ def basic_to_composite(boxes, members):
 
 def balance(parts, targets):
     """Balance (Alg. 4 line 6; the procedure is deferred to
-    BoSch2020 §6, PAPER.md:1205 — reading R8, overlap-weighted transfer).
-    parts: list of arrays (same shape) nu_k, k in J; targets t_k with
-    sum t_k = sum ||nu_k||.  With delta_k = ||nu_k|| - t_k, donors (delta > 0)
-    send f_dr = delta_d (-delta_r) / Delta to receivers (Delta = sum of donor
-    deltas), distributed over the pixels where both are present:
-        transfer_dr(y) = f_dr / T_dr * nu_d(y) nu_r(y) / nu_J(y),
-        T_dr = sum_y nu_d(y) nu_r(y) / nu_J(y),  nu_J = sum_k nu_k.
-    Preserves sum_k nu_k pointwise, gives ||nu_k|| = t_k and keeps nu_k >= 0
-    when sum_r f_dr / T_dr <= 1 for every donor; otherwise (tiny overlaps) the
-    donors are scaled down and the pooled mass is shared in proportion to the
-    receivers' deficits (both rules exact)."""
+    BoSch2020 §6, PAPER.md:1205 — reading R8).  parts: list of arrays (same
+    shape) nu_k, k in J; targets t_k with sum t_k = sum ||nu_k||.  With
+    M_k = ||nu_k||, delta_k = M_k - t_k, donors (delta > 0) send
+    f_dr = delta_d (-delta_r) / Delta to each receiver r (Delta = sum of the
+    donor deltas), pixel by pixel:
+        tr_dr(y) = f_dr [ theta_d nu_d(y) nu_r(y) / (nu_J(y) T_dr)
+                          + (1 - theta_d) nu_d(y) / M_d ],
+        T_dr = sum_y nu_d nu_r / nu_J,  nu_J = sum_k nu_k,
+    i.e. mass moves where donor and receiver are both present (overlap
+    transfer), blended with a transfer in the donor's own shape only as much
+    as needed to stay non-negative: with L_d = sum_r f_dr / T_dr and
+    l_d = delta_d / M_d < 1, theta_d = 1 if L_d <= 1, else
+    (1 - l_d) / (L_d - l_d) (theta_d = 0 if some T_dr = 0).  The rule is
+    continuous in its inputs, preserves sum_k nu_k pointwise, gives
+    ||nu_k|| = t_k and keeps nu_k >= 0."""
     mass = np.array([p.sum() for p in parts])
     delta = mass - np.asarray(targets)
     donors = np.flatnonzero(delta > 0)
@@ -90,36 +94,22 @@ def balance(parts, targets):
     for p in parts:
         nuJ = nuJ + p
     safe = np.where(nuJ > 0, nuJ, 1.0)
-    T = {}
-    ok = True
-    for d in donors:
-        load = 0.0
-        for r in recv:
-            T[d, r] = float(np.sum(parts[d] * parts[r] / safe))
-            f = delta[d] * (-delta[r]) / D
-            if T[d, r] <= 0:
-                ok = False
-            else:
-                load += f / T[d, r]
-        if load > 1.0:
-            ok = False
     out = [p.copy() for p in parts]
-    if ok:
-        for d in donors:
-            for r in recv:
-                f = delta[d] * (-delta[r]) / D
-                tr = (f / T[d, r]) * parts[d] * parts[r] / safe
-                out[d] = out[d] - tr
-                out[r] = out[r] + tr
-        return out
-    P = np.zeros_like(parts[0])
     for d in donors:
-        P += (delta[d] / mass[d]) * parts[d]
-    for k in range(len(parts)):
-        if delta[k] > 0:
-            out[k] = parts[k] * (1.0 - delta[k] / mass[k])
-        elif delta[k] < 0:
-            out[k] = parts[k] + (-delta[k] / D) * P
+        T = {r: float(np.sum(parts[d] * parts[r] / safe)) for r in recv}
+        f = {r: delta[d] * (-delta[r]) / D for r in recv}
+        if any(T[r] <= 0 for r in recv):
+            theta = 0.0
+        else:
+            L = sum(f[r] / T[r] for r in recv)
+            l = delta[d] / mass[d]
+            theta = 1.0 if L <= 1.0 else (1.0 - l) / (L - l)
+        for r in recv:
+            tr = f[r] * (1.0 - theta) / mass[d] * parts[d]
+            if theta > 0:
+                tr = tr + f[r] * theta / T[r] * parts[d] * parts[r] / safe
+            out[d] = out[d] - tr
+            out[r] = out[r] + tr
     return out
 
 

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdomdec.so")
+LIB_PATH = os.environ.get("DOMDEC_LIB") or os.path.join(_HERE, "libdomdec.so")
 
 DD_OK, DD_ERR_ARG, DD_ERR_PRECOND, DD_ERR_NUMERIC, DD_ERR_CUDA, DD_ERR_OOM = 0, 1, 2, 3, 4, 6
 PART_A, PART_B = 0, 1

@@ -169,6 +169,10 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c) 
     c->err = "cell_size must be positive and divide N1 and N2";
     return DD_ERR_ARG;
   }
+  if (P->cell_size != 1 && P->cell_size != 2 && P->cell_size != 4 && P->cell_size != 8) {
+    c->err = "cell_size must be 1, 2, 4 or 8 in this build";
+    return DD_ERR_ARG;
+  }
   if (!(P->eps > 0) || !(P->h > 0)) {
     c->err = "eps and h must be > 0";
     return DD_ERR_ARG;

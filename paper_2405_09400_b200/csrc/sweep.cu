@@ -20,6 +20,10 @@
 // the global Y-marginal is preserved to fp64 rounding.
 #include "internal.cuh"
 
+#ifndef DD_SWEEP_MINB
+#define DD_SWEEP_MINB 4
+#endif
+
 namespace dd {
 
 __device__ __forceinline__ float ex2f(float x) {
@@ -43,21 +47,24 @@ __device__ __forceinline__ float exp2m1f(float x) {
 }
 
 // Deterministic block reductions (fixed thread->data map, fixed tree).
+// Deterministic block sum of NV doubles (fixed thread->data map, fixed tree).
+// Not unrolled on purpose: it runs once per cell and code size matters more.
 template <int NV>
-__device__ __forceinline__ void block_sum_d(double (&v)[NV], double* scratch) {
+__device__ __noinline__ void block_sum_d(double* v, double* scratch) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
+#pragma unroll 1
   for (int k = 0; k < NV; ++k) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    double x = v[k];
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    v[k] = x;
   }
   __syncthreads();
   if (lane == 0) {
-#pragma unroll
+#pragma unroll 1
     for (int k = 0; k < NV; ++k) scratch[wid * NV + k] = v[k];
   }
   __syncthreads();
-#pragma unroll
+#pragma unroll 1
   for (int k = 0; k < NV; ++k) {
     double t = 0.0;
     for (int w = 0; w < nw; ++w) t += scratch[w * NV + k];
@@ -79,17 +86,68 @@ __device__ __forceinline__ float block_max_f(float v, float* scratch) {
   return t;
 }
 
-__device__ __forceinline__ float block_sum_f(float v, float* scratch) {
+// Sum over the block; scratch must hold 2 * (blockDim / 32) floats and
+// consecutive calls must alternate 'parity' (one barrier per call).
+__device__ __forceinline__ float block_sum_f(float v, float* scratch, int parity) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  __syncthreads();
-  if (lane == 0) scratch[wid] = v;
+  float* sc = scratch + (parity & 1) * nw;
+  if (lane == 0) sc[wid] = v;
   __syncthreads();
   float t = 0.f;
-  for (int w = 0; w < nw; ++w) t += scratch[w];
-  __syncthreads();
+  for (int w = 0; w < nw; ++w) t += sc[w];
   return t;
+}
+
+
+// Warp all-reduce max.
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Transpose butterfly: reduce NV per-lane partial sums over the warp so that
+// every lane ends with the total of output xreduce_index<NV>(lane) (NV - 1 +
+// log2(32/NV) shuffles instead of 5 NV).
+template <int NV>
+__device__ __forceinline__ float xreduce(float (&v)[NV], int lane) {
+  int o = 16;
+#pragma unroll
+  for (int n = NV; n > 1; n >>= 1) {
+    const int h = n >> 1;
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const float send = up ? v[i] : v[i + h];
+      const float keep = up ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+    o >>= 1;
+  }
+  float t = v[0];
+  for (; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  return t;
+}
+
+template <int NV>
+__device__ __forceinline__ int xreduce_index(int lane) {
+  int idx = 0, o = 16;
+#pragma unroll
+  for (int n = NV; n > 1; n >>= 1) {
+    if (lane & o) idx += n >> 1;
+    o >>= 1;
+  }
+  return idx;
+}
+
+template <int NV>
+__device__ __forceinline__ bool xreduce_writer(int lane) {
+  int o = 16;
+#pragma unroll
+  for (int n = NV; n > 1; n >>= 1) o >>= 1;
+  return (lane & (2 * o - 1)) == 0;   // lowest lane of each group of equal outputs
 }
 
 struct SmemLayout {
@@ -109,7 +167,7 @@ __host__ __device__ inline SmemLayout smem_layout(int ccap, int s) {
   L.P3 = take(BB * 4);
   L.U = take(2 * NX * ccap * 4);
   L.R = take(4 * NX * ccap * 4);
-  L.V = take(NX * ccap * 4);
+  L.V = take(2 * NX * ccap * 4);
   L.A2 = take(NX * NX * 4);
   L.A2n = take(NX * NX * 4);
   L.LM = take(NX * NX * 4);
@@ -125,44 +183,51 @@ size_t sweep_smem_bytes(int ccap, int s) { return smem_layout(ccap, s).total; }
 
 // Final (balanced) value of every member at one box entry.  Explicit _rn
 // intrinsics: bitwise identical in the truncation and the write pass.
-// Balance (reading R8): overlap-weighted transfer
-//   v_k = parts_k + parts_k * sum_j s_kj parts_j / nu_J      (mode 1)
-// with s_dr = -f_dr/T_dr (donor d), s_rd = +f_dr/T_dr (receiver r); exact
-// fallback (mode 2) = donors scaled by f_k, pooled mass shared by g_k.
+// Balance (reading R8): blended overlap / own-shape transfer
+//   v_k = parts_k + parts_k * (sum_j O_kj parts_j) / nu_J + sum_j P_kj parts_j
+// (O: overlap-transfer coefficients f theta / T, P: own-shape coefficients
+// f (1 - theta) / M_d; see oracle/domdec.py:balance for the definition).
 struct BalanceCoef {
-  int mode;      // 0 identity, 1 overlap transfer, 2 proportional pooling
-  double s[4][4];
-  double f[4];
-  double g[4];
-  double c[4];
+  int active;
+  double O[4][4];
+  double P[4][4];
 };
 
-__device__ __noinline__ void member_values(double nuj, const float* p, int nmem,
-                                           const BalanceCoef& bc, double* out) {
+__device__ __forceinline__ void member_values(double nuj, const float* p, int nmem,
+                                              const BalanceCoef& bc, double* out) {
   int am = 0;
-  for (int k = 1; k < nmem; ++k)
-    if (p[k] > p[am]) am = k;
+#pragma unroll
+  for (int k = 1; k < 4; ++k)
+    if (k < nmem && p[k] > p[am]) am = k;
   double parts[4];
   double rest = 0.0;
-  for (int k = 0; k < nmem; ++k) {
-    if (k == am) continue;
-    parts[k] = __dmul_rn(nuj, (double)p[k]);
-    rest = __dadd_rn(rest, parts[k]);
-  }
-  double pa = __dsub_rn(nuj, rest);
-  parts[am] = pa > 0.0 ? pa : 0.0;
-  if (bc.mode == 1 && nuj > 0.0) {
-    for (int k = 0; k < nmem; ++k) {
-      double t = 0.0;
-      for (int j = 0; j < nmem; ++j) t = __dadd_rn(t, __dmul_rn(bc.s[k][j], parts[j]));
-      out[k] = __dadd_rn(parts[k], __dmul_rn(parts[k], __ddiv_rn(t, nuj)));
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    parts[k] = 0.0;
+    if (k < nmem && k != am) {
+      parts[k] = __dmul_rn(nuj, (double)p[k]);
+      rest = __dadd_rn(rest, parts[k]);
     }
-  } else if (bc.mode == 2) {
-    double pool = 0.0;
-    for (int k = 0; k < nmem; ++k) pool = __dadd_rn(pool, __dmul_rn(bc.c[k], parts[k]));
-    for (int k = 0; k < nmem; ++k) out[k] = __dadd_rn(__dmul_rn(bc.f[k], parts[k]), __dmul_rn(bc.g[k], pool));
+  }
+  const double pa = __dsub_rn(nuj, rest);
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (k == am) parts[k] = pa > 0.0 ? pa : 0.0;
+  if (bc.active && nuj > 0.0) {
+    const double inv = __drcp_rn(nuj);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      double t = 0.0, u = 0.0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        t = __dadd_rn(t, __dmul_rn(bc.O[k][j], parts[j]));
+        u = __dadd_rn(u, __dmul_rn(bc.P[k][j], parts[j]));
+      }
+      out[k] = __dadd_rn(__dadd_rn(parts[k], __dmul_rn(parts[k], __dmul_rn(t, inv))), u);
+    }
   } else {
-    for (int k = 0; k < nmem; ++k) out[k] = parts[k];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) out[k] = parts[k];
   }
 }
 
@@ -170,6 +235,7 @@ __device__ __forceinline__ int pair_id(int a, int b) {   // a < b, 4 members -> 
   return a == 0 ? b - 1 : (a == 1 ? b + 1 : 5);
 }
 
+template <int NX>
 __device__ void sweep_cell(const SweepParams& p, const int J, unsigned char* smem) {
   const int tid = threadIdx.x, T = blockDim.x;
   const SmemLayout Ls = smem_layout(p.ccap, p.s);
@@ -269,141 +335,290 @@ __device__ void sweep_cell(const SweepParams& p, const int J, unsigned char* sme
   double massJ_v[1] = {0.0};
   for (int t = tid; t < BB; t += T) {
     const double v = nuJ[t];
-    P1[t] = v > 0.0 ? (float)log2(v) : kNeg;   // log2 nu_J (zeros -> kNeg, R19)
+    P1[t] = v > 0.0 ? lg2f((float)v) : kNeg;   // log2 nu_J (zeros -> kNeg, R19)
     massJ_v[0] += v;
   }
   // ---- X-block data, warm start (R7) and re-gauge ------------------------
+  // The X-block is padded to NX x NX (ragged B cells have n = s on an axis);
+  // padded pixels carry log2 mu = kNeg, so their terms vanish.
   const int NN = n1 * n2;
+  constexpr int NXX = NX * NX;
   float amax = kNeg;
-  for (int t = tid; t < NN; t += T) {
-    const int k1 = t / n2, k2 = t - k1 * n2;
-    const long long pix = (long long)(cc.r0 + k1) * p.N2 + cc.c0 + k2;
-    float a;
-    if (p.alpha_valid) {
-      const int g1 = p.gauge[2 * J], g2 = p.gauge[2 * J + 1];
-      a = p.alpha[pix] + 2.f * w * ((float)(G1 - g1) * k1 + (float)(G2 - g2) * k2);
-    } else {
-      // first sweep: a = 0 in the global gauge (R7), i.e. A = -2 w D.kappa, D = K - G
-      a = -2.f * w * ((float)(cc.r0 - G1) * k1 + (float)(cc.c0 - G2) * k2);
+  for (int t = tid; t < NXX; t += T) {
+    const int k1 = t / NX, k2 = t % NX;
+    float a = 0.f, lm = kNeg, mu = 0.f;
+    if (k1 < n1 && k2 < n2) {
+      const long long pix = (long long)(cc.r0 + k1) * p.N2 + cc.c0 + k2;
+      if (p.alpha_valid) {
+        const int g1 = p.gauge[2 * J], g2 = p.gauge[2 * J + 1];
+        a = p.alpha[pix] + 2.f * w * ((float)(G1 - g1) * k1 + (float)(G2 - g2) * k2);
+      } else {
+        // first sweep: a = 0 in the global gauge (R7), i.e. A = -2 w D.kappa, D = K - G
+        a = -2.f * w * ((float)(cc.r0 - G1) * k1 + (float)(cc.c0 - G2) * k2);
+      }
+      lm = p.log2mu[pix];
+      mu = p.mu[pix];
+      amax = fmaxf(amax, a);
     }
     A2[t] = a;
-    LM[t] = p.log2mu[pix];
-    MU[t] = p.mu[pix];
-    amax = fmaxf(amax, a);
+    LM[t] = lm;
+    MU[t] = mu;
   }
   block_sum_d<1>(massJ_v, red);
   const double massJ = massJ_v[0];
   amax = block_max_f(amax, fred);
-  for (int t = tid; t < NN; t += T) A2[t] -= amax;
+  for (int t = tid; t < NXX; t += T) {
+    A2[t] -= amax;
+    AL[t] = A2[t] + LM[t] - w * (float)((t % NX) * (t % NX));   // AK of the first pass
+  }
   double muXJ = 0.0;
-  for (int k = 0; k < nmem; ++k) muXJ += p.m[cc.mem[k]];
+  for (int q = 0; q < nmem; ++q) muXJ += p.m[cc.mem[q]];
   const float tolJ = (float)(p.tol * muXJ);
   __syncthreads();
 
   // ---- a2: separable log-domain Sinkhorn ---------------------------------
+  // Every term of every 1-D LSE stage is evaluated as
+  //     z = fma(g, x, a) - c,   sum += ex2(z)
+  // by expanding -w (k - l)^2 = -w k^2 + 2 w k l - w l^2, folding the
+  // input-only part into a precomputed array (AK = AL, UK, BK, VK) and the
+  // output-only part into the shift c.  After the first pass the shift is the
+  // previous iterate of the same output.  Threads
+  // own outputs; the long-axis stages (X1, X2) give each thread two outputs
+  // that share every loaded input (two ex2 per shared-memory load), X2 also
+  // splits its terms over SX lanes.  ~5 instructions per ex2.
   int it = 0;
   float e0 = 0.f, e = 0.f;
   bool first = true;
+  float* UK = Rb;                     // [NX][b2]  U - w k1^2   (Rb is free during the loop)
+  float* VK = Vb + NX * p.ccap;       // [b1][NX]  V - w l1^2
+  float* BK = P2;                     // [b1][b2]  B + log2 nu_J - w l2^2
+  const float w2 = 2.f * w;
   const float fo1 = (float)o1, fo2 = (float)o2;
+  constexpr int HX = NX / 2;
+  // Y2 mapping: thread -> (column l2, row group rg of RG)
+  const int RG = max(1, T / b2);
+  const int y2_col = tid % b2, y2_rg = tid / b2;
+  // X2 mapping: thread -> (pair qa in [0, HX), column k2, split h of SX)
+  constexpr int SX = (kSweepThreads / (HX * NX)) > 8 ? 8 : (kSweepThreads / (HX * NX));
+  const int x2_h = tid % SX, x2_pair = tid / SX;
+  const int x2_k2 = x2_pair % NX, x2_qa = x2_pair / NX;
+  const bool x2_valid = x2_pair < HX * NX;
   for (;;) {
     ++it;
-    for (int t = tid; t < NN; t += T) AL[t] = A2[t] + LM[t];
-    __syncthreads();
-    // Y-half stage 1: U(k1, l2) = LSE_k2 [A + log mu - w (k2 - l2~)^2]
-    for (int o = tid; o < n1 * b2; o += T) {
-      const int k1 = o / b2, l2 = o - k1 * b2;
-      const float lt = (float)l2 - fo2;
-      const float* ar = AL + k1 * n2;
-      float sh;
+    // Y-half stage 1: U(k1, l2) = LSE_k2 [A + log2 mu - w (k2 - l2~)^2]
+    for (int o = tid, k1 = tid / b2, l2 = tid % b2; o < NX * b2;
+         o += T, k1 += T / b2, l2 += T % b2, (l2 >= b2 ? (l2 -= b2, ++k1) : 0)) {
+      const float x = (float)l2 - fo2;
+      const float* ar = AL + k1 * NX;
+      float a[NX];
+#pragma unroll
+      for (int q = 0; q < NX; ++q) a[q] = ar[q];
+      float c;
       if (first) {
-        sh = kNeg;
-        for (int k2 = 0; k2 < n2; ++k2) { const float d = (float)k2 - lt; sh = fmaxf(sh, ar[k2] - w * d * d); }
+        c = kNeg;
+#pragma unroll
+        for (int q = 0; q < NX; ++q) c = fmaxf(c, fmaf(w2 * (float)q, x, a[q]));
       } else {
-        sh = Ub[o];
+        c = Ub[o] + w * x * x;
       }
       float sum = 0.f;
-      for (int k2 = 0; k2 < n2; ++k2) { const float d = (float)k2 - lt; sum += ex2f(ar[k2] - w * d * d - sh); }
+#pragma unroll
+      for (int q = 0; q < NX; ++q) sum += ex2f(fmaf(w2 * (float)q, x, a[q]) - c);
       if (!(sum > 0x1p-60f && sum < 0x1p60f)) {
-        sh = kNeg;
-        for (int k2 = 0; k2 < n2; ++k2) { const float d = (float)k2 - lt; sh = fmaxf(sh, ar[k2] - w * d * d); }
+        c = kNeg;
+        for (int q = 0; q < NX; ++q) c = fmaxf(c, fmaf(w2 * (float)q, x, a[q]));
         sum = 0.f;
-        for (int k2 = 0; k2 < n2; ++k2) { const float d = (float)k2 - lt; sum += ex2f(ar[k2] - w * d * d - sh); }
+        for (int q = 0; q < NX; ++q) sum += ex2f(fmaf(w2 * (float)q, x, a[q]) - c);
       }
-      Ub[o] = sh + lg2f(sum);
+      const float U = c + lg2f(sum) - w * x * x;
+      Ub[o] = U;
+      UK[o] = U - w * (float)(k1 * k1);
     }
     __syncthreads();
     // Y-half stage 2: B(l1, l2) = -LSE_k1 [U(k1, l2) - w (k1 - l1~)^2]
-    for (int o = tid; o < BB; o += T) {
-      const int l1 = o / b2, l2 = o - l1 * b2;
-      const float lt = (float)l1 - fo1;
-      float sh;
-      if (first) {
-        sh = kNeg;
-        for (int k1 = 0; k1 < n1; ++k1) { const float d = (float)k1 - lt; sh = fmaxf(sh, Ub[k1 * b2 + l2] - w * d * d); }
-      } else {
-        sh = -P0[o];
+    if (y2_rg < RG) {
+      const int l2 = y2_col;
+      float u[NX];
+#pragma unroll
+      for (int q = 0; q < NX; ++q) u[q] = UK[q * b2 + l2];
+      const float wl2 = w * (float)(l2 * l2);
+      for (int l1 = y2_rg; l1 < b1; l1 += RG) {
+        const int o = l1 * b2 + l2;
+        const float x = (float)l1 - fo1;
+        float c;
+        if (first) {
+          c = kNeg;
+#pragma unroll
+          for (int q = 0; q < NX; ++q) c = fmaxf(c, fmaf(w2 * (float)q, x, u[q]));
+        } else {
+          c = -P0[o] + w * x * x;
+        }
+        float sum = 0.f;
+#pragma unroll
+        for (int q = 0; q < NX; ++q) sum += ex2f(fmaf(w2 * (float)q, x, u[q]) - c);
+        if (!(sum > 0x1p-60f && sum < 0x1p60f)) {
+          c = kNeg;
+          for (int q = 0; q < NX; ++q) c = fmaxf(c, fmaf(w2 * (float)q, x, u[q]));
+          sum = 0.f;
+          for (int q = 0; q < NX; ++q) sum += ex2f(fmaf(w2 * (float)q, x, u[q]) - c);
+        }
+        const float Bv = -(c + lg2f(sum) - w * x * x);
+        P0[o] = Bv;
+        BK[o] = Bv + P1[o] - wl2;
       }
-      float sum = 0.f;
-      for (int k1 = 0; k1 < n1; ++k1) { const float d = (float)k1 - lt; sum += ex2f(Ub[k1 * b2 + l2] - w * d * d - sh); }
-      if (!(sum > 0x1p-60f && sum < 0x1p60f)) {
-        sh = kNeg;
-        for (int k1 = 0; k1 < n1; ++k1) { const float d = (float)k1 - lt; sh = fmaxf(sh, Ub[k1 * b2 + l2] - w * d * d); }
-        sum = 0.f;
-        for (int k1 = 0; k1 < n1; ++k1) { const float d = (float)k1 - lt; sum += ex2f(Ub[k1 * b2 + l2] - w * d * d - sh); }
-      }
-      P0[o] = -(sh + lg2f(sum));
     }
     __syncthreads();
-    // X-half stage 1: V(l1, k2) = LSE_l2 [B + log nu_J - w (k2 - l2~)^2]
-    for (int o = tid; o < b1 * n2; o += T) {
-      const int l1 = o / n2, k2 = o - l1 * n2;
-      const float kt = (float)k2 + fo2;   // k2 - l2~ = (k2 + o2) - l2
-      const float* br = P0 + l1 * b2;
-      const float* nr = P1 + l1 * b2;
-      float sh;
+    // X-half stage 1: V(l1, k2) = LSE_l2 [B + log2 nu_J - w (k2 - l2~)^2],
+    // two outputs (k2 = qa, qa + HX) per thread sharing the loaded BK
+    for (int t = tid; t < b1 * HX; t += T) {
+      const int l1 = t / HX, qa = t % HX, qb = qa + HX;
+      const float kta = (float)qa + fo2, ktb = (float)qb + fo2;   // k2 - l2~ = kt - l2
+      const float ga = w2 * kta, gb = w2 * ktb;
+      const float* br = BK + l1 * b2;
+      float ca, cb;
       if (first) {
-        sh = kNeg;
-        for (int l2 = 0; l2 < b2; ++l2) { const float d = kt - (float)l2; sh = fmaxf(sh, br[l2] + nr[l2] - w * d * d); }
+        ca = kNeg;
+        cb = kNeg;
+        float lf = 0.f;
+        for (int l2 = 0; l2 < b2; ++l2, lf += 1.f) {
+          const float bk = br[l2];
+          ca = fmaxf(ca, fmaf(ga, lf, bk));
+          cb = fmaxf(cb, fmaf(gb, lf, bk));
+        }
       } else {
-        sh = Vb[o];
+        ca = Vb[l1 * NX + qa] + w * kta * kta;
+        cb = Vb[l1 * NX + qb] + w * ktb * ktb;
       }
-      float sum = 0.f;
-      for (int l2 = 0; l2 < b2; ++l2) { const float d = kt - (float)l2; sum += ex2f(br[l2] + nr[l2] - w * d * d - sh); }
-      if (!(sum > 0x1p-60f && sum < 0x1p60f)) {
-        sh = kNeg;
-        for (int l2 = 0; l2 < b2; ++l2) { const float d = kt - (float)l2; sh = fmaxf(sh, br[l2] + nr[l2] - w * d * d); }
-        sum = 0.f;
-        for (int l2 = 0; l2 < b2; ++l2) { const float d = kt - (float)l2; sum += ex2f(br[l2] + nr[l2] - w * d * d - sh); }
+      float sa = 0.f, sb = 0.f, sa1 = 0.f, sb1 = 0.f;
+      float lf = 0.f;
+      int l2 = 0;
+      for (; l2 + 1 < b2; l2 += 2, lf += 2.f) {
+        const float bk0 = br[l2], bk1 = br[l2 + 1];
+        sa += ex2f(fmaf(ga, lf, bk0) - ca);
+        sb += ex2f(fmaf(gb, lf, bk0) - cb);
+        sa1 += ex2f(fmaf(ga, lf + 1.f, bk1) - ca);
+        sb1 += ex2f(fmaf(gb, lf + 1.f, bk1) - cb);
       }
-      Vb[o] = sh + lg2f(sum);
+      if (l2 < b2) {
+        const float bk0 = br[l2];
+        sa += ex2f(fmaf(ga, lf, bk0) - ca);
+        sb += ex2f(fmaf(gb, lf, bk0) - cb);
+      }
+      sa += sa1;
+      sb += sb1;
+      if (!(sa > 0x1p-60f && sa < 0x1p60f) || !(sb > 0x1p-60f && sb < 0x1p60f)) {
+        ca = kNeg;
+        cb = kNeg;
+        float lg = 0.f;
+        for (int q = 0; q < b2; ++q, lg += 1.f) {
+          ca = fmaxf(ca, fmaf(ga, lg, br[q]));
+          cb = fmaxf(cb, fmaf(gb, lg, br[q]));
+        }
+        sa = 0.f;
+        sb = 0.f;
+        lg = 0.f;
+        for (int q = 0; q < b2; ++q, lg += 1.f) {
+          sa += ex2f(fmaf(ga, lg, br[q]) - ca);
+          sb += ex2f(fmaf(gb, lg, br[q]) - cb);
+        }
+      }
+      const float Va = ca + lg2f(sa) - w * kta * kta;
+      const float Vbv = cb + lg2f(sb) - w * ktb * ktb;
+      const float wl1 = w * (float)(l1 * l1);
+      Vb[l1 * NX + qa] = Va;
+      Vb[l1 * NX + qb] = Vbv;
+      VK[l1 * NX + qa] = Va - wl1;
+      VK[l1 * NX + qb] = Vbv - wl1;
     }
     __syncthreads();
-    // X-half stage 2: A'(k1, k2) = -LSE_l1 [V(l1, k2) - w (k1 - l1~)^2]
-    for (int o = tid; o < NN; o += T) {
-      const int k1 = o / n2, k2 = o - k1 * n2;
-      const float kt = (float)k1 + fo1;
-      float sh;
+    // X-half stage 2: A'(k1, k2) = -LSE_l1 [V(l1, k2) - w (k1 - l1~)^2],
+    // two outputs (k1 = qa, qa + HX) per thread, terms split over SX lanes
+    float epart = 0.f;
+    {
+      const int qa = x2_qa, qb = qa + HX, k2 = x2_k2;
+      const float kta = (float)qa + fo1, ktb = (float)qb + fo1;
+      const float ga = w2 * kta, gb = w2 * ktb;
+      float ca = 0.f, cb = 0.f;
       if (first) {
-        sh = kNeg;
-        for (int l1 = 0; l1 < b1; ++l1) { const float d = kt - (float)l1; sh = fmaxf(sh, Vb[l1 * n2 + k2] - w * d * d); }
-      } else {
-        sh = -A2[o];   // previous pass's A' is the current A
+        ca = kNeg;
+        cb = kNeg;
+        if (x2_valid) {
+          float lf = (float)x2_h;
+          for (int l1 = x2_h; l1 < b1; l1 += SX, lf += (float)SX) {
+            const float vk = VK[l1 * NX + k2];
+            ca = fmaxf(ca, fmaf(ga, lf, vk));
+            cb = fmaxf(cb, fmaf(gb, lf, vk));
+          }
+        }
+#pragma unroll
+        for (int off = SX >> 1; off > 0; off >>= 1) {
+          ca = fmaxf(ca, __shfl_xor_sync(0xffffffffu, ca, off));
+          cb = fmaxf(cb, __shfl_xor_sync(0xffffffffu, cb, off));
+        }
+      } else if (x2_valid) {
+        ca = -A2[qa * NX + k2] + w * kta * kta;
+        cb = -A2[qb * NX + k2] + w * ktb * ktb;
       }
-      float sum = 0.f;
-      for (int l1 = 0; l1 < b1; ++l1) { const float d = kt - (float)l1; sum += ex2f(Vb[l1 * n2 + k2] - w * d * d - sh); }
-      if (!(sum > 0x1p-60f && sum < 0x1p60f)) {
-        sh = kNeg;
-        for (int l1 = 0; l1 < b1; ++l1) { const float d = kt - (float)l1; sh = fmaxf(sh, Vb[l1 * n2 + k2] - w * d * d); }
-        sum = 0.f;
-        for (int l1 = 0; l1 < b1; ++l1) { const float d = kt - (float)l1; sum += ex2f(Vb[l1 * n2 + k2] - w * d * d - sh); }
+      float sa = 0.f, sb = 0.f;
+      if (x2_valid) {
+        float lf = (float)x2_h;
+        for (int l1 = x2_h; l1 < b1; l1 += SX, lf += (float)SX) {
+          const float vk = VK[l1 * NX + k2];
+          sa += ex2f(fmaf(ga, lf, vk) - ca);
+          sb += ex2f(fmaf(gb, lf, vk) - cb);
+        }
       }
-      A2n[o] = -(sh + lg2f(sum));
+#pragma unroll
+      for (int off = SX >> 1; off > 0; off >>= 1) {
+        sa += __shfl_xor_sync(0xffffffffu, sa, off);
+        sb += __shfl_xor_sync(0xffffffffu, sb, off);
+      }
+      const bool bad = x2_valid && (!(sa > 0x1p-60f && sa < 0x1p60f) || !(sb > 0x1p-60f && sb < 0x1p60f));
+      if (__any_sync(0xffffffffu, bad)) {
+        float ma = kNeg, mb = kNeg;
+        if (x2_valid) {
+          float lf = (float)x2_h;
+          for (int l1 = x2_h; l1 < b1; l1 += SX, lf += (float)SX) {
+            const float vk = VK[l1 * NX + k2];
+            ma = fmaxf(ma, fmaf(ga, lf, vk));
+            mb = fmaxf(mb, fmaf(gb, lf, vk));
+          }
+        }
+#pragma unroll
+        for (int off = SX >> 1; off > 0; off >>= 1) {
+          ma = fmaxf(ma, __shfl_xor_sync(0xffffffffu, ma, off));
+          mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, off));
+        }
+        float ta = 0.f, tb = 0.f;
+        if (x2_valid) {
+          float lf = (float)x2_h;
+          for (int l1 = x2_h; l1 < b1; l1 += SX, lf += (float)SX) {
+            const float vk = VK[l1 * NX + k2];
+            ta += ex2f(fmaf(ga, lf, vk) - ma);
+            tb += ex2f(fmaf(gb, lf, vk) - mb);
+          }
+        }
+#pragma unroll
+        for (int off = SX >> 1; off > 0; off >>= 1) {
+          ta += __shfl_xor_sync(0xffffffffu, ta, off);
+          tb += __shfl_xor_sync(0xffffffffu, tb, off);
+        }
+        if (bad) { ca = ma; cb = mb; sa = ta; sb = tb; }
+      }
+      if (x2_valid && x2_h == 0) {
+        const float wk2 = w * (float)(k2 * k2);
+        const int oa = qa * NX + k2, ob = qb * NX + k2;
+        const float ana = -(ca + lg2f(sa) - w * kta * kta);
+        const float anb = -(cb + lg2f(sb) - w * ktb * ktb);
+        A2n[oa] = ana;
+        A2n[ob] = anb;
+        // L1 X-marginal error of the plan (A, B): sum mu |1 - 2^(A - A')|
+        epart += MU[oa] * fabsf(exp2m1f(A2[oa] - ana)) + MU[ob] * fabsf(exp2m1f(A2[ob] - anb));
+        AL[oa] = ana + LM[oa] - wk2;   // AK of the next pass
+        AL[ob] = anb + LM[ob] - wk2;
+      }
     }
-    __syncthreads();
-    // L1 X-marginal error of the plan (A, B): sum mu |1 - 2^(A - A')|
-    float part = 0.f;
-    for (int o = tid; o < NN; o += T) part += MU[o] * fabsf(exp2m1f(A2[o] - A2n[o]));
-    const float etot = block_sum_f(part, fred);
+    const float etot = block_sum_f(epart, fred, it);
     if (it == 1) e0 = etot;
     e = etot;
     const bool stop = p.fixed_iter > 0 ? (it >= p.fixed_iter) : (etot <= tolJ || it >= p.max_iter);
@@ -411,8 +626,8 @@ __device__ void sweep_cell(const SweepParams& p, const int J, unsigned char* sme
     float* tmp = A2; A2 = A2n; A2n = tmp;   // A <- A'
     first = false;
   }
-  // Now A2 = plan potential, P0 = B = Y(A2), AL = A2 + log2 mu.
-
+  for (int t = tid; t < NXX; t += T) AL[t] = A2[t] + LM[t];
+  __syncthreads();
   // ---- a3: CompositeToBasic (share form) + plan moments (R13) --------------
   // Stage 1 split by column half h2: U_h2(k1, l2) = LSE over k2 in half h2,
   // plus the conditional moments of x2' = x2 - (centre column of the member).
@@ -423,7 +638,7 @@ __device__ void sweep_cell(const SweepParams& p, const int J, unsigned char* sme
     const int rem = o - h2 * n1 * b2;
     const int k1 = rem / b2, l2 = rem - k1 * b2;
     const float lt = (float)l2 - fo2;
-    const float* ar = AL + k1 * n2;
+    const float* ar = AL + k1 * NX;
     float sh = kNeg;
     for (int k2 = h2 * s; k2 < h2 * s + s; ++k2) { const float d = (float)k2 - lt; sh = fmaxf(sh, ar[k2] - w * d * d); }
     float sum = 0.f, m1 = 0.f, m2 = 0.f;
@@ -485,8 +700,30 @@ __device__ void sweep_cell(const SweepParams& p, const int J, unsigned char* sme
     P1[o] = pk[1];
     P2[o] = pk[2];
     P3[o] = pk[3];
-    // plan moments of the pre-balance marginals nu_k^pre = nu_J p_k (R13)
+    // split masses and pairwise overlaps (balance, R8) of nu_k = nu_J p_k
     const double nj = nuJ[o];
+    if (nj > 0.0) {
+      // identity split: the largest share takes the remainder (exact sum)
+      double v[4];
+      {
+        int am = 0;
+        for (int q = 1; q < nmem; ++q)
+          if (pk[q] > pk[am]) am = q;
+        double rest = 0.0;
+        for (int q = 0; q < nmem; ++q) {
+          v[q] = 0.0;
+          if (q != am) { v[q] = __dmul_rn(nj, (double)pk[q]); rest = __dadd_rn(rest, v[q]); }
+        }
+        const double pa = __dsub_rn(nj, rest);
+        v[am] = pa > 0.0 ? pa : 0.0;
+      }
+      const double inv = 1.0 / nj;
+      for (int a = 0; a < nmem; ++a) {
+        acc[a] += v[a];
+        for (int b = a + 1; b < nmem; ++b) acc[28 + pair_id(a, b)] += v[a] * v[b] * inv;
+      }
+    }
+    // plan moments of the pre-balance marginals nu_k^pre = nu_J p_k (R13)
     if (nj > 0.0) {
       for (int k = 0; k < nmem; ++k) {
         const int h1 = mq[k] >> 1, h2 = mq[k] & 1;
@@ -504,61 +741,49 @@ __device__ void sweep_cell(const SweepParams& p, const int J, unsigned char* sme
     }
   }
   __syncthreads();
-  // member masses and pairwise overlaps of the split (fp64)
-  {
-    BalanceCoef id;
-    id.mode = 0;
-    for (int o = tid; o < BB; o += T) {
-      const float pk[4] = {P0[o], P1[o], P2[o], P3[o]};
-      double v[4];
-      const double nj = nuJ[o];
-      member_values(nj, pk, nmem, id, v);
-      for (int k = 0; k < nmem; ++k) acc[k] += v[k];
-      if (nj > 0.0)
-        for (int a = 0; a < nmem; ++a)
-          for (int b = a + 1; b < nmem; ++b) acc[28 + pair_id(a, b)] += v[a] * v[b] / nj;
-    }
-  }
   block_sum_d<34>(acc, red);
   // ---- a4: balance coefficients (reading R8) ------------------------------
   BalanceCoef bc;
   {
     double delta[4], Dsum = 0.0;
     bool any_d = false, any_r = false;
-    bc.mode = 0;
+    bc.active = 0;
     for (int a = 0; a < 4; ++a) {
-      bc.f[a] = 1.0; bc.g[a] = 0.0; bc.c[a] = 0.0; delta[a] = 0.0;
-      for (int b = 0; b < 4; ++b) bc.s[a][b] = 0.0;
+      delta[a] = 0.0;
+      for (int b = 0; b < 4; ++b) { bc.O[a][b] = 0.0; bc.P[a][b] = 0.0; }
     }
-    for (int k = 0; k < nmem; ++k) {
-      const double t = p.m[cc.mem[k]] * massJ / muXJ;
-      delta[k] = acc[k] - t;
-      if (delta[k] > 0) { any_d = true; Dsum += delta[k]; }
-      if (delta[k] < 0) any_r = true;
+    for (int q = 0; q < nmem; ++q) {
+      const double t = p.m[cc.mem[q]] * massJ / muXJ;
+      delta[q] = acc[q] - t;
+      if (delta[q] > 0) { any_d = true; Dsum += delta[q]; }
+      if (delta[q] < 0) any_r = true;
     }
     if (any_d && any_r) {
-      bool ok = true;
-      for (int d = 0; d < nmem && ok; ++d) {
+      bc.active = 1;
+      for (int d = 0; d < nmem; ++d) {
         if (!(delta[d] > 0)) continue;
-        double load = 0.0;
+        bool zeroT = false;
+        double L = 0.0;
         for (int r = 0; r < nmem; ++r) {
           if (!(delta[r] < 0)) continue;
           const double T = acc[28 + (d < r ? pair_id(d, r) : pair_id(r, d))];
-          const double f = delta[d] * (-delta[r]) / Dsum;
-          if (!(T > 0.0)) { ok = false; break; }
-          bc.s[d][r] = -f / T;
-          bc.s[r][d] = f / T;
-          load += f / T;
+          if (!(T > 0.0)) { zeroT = true; continue; }
+          L += delta[d] * (-delta[r]) / Dsum / T;
         }
-        if (load > 1.0) ok = false;
-      }
-      if (ok) {
-        bc.mode = 1;
-      } else {
-        bc.mode = 2;
-        for (int a = 0; a < nmem; ++a) {
-          if (delta[a] > 0) { bc.f[a] = 1.0 - delta[a] / acc[a]; bc.c[a] = delta[a] / acc[a]; }
-          else if (delta[a] < 0) { bc.g[a] = -delta[a] / Dsum; }
+        const double l = delta[d] / acc[d];
+        const double theta = zeroT ? 0.0 : (L <= 1.0 ? 1.0 : (1.0 - l) / (L - l));
+        for (int r = 0; r < nmem; ++r) {
+          if (!(delta[r] < 0)) continue;
+          const double f = delta[d] * (-delta[r]) / Dsum;
+          const double T = acc[28 + (d < r ? pair_id(d, r) : pair_id(r, d))];
+          if (theta > 0.0) {
+            const double a = f * theta / T;
+            bc.O[d][r] -= a;
+            bc.O[r][d] += a;
+          }
+          const double b = f * (1.0 - theta) / acc[d];
+          bc.P[d][d] -= b;
+          bc.P[r][d] += b;
         }
       }
     }
@@ -630,7 +855,7 @@ __device__ void sweep_cell(const SweepParams& p, const int J, unsigned char* sme
   // ---- warm start store (R7) ---------------------------------------------
   for (int t = tid; t < NN; t += T) {
     const int k1 = t / n2, k2 = t - k1 * n2;
-    p.alpha[(long long)(cc.r0 + k1) * p.N2 + cc.c0 + k2] = A2[t];
+    p.alpha[(long long)(cc.r0 + k1) * p.N2 + cc.c0 + k2] = A2[k1 * NX + k2];
   }
   if (tid == 0) {
     p.gauge[2 * J] = G1;
@@ -669,15 +894,16 @@ __device__ void sweep_cell(const SweepParams& p, const int J, unsigned char* sme
   }
 }
 
-__global__ void __launch_bounds__(kSweepThreads) sweep_kernel(SweepParams p) {
+template <int NX>
+__global__ void __launch_bounds__(kSweepThreads, DD_SWEEP_MINB) sweep_kernel(SweepParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   if (p.mode == 0) {
     const int J = blockIdx.x;
-    if (J < p.ncells) sweep_cell(p, J, smem);
+    if (J < p.ncells) sweep_cell<NX>(p, J, smem);
   } else {
     const int n = *p.ovf_count;
     for (int k = blockIdx.x; k < n; k += gridDim.x) {
-      sweep_cell(p, p.ovf_list[k], smem);
+      sweep_cell<NX>(p, p.ovf_list[k], smem);
       __syncthreads();
     }
   }
@@ -688,13 +914,14 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(SweepParams p) {
 // shared memory for hulls <= ccap_small and queues larger cells; pass 1 runs
 // persistent CTAs with shared memory for hulls <= ccap_big over the queue.
 // No host synchronisation between the passes.
-cudaError_t launch_sweep(SweepParams p, int ccap_small, int ccap_big, cudaStream_t st) {
+template <int NX>
+static cudaError_t launch_sweep_t(SweepParams p, int ccap_small, int ccap_big, cudaStream_t st) {
   static size_t configured = 0;
   const size_t smem0 = sweep_smem_bytes(ccap_small, p.s);
   const size_t smem1 = sweep_smem_bytes(ccap_big, p.s);
   const size_t need = smem0 > smem1 ? smem0 : smem1;
   if (need > 48 * 1024 && need > configured) {
-    cudaError_t e = cudaFuncSetAttribute(sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);
     if (e != cudaSuccess) return e;
     configured = need;
   }
@@ -702,7 +929,7 @@ cudaError_t launch_sweep(SweepParams p, int ccap_small, int ccap_big, cudaStream
   if (e != cudaSuccess) return e;
   p.mode = 0;
   p.ccap = ccap_small;
-  sweep_kernel<<<p.ncells, kSweepThreads, smem0, st>>>(p);
+  sweep_kernel<NX><<<p.ncells, kSweepThreads, smem0, st>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (ccap_big > ccap_small) {
@@ -711,10 +938,20 @@ cudaError_t launch_sweep(SweepParams p, int ccap_small, int ccap_big, cudaStream
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     p.mode = 1;
     p.ccap = ccap_big;
-    sweep_kernel<<<nsm, kSweepThreads, smem1, st>>>(p);
+    sweep_kernel<NX><<<nsm, kSweepThreads, smem1, st>>>(p);
     e = cudaGetLastError();
   }
   return e;
+}
+
+cudaError_t launch_sweep(SweepParams p, int ccap_small, int ccap_big, cudaStream_t st) {
+  switch (p.s) {
+    case 1: return launch_sweep_t<2>(p, ccap_small, ccap_big, st);
+    case 2: return launch_sweep_t<4>(p, ccap_small, ccap_big, st);
+    case 4: return launch_sweep_t<8>(p, ccap_small, ccap_big, st);
+    case 8: return launch_sweep_t<16>(p, ccap_small, ccap_big, st);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace dd

@@ -170,14 +170,25 @@ def test_balance_identities():
     o0, o1 = O.balance([p0, p1], [0.5, 0.5])
     np.testing.assert_allclose(o0, [[0.2, 0.3]])
     np.testing.assert_allclose(o1, [[0.5, 0.0]])
-    # disjoint supports cannot exchange mass pointwise: the exact fallback
-    # (proportional pooling) is used
+    # disjoint supports cannot exchange mass pointwise: the transfer falls
+    # back to the donor's own shape (theta = 0)
     q0 = np.array([[0.6, 0.0]])
     q1 = np.array([[0.0, 0.4]])
     r0, r1 = O.balance([q0, q1], [0.5, 0.5])
     np.testing.assert_allclose(r0 + r1, q0 + q1)
     np.testing.assert_allclose([r0.sum(), r1.sum()], [0.5, 0.5])
     assert (r0 >= 0).all() and (r1 >= 0).all()
+    np.testing.assert_allclose(r1, [[0.1, 0.4]])
+    # continuity of the blend at the overlap-capacity threshold L = 1
+    a0 = np.array([[0.5, 0.1]])
+    a1 = np.array([[0.1, 0.3]])
+    Tov = 0.5 * 0.1 / 0.6 + 0.1 * 0.3 / 0.4
+    outs = []
+    for dlt in (Tov * (1 - 1e-9), Tov * (1 + 1e-9)):
+        m0, m1 = a0.sum(), a1.sum()
+        outs.append(O.balance([a0, a1], [m0 - dlt, m1 + dlt]))
+    np.testing.assert_allclose(outs[0][0], outs[1][0], rtol=1e-7)
+    np.testing.assert_allclose(outs[0][1], outs[1][1], rtol=1e-7)
 
 
 def test_truncate_box():

@@ -81,7 +81,7 @@ void solve(bool warm) {
   while (eps >= 1) {
     eps = (eps + alpha - 1) / alpha; if (eps < 1) eps = 1; ++refines;
     for (int i = 0; i < I; ++i) for (int a = 0; a < 5; ++a) { int j = nbr(i, a); if (j < 0) continue;
-      ll cp = cs[5*i+a] + pS[i] - pT[j]; if (cp < 0) w[5*i+a] = q[i]; else if (cp > 0) w[5*i+a] = 0; }
+      ll cp = cs[5*i+a] + pS[i] - pT[j]; ll th = getenv("SAT0") ? 0 : eps; if (cp < -th) w[5*i+a] = q[i]; else if (cp > th) w[5*i+a] = 0; }
     for (int i = 0; i < I; ++i) { ll out = 0; for (int a = 0; a < 5; ++a) out += w[5*i+a]; eS[i] = q[i] - out;
       ll in = 0; for (int k = 0; k < 5; ++k) { int a; int s = in_arc(i, k, &a); if (s >= 0) in += w[5LL*s+a]; } eT[i] = in - q[i]; }
     price_update(eps, gu_cap);
@@ -100,7 +100,7 @@ void solve(bool warm) {
       }
       ll active = 0;
       for (int i = 0; i < I; ++i) { eS[i] += addS[i]; eT[i] += addT[i]; addS[i] = addT[i] = 0; active += (eS[i] > 0) + (eT[i] > 0); }
-      if (getenv("TRACE") && refines == 3 && ((rounds - r0) < 20 || (rounds - r0) % 500 == 0)) {
+      if (getenv("TRACE") && refines == atoi(getenv("TRACE")) && ((rounds - r0) < 10 || (rounds - r0) % 250 == 0)) {
         ll ex = 0; for (int i = 0; i < I; ++i) ex += std::max(0LL, eS[i]) + std::max(0LL, eT[i]);
         printf("  r %lld active %lld excess %lld\n", rounds - r0, active, ex);
       }
@@ -130,5 +130,12 @@ int main(int argc, char** argv) {
   if (argc > 3) alpha = atoi(argv[3]);
   if (argc > 4) gu_every = atoi(argv[4]);
   load(argv[1]); solve(false);
-  if (argc > 2 && argv[2][0] != '-') { load(argv[2]); solve(true); }
+  if (argc > 2 && argv[2][0] == 'p') {   // restart from stationary flow with (perturbed) optimal prices
+    double noise = atof(argv[2] + 1);
+    ll SC = 2LL * I + 1;
+    srand(1);
+    for (int i = 0; i < I; ++i) { pS[i] += (ll)(noise * SC * ((rand() / (double)RAND_MAX) - 0.5)); pT[i] += (ll)(noise * SC * ((rand() / (double)RAND_MAX) - 0.5)); }
+    for (int i = 0; i < I; ++i) for (int a = 0; a < 5; ++a) w[5*i+a] = a == 0 ? q[i] : 0;
+    solve(true);
+  } else if (argc > 2 && argv[2][0] != '-') { load(argv[2]); solve(true); }
 }
