@@ -1,27 +1,36 @@
-// sweep.cu — the fused domain-decomposition sweep kernel (sm_100a).
+// sweep.cu — the domain-decomposition sweep (sm_100a): two kernels per
+// partition sweep, each batched over all composite cells (one CTA per cell,
+// as the batched SinkhornGPU of App. A.1):
 //
-// One CTA per composite cell J of the partition (batched over all cells, as
-// the batched SinkhornGPU of App. A.1).  Per cell, in one
-// launch and without leaving the SM:
+// solve_kernel (fp32 only, small register/shared footprint -> high occupancy)
 //   a1 BasicToComposite   nu_J = sum_{i in J} nu_i on the hull box
-//                         (Eq. get-composite-cell-marginal PAPER.md:1128-1133)
+//                         (Eq. get-composite-cell-marginal PAPER.md:1128-1133),
+//                         needed here only as log2 nu_J
 //   a2 log-domain separable Sinkhorn on X_J x box(nu_J),
-//      fp32, base-2, in a per-cell local gauge,
-//      stopping rule = L1 X-marginal error after the Y-update <= Err mu(X_J)
+//      base-2, in a per-cell local gauge, stopping
+//      rule = L1 X-marginal error after the Y-update <= Err mu(X_J)
 //      (per-cell reading R6), warm start from the previous
-//      sweep on the same partition (reading R7)
-//   a3 CompositeToBasic   nu_i = nu_J * exp(S_i - LSE_i' S_i') (share form of
+//      sweep on the same partition (reading R7); writes the plan's potential
+//      (the warm start of the next sweep) and per-cell stats.
+// split_kernel (fp64 marginals)
+//   a1 nu_J again, in fp64
+//   a3 CompositeToBasic   nu_i = nu_J exp(S_i - LSE_i' S_i') (share form of
 //                         PAPER.md:1151-1193), plus
-//                         the plan cost <c, pi_i> for the flow update (R13)
-//   a4 Balance            proportional pooling (Alg. 4 l.6 PAPER.md:1231, R8)
+//                         the plan moments for the flow update (R13)
+//   a4 Balance            (Alg. 4 l.6 PAPER.md:1231, reading R8)
 //   a5 Truncate + minimal box (Alg. 4 l.7 PAPER.md:1233, tau PAPER.md:1265)
 //   a6 per-cell stats for the sweep reductions.
-// The linear-domain marginals (pool, nu_J, shares, balance) are fp64 so that
-// the global Y-marginal is preserved to fp64 rounding.
+// The linear-domain marginals are fp64 so that the global Y-marginal is
+// preserved to fp64 rounding.  Cells whose hull
+// exceeds the fast size class are queued on the device and handled by a
+// second, large-shared-memory launch of each kernel.
 #include "internal.cuh"
 
-#ifndef DD_SWEEP_MINB
-#define DD_SWEEP_MINB 4
+#ifndef DD_SOLVE_MINB
+#define DD_SOLVE_MINB 8
+#endif
+#ifndef DD_SPLIT_MINB
+#define DD_SPLIT_MINB 4
 #endif
 
 namespace dd {
@@ -46,29 +55,44 @@ __device__ __forceinline__ float exp2m1f(float x) {
   return ex2f(x) - 1.0f;
 }
 
-// Deterministic block reductions (fixed thread->data map, fixed tree).
-// Deterministic block sum of NV doubles (fixed thread->data map, fixed tree).
-// Not unrolled on purpose: it runs once per cell and code size matters more.
-template <int NV>
-__device__ __noinline__ void block_sum_d(double* v, double* scratch) {
+// Deterministic block sum of one double (fixed tree); scratch >= 32 doubles.
+__device__ __forceinline__ double block_sum1_d(double v, double* scratch) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll 1
-  for (int k = 0; k < NV; ++k) {
-    double x = v[k];
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    v[k] = x;
-  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   __syncthreads();
-  if (lane == 0) {
-#pragma unroll 1
-    for (int k = 0; k < NV; ++k) scratch[wid * NV + k] = v[k];
-  }
+  if (lane == 0) scratch[wid] = v;
   __syncthreads();
+  double t = 0.0;
+  for (int k = 0; k < nw; ++k) t += scratch[k];
+  __syncthreads();
+  return t;
+}
+
+// Deterministic block sum of 32 doubles per thread: a transpose butterfly
+// leaves lane l with the warp total of value l (31 shuffles of doubles instead
+// of 160), then the warps are summed in a fixed order.  scratch >= 33 * nw.
+__device__ __noinline__ void block_sum32_d(double* v, double* scratch, double* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int o = 16;
 #pragma unroll 1
-  for (int k = 0; k < NV; ++k) {
+  for (int n = 32; n > 1; n >>= 1) {
+    const int h = n >> 1;
+    const bool up = (lane & o) != 0;
+#pragma unroll 1
+    for (int i = 0; i < h; ++i) {
+      const double send = up ? v[i] : v[i + h];
+      const double keep = up ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+    o >>= 1;
+  }
+  scratch[wid * 32 + lane] = v[0];   // lane l holds the total of value l
+  __syncthreads();
+  if (threadIdx.x < 32) {
     double t = 0.0;
-    for (int w = 0; w < nw; ++w) t += scratch[w * NV + k];
-    v[k] = t;
+    for (int k = 0; k < nw; ++k) t += scratch[k * 32 + threadIdx.x];
+    out[threadIdx.x] = t;
   }
   __syncthreads();
 }
@@ -100,62 +124,32 @@ __device__ __forceinline__ float block_sum_f(float v, float* scratch, int parity
   return t;
 }
 
-
-// Warp all-reduce max.
-__device__ __forceinline__ float warp_max(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-
-// Transpose butterfly: reduce NV per-lane partial sums over the warp so that
-// every lane ends with the total of output xreduce_index<NV>(lane) (NV - 1 +
-// log2(32/NV) shuffles instead of 5 NV).
-template <int NV>
-__device__ __forceinline__ float xreduce(float (&v)[NV], int lane) {
-  int o = 16;
-#pragma unroll
-  for (int n = NV; n > 1; n >>= 1) {
-    const int h = n >> 1;
-    const bool up = (lane & o) != 0;
-#pragma unroll
-    for (int i = 0; i < h; ++i) {
-      const float send = up ? v[i] : v[i + h];
-      const float keep = up ? v[i + h] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-    }
-    o >>= 1;
-  }
-  float t = v[0];
-  for (; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-  return t;
-}
-
-template <int NV>
-__device__ __forceinline__ int xreduce_index(int lane) {
-  int idx = 0, o = 16;
-#pragma unroll
-  for (int n = NV; n > 1; n >>= 1) {
-    if (lane & o) idx += n >> 1;
-    o >>= 1;
-  }
-  return idx;
-}
-
-template <int NV>
-__device__ __forceinline__ bool xreduce_writer(int lane) {
-  int o = 16;
-#pragma unroll
-  for (int n = NV; n > 1; n >>= 1) o >>= 1;
-  return (lane & (2 * o - 1)) == 0;   // lowest lane of each group of equal outputs
-}
-
-struct SmemLayout {
-  size_t nuJ, red, P0, P1, P2, P3, U, R, V, A2, A2n, LM, MU, AL, fred, ints, total;
+// ---------------------------------------------------------------------------
+// Shared-memory layouts.  BB = ccap^2 box entries, NX = 2 s.
+struct SolveLayout {
+  size_t B, LN, BK, U, V, X, fred, ints, total;   // X: A2, A2n, LM, MU, AL
 };
-
-__host__ __device__ inline SmemLayout smem_layout(int ccap, int s) {
-  SmemLayout L;
+__host__ __device__ inline SolveLayout solve_layout(int ccap, int s) {
+  SolveLayout L;
+  const size_t BB = (size_t)ccap * ccap, NX = 2 * (size_t)s;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 15) & ~size_t(15); return r; };
+  L.B = take(BB * 4);
+  L.LN = take(BB * 4);
+  L.BK = take(BB * 8);       // fp64 assembly scratch first, then BK (fp32)
+  L.U = take(2 * NX * ccap * 4);
+  L.V = take(2 * NX * ccap * 4);
+  L.X = take(5 * NX * NX * 4);
+  L.fred = take(64 * 4);
+  L.ints = take(32 * 4);
+  L.total = o;
+  return L;
+}
+struct SplitLayout {
+  size_t nuJ, red, P0, P1, P2, P3, U, R, AL, ints, total;
+};
+__host__ __device__ inline SplitLayout split_layout(int ccap, int s) {
+  SplitLayout L;
   const size_t BB = (size_t)ccap * ccap, NX = 2 * (size_t)s;
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 15) & ~size_t(15); return r; };
@@ -167,102 +161,21 @@ __host__ __device__ inline SmemLayout smem_layout(int ccap, int s) {
   L.P3 = take(BB * 4);
   L.U = take(2 * NX * ccap * 4);
   L.R = take(4 * NX * ccap * 4);
-  L.V = take(2 * NX * ccap * 4);
-  L.A2 = take(NX * NX * 4);
-  L.A2n = take(NX * NX * 4);
-  L.LM = take(NX * NX * 4);
-  L.MU = take(NX * NX * 4);
   L.AL = take(NX * NX * 4);
-  L.fred = take(64 * 4);
   L.ints = take(64 * 4);
   L.total = o;
   return L;
 }
-
-size_t sweep_smem_bytes(int ccap, int s) { return smem_layout(ccap, s).total; }
-
-// Final (balanced) value of every member at one box entry.  Explicit _rn
-// intrinsics: bitwise identical in the truncation and the write pass.
-// Balance (reading R8): blended overlap / own-shape transfer
-//   v_k = parts_k + parts_k * (sum_j O_kj parts_j) / nu_J + sum_j P_kj parts_j
-// (O: overlap-transfer coefficients f theta / T, P: own-shape coefficients
-// f (1 - theta) / M_d; see oracle/domdec.py:balance for the definition).
-struct BalanceCoef {
-  int active;
-  double O[4][4];
-  double P[4][4];
-};
-
-__device__ __forceinline__ void member_values(double nuj, const float* p, int nmem,
-                                              const BalanceCoef& bc, double* out) {
-  int am = 0;
-#pragma unroll
-  for (int k = 1; k < 4; ++k)
-    if (k < nmem && p[k] > p[am]) am = k;
-  double parts[4];
-  double rest = 0.0;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    parts[k] = 0.0;
-    if (k < nmem && k != am) {
-      parts[k] = __dmul_rn(nuj, (double)p[k]);
-      rest = __dadd_rn(rest, parts[k]);
-    }
-  }
-  const double pa = __dsub_rn(nuj, rest);
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-    if (k == am) parts[k] = pa > 0.0 ? pa : 0.0;
-  if (bc.active && nuj > 0.0) {
-    const double inv = __drcp_rn(nuj);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      double t = 0.0, u = 0.0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        t = __dadd_rn(t, __dmul_rn(bc.O[k][j], parts[j]));
-        u = __dadd_rn(u, __dmul_rn(bc.P[k][j], parts[j]));
-      }
-      out[k] = __dadd_rn(__dadd_rn(parts[k], __dmul_rn(parts[k], __dmul_rn(t, inv))), u);
-    }
-  } else {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) out[k] = parts[k];
-  }
+size_t sweep_smem_bytes(int ccap, int s) {
+  const size_t a = solve_layout(ccap, s).total, b = split_layout(ccap, s).total;
+  return a > b ? a : b;
 }
 
-__device__ __forceinline__ int pair_id(int a, int b) {   // a < b, 4 members -> 6 pairs
-  return a == 0 ? b - 1 : (a == 1 ? b + 1 : 5);
-}
-
-template <int NX>
-__device__ void sweep_cell(const SweepParams& p, const int J, unsigned char* smem) {
-  const int tid = threadIdx.x, T = blockDim.x;
-  const SmemLayout Ls = smem_layout(p.ccap, p.s);
-  double* nuJ = (double*)(smem + Ls.nuJ);
-  double* red = (double*)(smem + Ls.red);
-  float* P0 = (float*)(smem + Ls.P0);
-  float* P1 = (float*)(smem + Ls.P1);
-  float* P2 = (float*)(smem + Ls.P2);
-  float* P3 = (float*)(smem + Ls.P3);
-  float* Ub = (float*)(smem + Ls.U);
-  float* Rb = (float*)(smem + Ls.R);
-  float* Vb = (float*)(smem + Ls.V);
-  float* A2 = (float*)(smem + Ls.A2);
-  float* A2n = (float*)(smem + Ls.A2n);
-  float* LM = (float*)(smem + Ls.LM);
-  float* MU = (float*)(smem + Ls.MU);
-  float* AL = (float*)(smem + Ls.AL);
-  float* fred = (float*)(smem + Ls.fred);
-  int* ints = (int*)(smem + Ls.ints);
-
-  const CompCell cc = p.cells[J];
-  const int nmem = cc.nmem, n1 = cc.n1, n2 = cc.n2, s = p.s;
-  const float w = p.w;
-  const long long slot = p.slot;
-
-  // ---- member boxes and hull (a1) -------------------------------------
-  if (tid < nmem) {
+// Member boxes and hull of composite cell J (a1).  ints[0..15] receive the
+// member offsets/extents; returns (L1, L2, b1, b2).
+__device__ __forceinline__ int4 cell_hull(const SweepParams& p, const CompCell& cc, int* ints) {
+  const int tid = threadIdx.x;
+  if (tid < cc.nmem) {
     const int i = cc.mem[tid];
     ints[tid] = p.off_in[2 * i];
     ints[4 + tid] = p.off_in[2 * i + 1];
@@ -271,72 +184,76 @@ __device__ void sweep_cell(const SweepParams& p, const int J, unsigned char* sme
   }
   __syncthreads();
   int L1 = ints[0], L2 = ints[4], U1 = ints[0] + ints[8], U2 = ints[4] + ints[12];
-  for (int k = 1; k < nmem; ++k) {
+  for (int k = 1; k < cc.nmem; ++k) {
     L1 = min(L1, ints[k]);
     L2 = min(L2, ints[4 + k]);
     U1 = max(U1, ints[k] + ints[8 + k]);
     U2 = max(U2, ints[4 + k] + ints[12 + k]);
   }
-  const int b1 = U1 - L1, b2 = U2 - L2, BB = b1 * b2;
-  // gauge origin G = L + o, o = floor((b - n)/2) (DESIGN.md "Local gauge")
-  const int o1 = (b1 - n1) >> 1, o2 = (b2 - n2) >> 1;
-  const int G1 = L1 + o1, G2 = L2 + o2;
+  return make_int4(L1, L2, U1 - L1, U2 - L2);
+}
 
-  auto copy_unchanged = [&](int reason) {
-    for (int k = 0; k < nmem; ++k) {
-      const int i = cc.mem[k];
-      const long long len = (long long)ints[8 + k] * ints[12 + k];
-      const double* src = p.pool_in + (long long)i * slot;
-      double* dst = p.pool_out + (long long)i * slot;
-      for (long long t = tid; t < len; t += T) dst[t] = src[t];
-      if (tid == 0) {
-        p.off_out[2 * i] = ints[k];
-        p.off_out[2 * i + 1] = ints[4 + k];
-        p.ext_out[2 * i] = ints[8 + k];
-        p.ext_out[2 * i + 1] = ints[12 + k];
-      }
-    }
-    if (tid == 0) {
-      CellStats st;
-      st.iters = 0;
-      st.overflow = reason;
-      st.e0 = 0.f;
-      st.e = 0.f;
-      st.dropped = 0.0;
-      p.stats[J] = st;
-      atomicAdd(&p.totals->overflow, 1ull);
-      atomicAdd(&p.totals->cells, 1ull);
-    }
-  };
-
-  if (b1 > p.ccap || b2 > p.ccap) {
-    if (p.mode == 0) {   // defer to the large size class (second launch)
-      if (tid == 0) p.ovf_list[atomicAdd(p.ovf_count, 1)] = J;
-    } else {
-      copy_unchanged(1);
-    }
-    return;
-  }
-
-  // ---- assemble nu_J (fp64, member order) -------------------------------
+// nu_J = sum of the member boxes on the hull, fp64, member order (a1).
+__device__ __forceinline__ void assemble(const SweepParams& p, const CompCell& cc, const int* ints, int L1, int L2,
+                                         int b2, int BB, double* nuJ) {
+  const int tid = threadIdx.x, T = blockDim.x;
   for (int t = tid; t < BB; t += T) nuJ[t] = 0.0;
   __syncthreads();
-  for (int k = 0; k < nmem; ++k) {
+  for (int k = 0; k < cc.nmem; ++k) {
     const int i = cc.mem[k];
     const int e1 = ints[8 + k], e2 = ints[12 + k];
     const int d1 = ints[k] - L1, d2 = ints[4 + k] - L2;
-    const double* src = p.pool_in + (long long)i * slot;
+    const double* src = p.pool_in + (long long)i * p.slot;
     for (int t = tid; t < e1 * e2; t += T) {
       const int r = t / e2, c = t - r * e2;
       nuJ[(d1 + r) * b2 + d2 + c] += src[t];
     }
     __syncthreads();
   }
-  double massJ_v[1] = {0.0};
+}
+
+// ===========================================================================
+// solve_kernel: a1 (log2 nu_J) + a2 (Sinkhorn), one CTA per composite cell.
+template <int NX>
+__device__ void solve_cell(const SweepParams& p, const int J, unsigned char* smem) {
+  const int tid = threadIdx.x, T = blockDim.x;
+  const SolveLayout Ls = solve_layout(p.ccap, p.s);
+  float* P0 = (float*)(smem + Ls.B);       // B (Y potential)
+  float* P1 = (float*)(smem + Ls.LN);      // log2 nu_J
+  float* P2 = (float*)(smem + Ls.BK);      // BK
+  double* nuJ = (double*)(smem + Ls.BK);   // assembly scratch (before the loop)
+  float* Ub = (float*)(smem + Ls.U);
+  float* Rb = Ub + NX * p.ccap;            // UK
+  float* Vb = (float*)(smem + Ls.V);
+  float* X = (float*)(smem + Ls.X);
+  float* A2 = X;
+  float* A2n = X + NX * NX;
+  float* LM = X + 2 * NX * NX;
+  float* MU = X + 3 * NX * NX;
+  float* AL = X + 4 * NX * NX;
+  float* fred = (float*)(smem + Ls.fred);
+  int* ints = (int*)(smem + Ls.ints);
+
+  const CompCell cc = p.cells[J];
+  const int nmem = cc.nmem, n1 = cc.n1, n2 = cc.n2;
+  const float w = p.w;
+  const int4 hull = cell_hull(p, cc, ints);
+  const int L1 = hull.x, L2 = hull.y, b1 = hull.z, b2 = hull.w, BB = b1 * b2;
+  // gauge origin G = L + o, o = floor((b - n)/2) (DESIGN.md "Local gauge")
+  const int o1 = (b1 - n1) >> 1, o2 = (b2 - n2) >> 1;
+  const int G1 = L1 + o1, G2 = L2 + o2;
+  if (b1 > p.ccap || b2 > p.ccap) {
+    if (p.mode == 0) {   // defer to the large size class (second launch)
+      if (tid == 0) p.ovf_list[atomicAdd(p.ovf_count, 1)] = J;
+    } else if (tid == 0) {
+      p.stats[J].overflow = 1;   // split_kernel leaves the cell unchanged
+    }
+    return;
+  }
+  assemble(p, cc, ints, L1, L2, b2, BB, nuJ);
   for (int t = tid; t < BB; t += T) {
     const double v = nuJ[t];
     P1[t] = v > 0.0 ? lg2f((float)v) : kNeg;   // log2 nu_J (zeros -> kNeg, R19)
-    massJ_v[0] += v;
   }
   // ---- X-block data, warm start (R7) and re-gauge ------------------------
   // The X-block is padded to NX x NX (ragged B cells have n = s on an axis);
@@ -364,8 +281,6 @@ __device__ void sweep_cell(const SweepParams& p, const int J, unsigned char* sme
     LM[t] = lm;
     MU[t] = mu;
   }
-  block_sum_d<1>(massJ_v, red);
-  const double massJ = massJ_v[0];
   amax = block_max_f(amax, fred);
   for (int t = tid; t < NXX; t += T) {
     A2[t] -= amax;
@@ -626,8 +541,183 @@ __device__ void sweep_cell(const SweepParams& p, const int J, unsigned char* sme
     float* tmp = A2; A2 = A2n; A2n = tmp;   // A <- A'
     first = false;
   }
-  for (int t = tid; t < NXX; t += T) AL[t] = A2[t] + LM[t];
+  // ---- outputs: the plan's potential (next warm start, R7) and stats -----
+  for (int t = tid; t < NN; t += T) {
+    const int k1 = t / n2, k2 = t - k1 * n2;
+    p.alpha[(long long)(cc.r0 + k1) * p.N2 + cc.c0 + k2] = A2[k1 * NX + k2];
+  }
+  if (tid == 0) {
+    p.gauge[2 * J] = G1;
+    p.gauge[2 * J + 1] = G2;
+    CellStats st;
+    st.iters = it;
+    st.overflow = 0;
+    st.e0 = e0;
+    st.e = e;
+    st.dropped = 0.0;
+    p.stats[J] = st;
+    // algorithmic MUFU count of the Sinkhorn passes: E_it + L_it
+    // per pass plus NN for the X-error
+    const unsigned long long E_it = (unsigned long long)n1 * n2 * b2 + (unsigned long long)b1 * b2 * n1 +
+                                    (unsigned long long)b1 * n2 * b2 + (unsigned long long)n1 * n2 * b1;
+    const unsigned long long L_it = (unsigned long long)n1 * b2 + BB + (unsigned long long)b1 * n2 + NN;
+    const unsigned long long mufu = (unsigned long long)it * (E_it + L_it + NN) + BB;
+    atomicAdd(&p.totals->mufu, mufu);
+    atomicAdd(&p.cum->mufu, mufu);
+    atomicAdd(&p.cum->iters, (unsigned long long)it);
+    atomicAdd(&p.totals->iters, (unsigned long long)it);
+    if (p.fixed_iter <= 0 && it >= p.max_iter && e > tolJ) atomicAdd(&p.totals->nonconv, 1ull);
+    atomicMax(&p.totals->iters_max, it);
+    atomicAdd(&p.totals->e0, (double)e0);
+    atomicAdd(&p.totals->e, (double)e);
+  }
+}
+
+template <int NX>
+__global__ void __launch_bounds__(kSweepThreads, DD_SOLVE_MINB) solve_kernel(SweepParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  if (p.mode == 0) {
+    if ((int)blockIdx.x < p.ncells) solve_cell<NX>(p, blockIdx.x, smem);
+  } else {
+    const int n = *p.ovf_count;
+    for (int k = blockIdx.x; k < n; k += gridDim.x) {
+      solve_cell<NX>(p, p.ovf_list[k], smem);
+      __syncthreads();
+    }
+  }
+}
+
+// ===========================================================================
+// split_kernel: a1 (fp64) + a3 + a4 + a5 + a6, one CTA per composite cell.
+// Final (balanced) value of every member at one box entry.  Explicit _rn
+// intrinsics: bitwise identical in the truncation and the write pass.
+// Balance (reading R8): blended overlap / own-shape transfer
+//   v_k = parts_k + parts_k * (sum_j O_kj parts_j) / nu_J + sum_j P_kj parts_j
+// (O: overlap-transfer coefficients f theta / T, P: own-shape coefficients
+// f (1 - theta) / M_d; see oracle/domdec.py:balance for the definition).
+struct BalanceCoef {
+  int active;
+  double O[4][4];
+  double P[4][4];
+};
+
+__device__ __forceinline__ void member_values(double nuj, const float* p, int nmem,
+                                              const BalanceCoef& bc, double* out) {
+  int am = 0;
+#pragma unroll
+  for (int k = 1; k < 4; ++k)
+    if (k < nmem && p[k] > p[am]) am = k;
+  double parts[4];
+  double rest = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    parts[k] = 0.0;
+    if (k < nmem && k != am) {
+      parts[k] = __dmul_rn(nuj, (double)p[k]);
+      rest = __dadd_rn(rest, parts[k]);
+    }
+  }
+  const double pa = __dsub_rn(nuj, rest);
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (k == am) parts[k] = pa > 0.0 ? pa : 0.0;
+  if (bc.active && nuj > 0.0) {
+    const double inv = __drcp_rn(nuj);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      double t = 0.0, u = 0.0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        t = __dadd_rn(t, __dmul_rn(bc.O[k][j], parts[j]));
+        u = __dadd_rn(u, __dmul_rn(bc.P[k][j], parts[j]));
+      }
+      out[k] = __dadd_rn(__dadd_rn(parts[k], __dmul_rn(parts[k], __dmul_rn(t, inv))), u);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) out[k] = parts[k];
+  }
+}
+
+__device__ __forceinline__ int pair_id(int a, int b) {   // a < b, 4 members -> 6 pairs
+  return a == 0 ? b - 1 : (a == 1 ? b + 1 : 5);
+}
+
+template <int NX>
+__device__ void split_cell(const SweepParams& p, const int J, unsigned char* smem) {
+  const int tid = threadIdx.x, T = blockDim.x;
+  const SplitLayout Ls = split_layout(p.ccap, p.s);
+  double* nuJ = (double*)(smem + Ls.nuJ);
+  double* red = (double*)(smem + Ls.red);
+  float* P0 = (float*)(smem + Ls.P0);
+  float* P1 = (float*)(smem + Ls.P1);
+  float* P2 = (float*)(smem + Ls.P2);
+  float* P3 = (float*)(smem + Ls.P3);
+  float* Ub = (float*)(smem + Ls.U);
+  float* Rb = (float*)(smem + Ls.R);
+  float* AL = (float*)(smem + Ls.AL);
+  int* ints = (int*)(smem + Ls.ints);
+
+  const CompCell cc = p.cells[J];
+  const int nmem = cc.nmem, n1 = cc.n1, n2 = cc.n2, s = p.s;
+  const float w = p.w;
+  const long long slot = p.slot;
+  const int4 hull = cell_hull(p, cc, ints);
+  const int L1 = hull.x, L2 = hull.y, b1 = hull.z, b2 = hull.w, BB = b1 * b2;
+  const int o1 = (b1 - n1) >> 1, o2 = (b2 - n2) >> 1;
+  const float fo1 = (float)o1, fo2 = (float)o2;
+
+  auto copy_unchanged = [&](int reason) {
+    for (int k = 0; k < nmem; ++k) {
+      const int i = cc.mem[k];
+      const long long len = (long long)ints[8 + k] * ints[12 + k];
+      const double* src = p.pool_in + (long long)i * slot;
+      double* dst = p.pool_out + (long long)i * slot;
+      for (long long t = tid; t < len; t += T) dst[t] = src[t];
+      if (tid == 0) {
+        p.off_out[2 * i] = ints[k];
+        p.off_out[2 * i + 1] = ints[4 + k];
+        p.ext_out[2 * i] = ints[8 + k];
+        p.ext_out[2 * i + 1] = ints[12 + k];
+      }
+    }
+    if (tid == 0) {
+      p.stats[J].overflow = reason;
+      atomicAdd(&p.totals->overflow, 1ull);
+      atomicAdd(&p.totals->cells, 1ull);
+    }
+  };
+
+  if (b1 > p.ccap || b2 > p.ccap) {
+    if (p.mode == 1) copy_unchanged(1);
+    return;   // mode 0: handled by the large size class launch
+  }
+  if (p.stats[J].overflow) {
+    copy_unchanged(1);
+    return;
+  }
+  assemble(p, cc, ints, L1, L2, b2, BB, nuJ);
+  double massJ = 0.0;
+  {
+    double v = 0.0;
+    for (int t = tid; t < BB; t += T) v += nuJ[t];
+    massJ = block_sum1_d(v, red);
+  }
+  // plan potential of this sweep (written by solve_kernel in the same gauge)
+  constexpr int NXX = NX * NX;
+  for (int t = tid; t < NXX; t += T) {
+    const int k1 = t / NX, k2 = t % NX;
+    float al = kNeg;
+    if (k1 < n1 && k2 < n2) {
+      const long long pix = (long long)(cc.r0 + k1) * p.N2 + cc.c0 + k2;
+      al = p.alpha[pix] + p.log2mu[pix];
+    }
+    AL[t] = al;
+  }
+  double muXJ = 0.0;
+  for (int q = 0; q < nmem; ++q) muXJ += p.m[cc.mem[q]];
   __syncthreads();
+
   // ---- a3: CompositeToBasic (share form) + plan moments (R13) --------------
   // Stage 1 split by column half h2: U_h2(k1, l2) = LSE over k2 in half h2,
   // plus the conditional moments of x2' = x2 - (centre column of the member).
@@ -741,7 +831,16 @@ __device__ void sweep_cell(const SweepParams& p, const int J, unsigned char* sme
     }
   }
   __syncthreads();
-  block_sum_d<34>(acc, red);
+  {
+    // acc[32..33] hold the (3,? ) overlaps of pairs 4 and 5; reduce 32 + 2
+    const double x32 = acc[32], x33 = acc[33];
+    block_sum32_d(acc, red, red + 160);
+    const double s32 = block_sum1_d(x32, red + 200);
+    const double s33 = block_sum1_d(x33, red + 232);
+    for (int k = 0; k < 32; ++k) acc[k] = red[160 + k];
+    acc[32] = s32;
+    acc[33] = s33;
+  }
   // ---- a4: balance coefficients (reading R8) ------------------------------
   BalanceCoef bc;
   {
@@ -798,6 +897,7 @@ __device__ void sweep_cell(const SweepParams& p, const int J, unsigned char* sme
   }
   __syncthreads();
   double drop[1] = {0.0};
+  double dloc = 0.0;
   for (int o = tid; o < BB; o += T) {
     const int l1 = o / b2, l2 = o - l1 * b2;
     const float pk[4] = {P0[o], P1[o], P2[o], P3[o]};
@@ -810,11 +910,11 @@ __device__ void sweep_cell(const SweepParams& p, const int J, unsigned char* sme
         atomicMin(&ints[16 + 4 * k + 2], l2);
         atomicMax(&ints[16 + 4 * k + 3], l2);
       } else if (v[k] > 0.0) {
-        drop[0] += v[k];
+        dloc += v[k];
       }
     }
   }
-  block_sum_d<1>(drop, red);
+  drop[0] = block_sum1_d(dloc, red);
   // capacity check (uniform)
   bool ok = true;
   for (int k = 0; k < nmem; ++k) {
@@ -852,93 +952,86 @@ __device__ void sweep_cell(const SweepParams& p, const int J, unsigned char* sme
     }
     wbytes += (unsigned long long)e1 * e2 * 8ull;
   }
-  // ---- warm start store (R7) ---------------------------------------------
-  for (int t = tid; t < NN; t += T) {
-    const int k1 = t / n2, k2 = t - k1 * n2;
-    p.alpha[(long long)(cc.r0 + k1) * p.N2 + cc.c0 + k2] = A2[k1 * NX + k2];
-  }
   if (tid == 0) {
-    p.gauge[2 * J] = G1;
-    p.gauge[2 * J + 1] = G2;
-    CellStats st;
-    st.iters = it;
-    st.overflow = 0;
-    st.e0 = e0;
-    st.e = e;
-    st.dropped = drop[0];
-    p.stats[J] = st;
-    // algorithmic MUFU count: per pass E_it + L_it (+ NN for the error)
-    const unsigned long long E_it = (unsigned long long)n1 * n2 * b2 + (unsigned long long)b1 * b2 * n1 +
-                                    (unsigned long long)b1 * n2 * b2 + (unsigned long long)n1 * n2 * b1;
-    const unsigned long long L_it = (unsigned long long)n1 * b2 + BB + (unsigned long long)b1 * n2 + NN;
+    p.stats[J].dropped = drop[0];
+    const int c2n = n2 / s;
     const unsigned long long E_c2b = (unsigned long long)n1 * n2 * b2 + (unsigned long long)nmem * s * BB +
                                      3ull * nmem * BB;
-    const unsigned long long L_c2b = (unsigned long long)c2 * n1 * b2 + (unsigned long long)nmem * BB + BB;
-    const unsigned long long mufu = (unsigned long long)it * (E_it + L_it + NN) + E_c2b + L_c2b;
-    atomicAdd(&p.totals->mufu, mufu);
-    atomicAdd(&p.cum->mufu, mufu);
-    atomicAdd(&p.cum->iters, (unsigned long long)it);
+    const unsigned long long L_c2b = (unsigned long long)c2n * n1 * b2 + (unsigned long long)nmem * BB;
+    atomicAdd(&p.totals->mufu, E_c2b + L_c2b);
+    atomicAdd(&p.cum->mufu, E_c2b + L_c2b);
     atomicAdd(&p.cum->cells, 1ull);
     unsigned long long rbytes = 0;
     for (int k = 0; k < nmem; ++k) rbytes += (unsigned long long)ints[8 + k] * ints[12 + k] * 8ull;
-    const unsigned long long byts = rbytes + wbytes + 16ull * nmem * 2 + (unsigned long long)NN * 16ull + 48ull * nmem;
+    // pool read (twice: solve + split), pool write, metadata, mu/log2mu, alpha r/w, moments
+    const unsigned long long byts = 2 * rbytes + wbytes + 16ull * nmem * 2 + (unsigned long long)n1 * n2 * 20ull + 48ull * nmem;
     atomicAdd(&p.totals->bytes, byts);
     atomicAdd(&p.cum->bytes, byts);
-    atomicAdd(&p.totals->iters, (unsigned long long)it);
     atomicAdd(&p.totals->cells, 1ull);
-    if (p.fixed_iter <= 0 && it >= p.max_iter && e > tolJ) atomicAdd(&p.totals->nonconv, 1ull);
-    atomicMax(&p.totals->iters_max, it);
-    atomicAdd(&p.totals->e0, (double)e0);
-    atomicAdd(&p.totals->e, (double)e);
     atomicAdd(&p.totals->dropped, drop[0]);
   }
 }
 
 template <int NX>
-__global__ void __launch_bounds__(kSweepThreads, DD_SWEEP_MINB) sweep_kernel(SweepParams p) {
+__global__ void __launch_bounds__(kSweepThreads, DD_SPLIT_MINB) split_kernel(SweepParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   if (p.mode == 0) {
-    const int J = blockIdx.x;
-    if (J < p.ncells) sweep_cell<NX>(p, J, smem);
+    if ((int)blockIdx.x < p.ncells) split_cell<NX>(p, blockIdx.x, smem);
   } else {
     const int n = *p.ovf_count;
     for (int k = blockIdx.x; k < n; k += gridDim.x) {
-      sweep_cell<NX>(p, p.ovf_list[k], smem);
+      split_cell<NX>(p, p.ovf_list[k], smem);
       __syncthreads();
     }
   }
 }
 
-// Two size classes (the device-side analogue of the paper's clustering by
-// box size): pass 0 runs one CTA per composite cell with
-// shared memory for hulls <= ccap_small and queues larger cells; pass 1 runs
-// persistent CTAs with shared memory for hulls <= ccap_big over the queue.
-// No host synchronisation between the passes.
+// Two size classes for each kernel (the device-side analogue of the paper's
+// clustering by box size): pass 0 runs one CTA per
+// composite cell with shared memory for hulls <= ccap_small and queues larger
+// cells; pass 1 runs persistent CTAs with shared memory for hulls <= ccap_big
+// over the queue.  No host synchronisation anywhere in the sweep.
 template <int NX>
 static cudaError_t launch_sweep_t(SweepParams p, int ccap_small, int ccap_big, cudaStream_t st) {
-  static size_t configured = 0;
-  const size_t smem0 = sweep_smem_bytes(ccap_small, p.s);
-  const size_t smem1 = sweep_smem_bytes(ccap_big, p.s);
-  const size_t need = smem0 > smem1 ? smem0 : smem1;
-  if (need > 48 * 1024 && need > configured) {
-    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);
+  static size_t conf_solve = 0, conf_split = 0;
+  const size_t s0 = solve_layout(ccap_small, p.s).total, s1 = solve_layout(ccap_big, p.s).total;
+  const size_t t0 = split_layout(ccap_small, p.s).total, t1 = split_layout(ccap_big, p.s).total;
+  const size_t ns = s0 > s1 ? s0 : s1, nt = t0 > t1 ? t0 : t1;
+  cudaError_t e;
+  if (ns > 48 * 1024 && ns > conf_solve) {
+    e = cudaFuncSetAttribute(solve_kernel<NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ns);
     if (e != cudaSuccess) return e;
-    configured = need;
+    conf_solve = ns;
   }
-  cudaError_t e = cudaMemsetAsync(p.ovf_count, 0, sizeof(int), st);
+  if (nt > 48 * 1024 && nt > conf_split) {
+    e = cudaFuncSetAttribute(split_kernel<NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nt);
+    if (e != cudaSuccess) return e;
+    conf_split = nt;
+  }
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaMemsetAsync(p.ovf_count, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
   p.mode = 0;
   p.ccap = ccap_small;
-  sweep_kernel<NX><<<p.ncells, kSweepThreads, smem0, st>>>(p);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  if (ccap_big > ccap_small) {
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  solve_kernel<NX><<<p.ncells, kSweepThreads, s0, st>>>(p);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const bool big = ccap_big > ccap_small;
+  if (big) {
     p.mode = 1;
     p.ccap = ccap_big;
-    sweep_kernel<NX><<<nsm, kSweepThreads, smem1, st>>>(p);
+    solve_kernel<NX><<<nsm, kSweepThreads, s1, st>>>(p);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  p.mode = 0;
+  p.ccap = ccap_small;
+  split_kernel<NX><<<p.ncells, kSweepThreads, t0, st>>>(p);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (big) {
+    p.mode = 1;
+    p.ccap = ccap_big;
+    split_kernel<NX><<<nsm, kSweepThreads, t1, st>>>(p);
     e = cudaGetLastError();
   }
   return e;
