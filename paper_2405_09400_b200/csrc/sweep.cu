@@ -69,29 +69,29 @@ __device__ __forceinline__ double block_sum1_d(double v, double* scratch) {
   return t;
 }
 
-// Deterministic block sum of 32 doubles per thread: a transpose butterfly
-// leaves lane l with the warp total of value l (31 shuffles of doubles instead
-// of 160), then the warps are summed in a fixed order.  scratch >= 33 * nw.
-__device__ __noinline__ void block_sum32_d(double* v, double* scratch, double* out) {
+// Deterministic block sum of the first 32 of N doubles per thread: a
+// transpose butterfly leaves lane l with the warp total of value l (31
+// shuffles of doubles instead of 160), then the warps are summed in a fixed
+// order.  Fully unrolled so v stays in registers.  scratch >= 32 * nw.
+template <int N>
+__device__ __forceinline__ void block_sum32_d(double (&v)[N], double* scratch, double* out) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int o = 16;
-#pragma unroll 1
-  for (int n = 32; n > 1; n >>= 1) {
+#pragma unroll
+  for (int n = 32, o = 16; n > 1; n >>= 1, o >>= 1) {
     const int h = n >> 1;
     const bool up = (lane & o) != 0;
-#pragma unroll 1
+#pragma unroll
     for (int i = 0; i < h; ++i) {
       const double send = up ? v[i] : v[i + h];
       const double keep = up ? v[i + h] : v[i];
       v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
     }
-    o >>= 1;
   }
   scratch[wid * 32 + lane] = v[0];   // lane l holds the total of value l
   __syncthreads();
   if (threadIdx.x < 32) {
     double t = 0.0;
-    for (int k = 0; k < nw; ++k) t += scratch[k * 32 + threadIdx.x];
+    for (int q = 0; q < nw; ++q) t += scratch[q * 32 + threadIdx.x];
     out[threadIdx.x] = t;
   }
   __syncthreads();
@@ -154,7 +154,7 @@ __host__ __device__ inline SplitLayout split_layout(int ccap, int s) {
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 15) & ~size_t(15); return r; };
   L.nuJ = take(BB * 8);
-  L.red = take(256 * 8);
+  L.red = take(288 * 8);
   L.P0 = take(BB * 4);
   L.P1 = take(BB * 4);
   L.P2 = take(BB * 4);
@@ -595,14 +595,10 @@ __global__ void __launch_bounds__(kSweepThreads, DD_SOLVE_MINB) solve_kernel(Swe
 //   v_k = parts_k + parts_k * (sum_j O_kj parts_j) / nu_J + sum_j P_kj parts_j
 // (O: overlap-transfer coefficients f theta / T, P: own-shape coefficients
 // f (1 - theta) / M_d; see oracle/domdec.py:balance for the definition).
-struct BalanceCoef {
-  int active;
-  double O[4][4];
-  double P[4][4];
-};
-
-__device__ __forceinline__ void member_values(double nuj, const float* p, int nmem,
-                                              const BalanceCoef& bc, double* out) {
+// Balance coefficients live in shared memory: bc[0] = active flag,
+// bc[1 + 4k + j] = O_kj, bc[17 + 4k + j] = P_kj.
+__device__ __forceinline__ void member_values(double nuj, const float* p, int nmem, const double* bc,
+                                              double* out) {
   int am = 0;
 #pragma unroll
   for (int k = 1; k < 4; ++k)
@@ -621,15 +617,15 @@ __device__ __forceinline__ void member_values(double nuj, const float* p, int nm
 #pragma unroll
   for (int k = 0; k < 4; ++k)
     if (k == am) parts[k] = pa > 0.0 ? pa : 0.0;
-  if (bc.active && nuj > 0.0) {
+  if (bc[0] != 0.0 && nuj > 0.0) {
     const double inv = __drcp_rn(nuj);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       double t = 0.0, u = 0.0;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        t = __dadd_rn(t, __dmul_rn(bc.O[k][j], parts[j]));
-        u = __dadd_rn(u, __dmul_rn(bc.P[k][j], parts[j]));
+        t = __dadd_rn(t, __dmul_rn(bc[1 + 4 * k + j], parts[j]));
+        u = __dadd_rn(u, __dmul_rn(bc[17 + 4 * k + j], parts[j]));
       }
       out[k] = __dadd_rn(__dadd_rn(parts[k], __dmul_rn(parts[k], __dmul_rn(t, inv))), u);
     }
@@ -697,12 +693,6 @@ __device__ void split_cell(const SweepParams& p, const int J, unsigned char* sme
     return;
   }
   assemble(p, cc, ints, L1, L2, b2, BB, nuJ);
-  double massJ = 0.0;
-  {
-    double v = 0.0;
-    for (int t = tid; t < BB; t += T) v += nuJ[t];
-    massJ = block_sum1_d(v, red);
-  }
   // plan potential of this sweep (written by solve_kernel in the same gauge)
   constexpr int NXX = NX * NX;
   for (int t = tid; t < NXX; t += T) {
@@ -748,145 +738,170 @@ __device__ void split_cell(const SweepParams& p, const int J, unsigned char* sme
   __syncthreads();
   int mq[4];
   for (int k = 0; k < 4; ++k) mq[k] = cc.quad[k];
-  // acc[0..3]: split masses; acc[4 + 6k + .]: M0, M1a, M1b, G0, G1, M2 of
-  // member k; acc[28 + pair]: overlaps sum parts_a parts_b / nu_J (balance)
-  double acc[34];
-  for (int k = 0; k < 34; ++k) acc[k] = 0.0;
+  // acc[0..3]: split masses (= moment M0); acc[4 + 5k + .]: M1a, M1b, G0, G1,
+  // M2 of member k; acc[24 + pair]: overlaps sum parts_a parts_b / nu_J (R8)
+  double acc[32];
+#pragma unroll
+  for (int q = 0; q < 32; ++q) acc[q] = 0.0;
   for (int o = tid; o < BB; o += T) {
     const int l1 = o / b2, l2 = o - l1 * b2;
     const float lt = (float)l1 - fo1;
     float S[4], Ex1[4], Ex2[4], Exx[4];
-    for (int k = 0; k < nmem; ++k) {
-      const int h1 = mq[k] >> 1, h2 = mq[k] & 1;
-      const float* ur = Ub + (h2 * n1) * b2 + l2;
-      const float* r1 = Rb + (h2 * n1) * b2 + l2;
-      const float* r2 = Rb + c2 * n1 * b2 + (h2 * n1) * b2 + l2;
-      float sh = kNeg;
-      for (int k1 = h1 * s; k1 < h1 * s + s; ++k1) { const float d = (float)k1 - lt; sh = fmaxf(sh, ur[k1 * b2] - w * d * d); }
-      float sum = 0.f, a1 = 0.f, a2 = 0.f, aq = 0.f;
-      for (int k1 = h1 * s; k1 < h1 * s + s; ++k1) {
-        const float d = (float)k1 - lt;
-        const float tt = ex2f(ur[k1 * b2] - w * d * d - sh);
-        const float xq = (float)(k1 - h1 * s) - cen;
-        sum += tt;
-        a1 += tt * xq;
-        a2 += tt * r1[k1 * b2];
-        aq += tt * (xq * xq + r2[k1 * b2]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      S[k] = kNeg; Ex1[k] = 0.f; Ex2[k] = 0.f; Exx[k] = 0.f;
+      if (k < nmem) {
+        const int h1 = mq[k] >> 1, h2 = mq[k] & 1;
+        const float* ur = Ub + (h2 * n1) * b2 + l2;
+        const float* r1 = Rb + (h2 * n1) * b2 + l2;
+        const float* r2 = Rb + c2 * n1 * b2 + (h2 * n1) * b2 + l2;
+        float sh = kNeg;
+        for (int k1 = h1 * s; k1 < h1 * s + s; ++k1) { const float d = (float)k1 - lt; sh = fmaxf(sh, ur[k1 * b2] - w * d * d); }
+        float sum = 0.f, a1 = 0.f, a2 = 0.f, aq = 0.f;
+        for (int k1 = h1 * s; k1 < h1 * s + s; ++k1) {
+          const float d = (float)k1 - lt;
+          const float tt = ex2f(ur[k1 * b2] - w * d * d - sh);
+          const float xq = (float)(k1 - h1 * s) - cen;
+          sum += tt;
+          a1 += tt * xq;
+          a2 += tt * r1[k1 * b2];
+          aq += tt * (xq * xq + r2[k1 * b2]);
+        }
+        const float inv = 1.0f / sum;
+        S[k] = sh + lg2f(sum);
+        Ex1[k] = a1 * inv;
+        Ex2[k] = a2 * inv;
+        Exx[k] = aq * inv;
       }
-      const float inv = 1.0f / sum;
-      S[k] = sh + lg2f(sum);
-      Ex1[k] = a1 * inv;
-      Ex2[k] = a2 * inv;
-      Exx[k] = aq * inv;
     }
     float mx = S[0];
-    for (int k = 1; k < nmem; ++k) mx = fmaxf(mx, S[k]);
+#pragma unroll
+    for (int k = 1; k < 4; ++k) mx = fmaxf(mx, S[k]);
     float es[4], tot = 0.f;
-    for (int k = 0; k < nmem; ++k) { es[k] = ex2f(S[k] - mx); tot += es[k]; }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { es[k] = k < nmem ? ex2f(S[k] - mx) : 0.f; tot += es[k]; }
     const float inv = 1.0f / tot;
-    float pk[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int k = 0; k < nmem; ++k) pk[k] = es[k] * inv;
+    float pk[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) pk[k] = es[k] * inv;
     P0[o] = pk[0];
     P1[o] = pk[1];
     P2[o] = pk[2];
     P3[o] = pk[3];
-    // split masses and pairwise overlaps (balance, R8) of nu_k = nu_J p_k
     const double nj = nuJ[o];
     if (nj > 0.0) {
-      // identity split: the largest share takes the remainder (exact sum)
+      // identity split (the largest share takes the remainder: exact sum)
       double v[4];
-      {
-        int am = 0;
-        for (int q = 1; q < nmem; ++q)
-          if (pk[q] > pk[am]) am = q;
-        double rest = 0.0;
-        for (int q = 0; q < nmem; ++q) {
-          v[q] = 0.0;
-          if (q != am) { v[q] = __dmul_rn(nj, (double)pk[q]); rest = __dadd_rn(rest, v[q]); }
-        }
-        const double pa = __dsub_rn(nj, rest);
-        v[am] = pa > 0.0 ? pa : 0.0;
+      int am = 0;
+#pragma unroll
+      for (int q = 1; q < 4; ++q)
+        if (q < nmem && pk[q] > pk[am]) am = q;
+      double rest = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        v[q] = 0.0;
+        if (q < nmem && q != am) { v[q] = __dmul_rn(nj, (double)pk[q]); rest = __dadd_rn(rest, v[q]); }
       }
-      const double inv = 1.0 / nj;
-      for (int a = 0; a < nmem; ++a) {
+      const double pa = __dsub_rn(nj, rest);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q == am) v[q] = pa > 0.0 ? pa : 0.0;
+      // split masses and pairwise overlaps (balance, R8)
+      const double invj = 1.0 / nj;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
         acc[a] += v[a];
-        for (int b = a + 1; b < nmem; ++b) acc[28 + pair_id(a, b)] += v[a] * v[b] * inv;
+#pragma unroll
+        for (int b = a + 1; b < 4; ++b) acc[24 + pair_id(a, b)] += v[a] * v[b] * invj;
       }
-    }
-    // plan moments of the pre-balance marginals nu_k^pre = nu_J p_k (R13)
-    if (nj > 0.0) {
-      for (int k = 0; k < nmem; ++k) {
-        const int h1 = mq[k] >> 1, h2 = mq[k] & 1;
-        const double v = nj * (double)pk[k];
-        const double y1 = (double)(L1 + l1 - cc.r0 - h1 * s) - (double)cen;
-        const double y2 = (double)(L2 + l2 - cc.c0 - h2 * s) - (double)cen;
-        double* a = acc + 4 + 6 * k;
-        a[0] += v;
-        a[1] += v * y1;
-        a[2] += v * y2;
-        a[3] += v * (double)Exx[k];
-        a[4] += v * (y1 * (double)Ex1[k] + y2 * (double)Ex2[k]);
-        a[5] += v * (y1 * y1 + y2 * y2);
+      // plan moments of the pre-balance marginals nu_k^pre = nu_J p_k (R13)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (q < nmem) {
+          const int h1 = mq[q] >> 1, h2 = mq[q] & 1;
+          const double vv = nj * (double)pk[q];
+          const double y1 = (double)(L1 + l1 - cc.r0 - h1 * s) - (double)cen;
+          const double y2 = (double)(L2 + l2 - cc.c0 - h2 * s) - (double)cen;
+          acc[4 + 5 * q + 0] += vv * y1;
+          acc[4 + 5 * q + 1] += vv * y2;
+          acc[4 + 5 * q + 2] += vv * (double)Exx[q];
+          acc[4 + 5 * q + 3] += vv * (y1 * (double)Ex1[q] + y2 * (double)Ex2[q]);
+          acc[4 + 5 * q + 4] += vv * (y1 * y1 + y2 * y2);
+        }
       }
     }
   }
   __syncthreads();
-  {
-    // acc[32..33] hold the (3,? ) overlaps of pairs 4 and 5; reduce 32 + 2
-    const double x32 = acc[32], x33 = acc[33];
-    block_sum32_d(acc, red, red + 160);
-    const double s32 = block_sum1_d(x32, red + 200);
-    const double s33 = block_sum1_d(x33, red + 232);
-    for (int k = 0; k < 32; ++k) acc[k] = red[160 + k];
-    acc[32] = s32;
-    acc[33] = s33;
-  }
-  // ---- a4: balance coefficients (reading R8) ------------------------------
-  BalanceCoef bc;
-  {
+  block_sum32_d(acc, red, red + 160);
+#pragma unroll
+  for (int q = 0; q < 32; ++q) acc[q] = red[160 + q];
+  const double massJ = acc[0] + acc[1] + acc[2] + acc[3];
+  // ---- a4: balance coefficients (reading R8), in shared memory -----------
+  // Warp 0 computes them lane-parallel: lane 4 d + r -> O_dr, lane 16 + 4 k +
+  // j -> P_kj (see oracle/domdec.py:balance for the definition).
+  double* bc = red + 240;
+  if (tid < 32) {
     double delta[4], Dsum = 0.0;
     bool any_d = false, any_r = false;
-    bc.active = 0;
-    for (int a = 0; a < 4; ++a) {
-      delta[a] = 0.0;
-      for (int b = 0; b < 4; ++b) { bc.O[a][b] = 0.0; bc.P[a][b] = 0.0; }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      delta[q] = 0.0;
+      if (q < nmem) {
+        delta[q] = acc[q] - p.m[cc.mem[q]] * massJ / muXJ;
+        if (delta[q] > 0) { any_d = true; Dsum += delta[q]; }
+        if (delta[q] < 0) any_r = true;
+      }
     }
-    for (int q = 0; q < nmem; ++q) {
-      const double t = p.m[cc.mem[q]] * massJ / muXJ;
-      delta[q] = acc[q] - t;
-      if (delta[q] > 0) { any_d = true; Dsum += delta[q]; }
-      if (delta[q] < 0) any_r = true;
-    }
-    if (any_d && any_r) {
-      bc.active = 1;
-      for (int d = 0; d < nmem; ++d) {
-        if (!(delta[d] > 0)) continue;
+    const bool active = any_d && any_r;
+    // theta of every donor (redundant per lane, compile-time indices)
+    double theta[4];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      theta[d] = 0.0;
+      if (active && d < nmem && delta[d] > 0) {
         bool zeroT = false;
         double L = 0.0;
-        for (int r = 0; r < nmem; ++r) {
-          if (!(delta[r] < 0)) continue;
-          const double T = acc[28 + (d < r ? pair_id(d, r) : pair_id(r, d))];
-          if (!(T > 0.0)) { zeroT = true; continue; }
-          L += delta[d] * (-delta[r]) / Dsum / T;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if (r < nmem && r != d && delta[r] < 0) {
+            const double T = acc[24 + (d < r ? pair_id(d, r) : pair_id(r, d))];
+            if (!(T > 0.0)) zeroT = true;
+            else L += delta[d] * (-delta[r]) / Dsum / T;
+          }
         }
         const double l = delta[d] / acc[d];
-        const double theta = zeroT ? 0.0 : (L <= 1.0 ? 1.0 : (1.0 - l) / (L - l));
-        for (int r = 0; r < nmem; ++r) {
-          if (!(delta[r] < 0)) continue;
-          const double f = delta[d] * (-delta[r]) / Dsum;
-          const double T = acc[28 + (d < r ? pair_id(d, r) : pair_id(r, d))];
-          if (theta > 0.0) {
-            const double a = f * theta / T;
-            bc.O[d][r] -= a;
-            bc.O[r][d] += a;
+        theta[d] = zeroT ? 0.0 : (L <= 1.0 ? 1.0 : (1.0 - l) / (L - l));
+      }
+    }
+    const int a = (tid & 15) >> 2, b = tid & 3;   // entry (a, b)
+    double val = 0.0;
+    if (active) {
+#pragma unroll
+      for (int d = 0; d < 4; ++d) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if (d < nmem && r < nmem && delta[d] > 0 && delta[r] < 0) {
+            const double f = delta[d] * (-delta[r]) / Dsum;
+            if (tid < 16) {            // O: O_dr -= f theta / T, O_rd += f theta / T
+              const double T = acc[24 + (d < r ? pair_id(d, r) : pair_id(r, d))];
+              if (theta[d] > 0.0) {
+                const double x = f * theta[d] / T;
+                if (a == d && b == r) val -= x;
+                if (a == r && b == d) val += x;
+              }
+            } else {                   // P: P_dd -= f (1 - theta) / M_d, P_rd += same
+              const double x = f * (1.0 - theta[d]) / acc[d];
+              if (a == d && b == d) val -= x;
+              if (a == r && b == d) val += x;
+            }
           }
-          const double b = f * (1.0 - theta) / acc[d];
-          bc.P[d][d] -= b;
-          bc.P[r][d] += b;
         }
       }
     }
+    bc[1 + tid] = val;   // tid < 16 -> O, tid >= 16 -> P (bc[17 + 4a + b])
+    if (tid == 0) bc[0] = active ? 1.0 : 0.0;
   }
+  __syncthreads();
   // ---- a5: truncate + minimal box -----------------------------------------
   // layout: ints[16 + 4k + 0] = min row, +1 = max row, +2 = min col, +3 = max col
   if (tid < 4) {
@@ -927,30 +942,52 @@ __device__ void split_cell(const SweepParams& p, const int J, unsigned char* sme
     copy_unchanged(2);
     return;
   }
-  // ---- write the new boxes -------------------------------------------------
+  // ---- write the new boxes: one pass over the union of the member boxes,
+  // every entry evaluated once and scattered to the boxes containing it ----
   unsigned long long wbytes = 0;
-  for (int k = 0; k < nmem; ++k) {
-    const int i = cc.mem[k];
-    const int mn1 = ints[16 + 4 * k], mx1 = ints[16 + 4 * k + 1];
-    const int mn2 = ints[16 + 4 * k + 2], mx2 = ints[16 + 4 * k + 3];
-    const int e1 = mx1 - mn1 + 1, e2 = mx2 - mn2 + 1;
-    double* dst = p.pool_out + (long long)i * slot;
-    for (int t = tid; t < e1 * e2; t += T) {
-      const int r = t / e2, c = t - r * e2;
-      const int o = (mn1 + r) * b2 + mn2 + c;
+  int bx[4][4];
+  int umn1 = 1 << 30, umx1 = -1, umn2 = 1 << 30, umx2 = -1;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    bx[q][0] = ints[16 + 4 * q]; bx[q][1] = ints[16 + 4 * q + 1];
+    bx[q][2] = ints[16 + 4 * q + 2]; bx[q][3] = ints[16 + 4 * q + 3];
+    if (q < nmem) {
+      umn1 = min(umn1, bx[q][0]); umx1 = max(umx1, bx[q][1]);
+      umn2 = min(umn2, bx[q][2]); umx2 = max(umx2, bx[q][3]);
+      wbytes += (unsigned long long)(bx[q][1] - bx[q][0] + 1) * (bx[q][3] - bx[q][2] + 1) * 8ull;
+    }
+  }
+  {
+    const int ue2 = umx2 - umn2 + 1, un = (umx1 - umn1 + 1) * ue2;
+    for (int t = tid; t < un; t += T) {
+      const int l1 = umn1 + t / ue2, l2 = umn2 + t % ue2;
+      const int o = l1 * b2 + l2;
       const float pk[4] = {P0[o], P1[o], P2[o], P3[o]};
       double v[4];
       member_values(nuJ[o], pk, nmem, bc, v);
-      dst[t] = v[k] >= p.tau ? v[k] : 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (q < nmem && l1 >= bx[q][0] && l1 <= bx[q][1] && l2 >= bx[q][2] && l2 <= bx[q][3]) {
+          const int e2q = bx[q][3] - bx[q][2] + 1;
+          p.pool_out[(long long)cc.mem[q] * slot + (l1 - bx[q][0]) * e2q + (l2 - bx[q][2])] =
+              v[q] >= p.tau ? v[q] : 0.0;
+        }
+      }
     }
-    if (tid == 0) {
-      p.off_out[2 * i] = L1 + mn1;
-      p.off_out[2 * i + 1] = L2 + mn2;
-      p.ext_out[2 * i] = e1;
-      p.ext_out[2 * i + 1] = e2;
-      for (int q = 0; q < 6; ++q) p.mom[6 * i + q] = acc[4 + 6 * k + q];
+  }
+  if (tid < nmem) {
+    const int q = tid, i = cc.mem[q];
+    p.off_out[2 * i] = L1 + bx[q][0];
+    p.off_out[2 * i + 1] = L2 + bx[q][2];
+    p.ext_out[2 * i] = bx[q][1] - bx[q][0] + 1;
+    p.ext_out[2 * i + 1] = bx[q][3] - bx[q][2] + 1;
+  }
+  if (tid == 0) {
+    for (int q = 0; q < nmem; ++q)
+    {
+      p.mom[6 * cc.mem[q]] = acc[q];
+      for (int c = 0; c < 5; ++c) p.mom[6 * cc.mem[q] + 1 + c] = acc[4 + 5 * q + c];
     }
-    wbytes += (unsigned long long)e1 * e2 * 8ull;
   }
   if (tid == 0) {
     p.stats[J].dropped = drop[0];
