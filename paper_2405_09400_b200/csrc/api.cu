@@ -24,11 +24,12 @@ __global__ void k_init_mu(const double* __restrict__ mu, float* __restrict__ muf
 }
 
 // Y-marginal of the stored state: scatter-add all boxes (diagnostic, fp64).
-__global__ void k_scatter_boxes(const double* __restrict__ pool, const int* __restrict__ off,
-                                const int* __restrict__ ext, long long slot, int N2, double* __restrict__ acc) {
+__global__ void k_scatter_boxes(const double* __restrict__ pool, const long long* __restrict__ pos,
+                                const int* __restrict__ off, const int* __restrict__ ext, int N2,
+                                double* __restrict__ acc) {
   const int i = blockIdx.x;
   const int r0 = off[2 * i], c0 = off[2 * i + 1], e1 = ext[2 * i], e2 = ext[2 * i + 1];
-  const double* src = pool + (long long)i * slot;
+  const double* src = pool + pos[i];
   for (int t = threadIdx.x; t < e1 * e2; t += blockDim.x) {
     const int r = t / e2, c = t - r * e2;
     atomicAdd(&acc[(long long)(r0 + r) * N2 + c0 + c], src[t]);
@@ -141,7 +142,8 @@ void free_ctx(dd_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  void* ptrs[] = {c->d_mu, c->d_log2mu, c->d_nu, c->d_m, c->d_q, c->d_pool[0], c->d_pool[1], c->d_off[0],
+  void* ptrs[] = {c->d_pos[0], c->d_pos[1], c->d_poolctr, c->d_scratch_huge,
+                  c->d_mu, c->d_log2mu, c->d_nu, c->d_m, c->d_q, c->d_pool[0], c->d_pool[1], c->d_off[0],
                   c->d_off[1], c->d_ext[0], c->d_ext[1], c->d_cells[0], c->d_cells[1], c->d_alpha[0],
                   c->d_alpha[1], c->d_gauge[0], c->d_gauge[1], c->d_stats[0], c->d_stats[1], c->d_totals[0],
                   c->d_totals[1], c->d_mom, c->d_xbar, c->d_var, c->d_cbar, c->d_C, c->d_w, c->d_mcf,
@@ -273,8 +275,14 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c) 
     c->err = "composite box capacity too large for shared memory (eps too large for this build)";
     return DD_ERR_ARG;
   }
-  side = std::max(side, std::min(c->ccap_big, 2 * s + 2 * (int)std::ceil(tail) + 24));
-  c->slot = c->opt.slot_cap > 0 ? c->opt.slot_cap : std::max<long long>((long long)side * side, maxbox);
+  // variable-size pool (bump-allocated each sweep): average capacity per basic
+  // cell from the eps blur, generous; the total is what matters
+  side = std::max(side, 2 * s + 2 * (int)std::ceil(tail) + 12);
+  long long init_total = 0;
+  for (int i = 0; i < I; ++i) init_total += (long long)P->init_ext[2 * i] * P->init_ext[2 * i + 1];
+  const long long per_cell = c->opt.slot_cap > 0 ? c->opt.slot_cap : (long long)side * side;
+  c->pool_cap = std::max<long long>((long long)I * per_cell, 2 * init_total);
+  c->ccap_huge = std::max(c->N1, c->N2);
   // ---- device --------------------------------------------------------------
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= c->device) {
@@ -294,9 +302,13 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c) 
   TRY(dalloc(c, &c->d_scratch, NN));
   TRY(dalloc(c, &c->d_red, 64));
   TRY(dalloc(c, &c->d_cum, 1));
+  TRY(dalloc(c, &c->d_poolctr, 2));
+  c->scratch_stride = (sweep_scratch_bytes(c->ccap_huge, s) + 255) & ~size_t(255);
+  TRY(dalloc(c, &c->d_scratch_huge, 16 * c->scratch_stride));
   DD_CUDA(cudaMemsetAsync(c->d_cum, 0, sizeof(SweepTotals), c->stream));
   for (int b = 0; b < 2; ++b) {
-    TRY(dalloc(c, &c->d_pool[b], (size_t)I * c->slot));
+    TRY(dalloc(c, &c->d_pool[b], (size_t)c->pool_cap));
+    TRY(dalloc(c, &c->d_pos[b], (size_t)I));
     TRY(dalloc(c, &c->d_off[b], (size_t)I * 2));
     TRY(dalloc(c, &c->d_ext[b], (size_t)I * 2));
     c->h_cells[b] = build_partition(c->n1, c->n2, s, b);
@@ -305,7 +317,7 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c) 
     TRY(dalloc(c, &c->d_alpha[b], NN));
     TRY(dalloc(c, &c->d_gauge[b], (size_t)c->ncells[b] * 2));
     TRY(dalloc(c, &c->d_stats[b], c->ncells[b]));
-    if (b == 1) TRY(dalloc(c, &c->d_ovf, (size_t)std::max(c->ncells[0], c->ncells[1]) + 4));
+    if (b == 1) TRY(dalloc(c, &c->d_ovf, 2 * (size_t)std::max(c->ncells[0], c->ncells[1]) + 8));
     TRY(dalloc(c, &c->d_totals[b], 1));
     DD_CUDA(cudaMemcpyAsync(c->d_cells[b], c->h_cells[b].data(), sizeof(CompCell) * c->ncells[b],
                             cudaMemcpyHostToDevice, st));
@@ -329,12 +341,19 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c) 
   DD_CUDA(cudaMemcpyAsync(c->d_q, q.data(), I * 8, cudaMemcpyHostToDevice, st));
   // initial boxes -> pool[0] (slots)
   {
-    std::vector<double> pool((size_t)I * c->slot, 0.0);
+    std::vector<double> pool((size_t)init_total);
+    std::vector<long long> pos(I);
+    long long at = 0;
     for (int i = 0; i < I; ++i) {
       const long long len = (long long)P->init_ext[2 * i] * P->init_ext[2 * i + 1];
-      std::memcpy(&pool[(size_t)i * c->slot], P->init_data + P->init_pos[i], len * 8);
+      std::memcpy(&pool[at], P->init_data + P->init_pos[i], len * 8);
+      pos[i] = at;
+      at += len;
     }
+    const unsigned long long ctr0[2] = {(unsigned long long)init_total, 0ull};
     DD_CUDA(cudaMemcpyAsync(c->d_pool[0], pool.data(), pool.size() * 8, cudaMemcpyHostToDevice, st));
+    DD_CUDA(cudaMemcpyAsync(c->d_pos[0], pos.data(), I * 8, cudaMemcpyHostToDevice, st));
+    DD_CUDA(cudaMemcpyAsync(c->d_poolctr, ctr0, 16, cudaMemcpyHostToDevice, st));
     DD_CUDA(cudaMemcpyAsync(c->d_off[0], P->init_off, I * 8, cudaMemcpyHostToDevice, st));
     DD_CUDA(cudaMemcpyAsync(c->d_ext[0], P->init_ext, I * 8, cudaMemcpyHostToDevice, st));
     DD_CUDA(cudaStreamSynchronize(st));   // host staging buffer goes out of scope
@@ -378,12 +397,17 @@ dd_status domdec_sweep(dd_ctx* c, dd_partition part, dd_sweep_stats* stats) {
   p.cells = c->d_cells[b];
   p.ncells = c->ncells[b];
   p.pool_in = c->d_pool[c->cur];
+  p.pos_in = c->d_pos[c->cur];
   p.off_in = c->d_off[c->cur];
   p.ext_in = c->d_ext[c->cur];
   p.pool_out = c->d_pool[1 - c->cur];
+  p.pos_out = c->d_pos[1 - c->cur];
   p.off_out = c->d_off[1 - c->cur];
   p.ext_out = c->d_ext[1 - c->cur];
-  p.slot = c->slot;
+  p.pool_ctr = c->d_poolctr + (1 - c->cur);
+  p.pool_cap = c->pool_cap;
+  p.scratch = c->d_scratch_huge;
+  p.scratch_stride = c->scratch_stride;
   p.ccap = c->ccap;
   p.alpha = c->d_alpha[b];
   p.gauge = c->d_gauge[b];
@@ -398,9 +422,12 @@ dd_status domdec_sweep(dd_ctx* c, dd_partition part, dd_sweep_stats* stats) {
   p.cum = c->d_cum;
   p.mom = c->d_mom;
   DD_CUDA(cudaMemsetAsync(c->d_totals[b], 0, sizeof(SweepTotals), c->stream));
+  const int mc = std::max(c->ncells[0], c->ncells[1]);
   p.ovf_count = c->d_ovf;
-  p.ovf_list = c->d_ovf + 1;
-  DD_CUDA(launch_sweep(p, c->ccap, c->ccap_big, c->stream));
+  p.ovf2_count = c->d_ovf + 1;
+  p.ovf_list = c->d_ovf + 8;
+  p.ovf2_list = c->d_ovf + 8 + mc;
+  DD_CUDA(launch_sweep(p, c->ccap, c->ccap_big, c->ccap_huge, c->stream));
   c->cur = 1 - c->cur;
   ++c->n_sweeps;
   c->alpha_valid[b] = 1;
@@ -439,8 +466,8 @@ dd_status marginal_error(dd_ctx* c, double* l1_x, double* l1_y) {
     DD_CUDA(cudaMemcpyAsync(&hx, c->d_red, 8, cudaMemcpyDeviceToHost, c->stream));
   }
   DD_CUDA(cudaMemsetAsync(c->d_scratch, 0, NN * 8, c->stream));
-  k_scatter_boxes<<<c->I, 128, 0, c->stream>>>(c->d_pool[c->cur], c->d_off[c->cur], c->d_ext[c->cur], c->slot,
-                                               c->N2, c->d_scratch);
+  k_scatter_boxes<<<c->I, 128, 0, c->stream>>>(c->d_pool[c->cur], c->d_pos[c->cur], c->d_off[c->cur],
+                                               c->d_ext[c->cur], c->N2, c->d_scratch);
   DD_CUDA(cudaGetLastError());
   k_l1_diff<<<1, 1024, 0, c->stream>>>(c->d_scratch, c->d_nu, NN, c->d_red + 8);
   DD_CUDA(cudaGetLastError());
@@ -477,13 +504,18 @@ dd_status domdec_export_cells(dd_ctx* c, int32_t* off, int32_t* ext, int64_t* po
     c->err = "data_cap too small";
     return DD_ERR_ARG;
   }
-  std::vector<double> pool((size_t)I * c->slot);
-  DD_CUDA(cudaMemcpyAsync(pool.data(), c->d_pool[c->cur], pool.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  unsigned long long used = 0;
+  std::vector<long long> hp(I);
+  DD_CUDA(cudaMemcpyAsync(&used, c->d_poolctr + c->cur, 8, cudaMemcpyDeviceToHost, c->stream));
+  DD_CUDA(cudaMemcpyAsync(hp.data(), c->d_pos[c->cur], I * 8, cudaMemcpyDeviceToHost, c->stream));
+  DD_CUDA(cudaStreamSynchronize(c->stream));
+  std::vector<double> pool((size_t)used + 1);
+  DD_CUDA(cudaMemcpyAsync(pool.data(), c->d_pool[c->cur], used * 8, cudaMemcpyDeviceToHost, c->stream));
   DD_CUDA(cudaStreamSynchronize(c->stream));
   int64_t p = 0;
   for (int i = 0; i < I; ++i) {
     const int64_t len = (int64_t)he[2 * i] * he[2 * i + 1];
-    std::memcpy(data + p, &pool[(size_t)i * c->slot], len * 8);
+    std::memcpy(data + p, &pool[(size_t)hp[i]], len * 8);
     p += len;
   }
   return DD_OK;

@@ -23,13 +23,18 @@ struct dd_ctx {
   double* d_m = nullptr;
   int64_t* d_q = nullptr;
   double* d_pool[2] = {nullptr, nullptr};
+  long long* d_pos[2] = {nullptr, nullptr};          // [I] start of box i
+  unsigned long long* d_poolctr = nullptr;           // [2] elements used per pool
+  long long pool_cap = 0;                            // elements per pool
+  int ccap_huge = 0;
+  unsigned char* d_scratch_huge = nullptr;           // global scratch of the huge class
+  size_t scratch_stride = 0;
   int* d_off[2] = {nullptr, nullptr};
   int* d_ext[2] = {nullptr, nullptr};
   int cur = 0;
-  long long slot = 0;
   int ccap = 0;        // small size class (composite hull side)
   int ccap_big = 0;    // large size class
-  int* d_ovf = nullptr; // [max ncells + 1] deferred-cell queue (count at [0])
+  int* d_ovf = nullptr; // [2 (counts) + 2 * max ncells] deferred-cell lists of the size classes
   dd::CompCell* d_cells[2] = {nullptr, nullptr};
   int ncells[2] = {0, 0};
   std::vector<dd::CompCell> h_cells[2];

@@ -13,6 +13,7 @@
 // Step 3 (F3): nu_hat_j = sum_{i in N(j)} (w_ij / q_i) nu_i (Lemma, Eq.
 // flow-update-cell-marginals PAPER.md:453-456), bounding-box merge + truncate
 // + minimal box, one CTA per changed cell.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -91,23 +92,46 @@ __global__ void k_flow_costs(const double* __restrict__ mom, const double* __res
   }
 }
 
-// F3: one CTA per target cell j.  Writes the new box of every changed cell
-// into the spare buffer; k_copy_back then moves it into the live buffer.
+// F3: one CTA per target cell j writes its new box into the spare pool
+// (bump-allocated); unchanged cells (w_jj = q_j) are copied.  The weighted
+// sum is accumulated in place in the output pool on the hull of the
+// contributing boxes (fixed order: self, from up, down, left, right; explicit
+// _rn operations), truncated, and compacted to the minimal box.
 __global__ void k_apply_flow(const long long* __restrict__ w, const long long* __restrict__ q, int n1, int n2,
-                             const double* __restrict__ pool, const int* __restrict__ off,
-                             const int* __restrict__ ext, double* __restrict__ pool_new, int* __restrict__ off_new,
-                             int* __restrict__ ext_new, long long slot, int cap_side, double tau,
+                             const double* __restrict__ pool, const long long* __restrict__ pos,
+                             const int* __restrict__ off, const int* __restrict__ ext, double* __restrict__ pool_new,
+                             long long* __restrict__ pos_new, int* __restrict__ off_new, int* __restrict__ ext_new,
+                             unsigned long long* __restrict__ ctr, long long cap, double tau,
                              unsigned long long* __restrict__ counters, double* __restrict__ dropped) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  double* acc = (double*)smem;
+  extern __shared__ __align__(16) double rowbuf[];
   __shared__ int src[5];
   __shared__ double frac[5];
   __shared__ int nsrc;
   __shared__ int bnd[4];
+  __shared__ long long base;
+  __shared__ int mm[4];
   __shared__ double dsum[32];
-  const int j = blockIdx.x;
-  if (w[5LL * j] == q[j]) return;   // no inflow from a neighbour: nu_j unchanged
-  if (threadIdx.x == 0) {
+  const int j = blockIdx.x, tid = threadIdx.x, T = blockDim.x;
+  if (w[5LL * j] == q[j]) {   // no inflow from a neighbour: nu_j unchanged
+    const long long len = (long long)ext[2 * j] * ext[2 * j + 1];
+    if (tid == 0) {
+      long long b = (long long)atomicAdd(ctr, (unsigned long long)len);
+      if (b + len > cap) { b = -1; atomicAdd(&counters[1], 1ull); }
+      base = b;
+    }
+    __syncthreads();
+    if (base < 0) return;
+    for (long long t = tid; t < len; t += T) pool_new[base + t] = pool[pos[j] + t];
+    if (tid == 0) {
+      pos_new[j] = base;
+      off_new[2 * j] = off[2 * j];
+      off_new[2 * j + 1] = off[2 * j + 1];
+      ext_new[2 * j] = ext[2 * j];
+      ext_new[2 * j + 1] = ext[2 * j + 1];
+    }
+    return;
+  }
+  if (tid == 0) {
     int k = 0;
     if (w[5LL * j] > 0) { src[k] = j; frac[k] = (double)w[5LL * j] / (double)q[j]; ++k; }
     // from up (its 'down' arc 2), down ('up' 1), left ('right' 4), right ('left' 3)
@@ -130,32 +154,32 @@ __global__ void k_apply_flow(const long long* __restrict__ w, const long long* _
       U2 = max(U2, off[2 * i + 1] + ext[2 * i + 1]);
     }
     bnd[0] = L1; bnd[1] = L2; bnd[2] = U1 - L1; bnd[3] = U2 - L2;
+    const long long A = (long long)bnd[2] * bnd[3];
+    long long b = (long long)atomicAdd(ctr, (unsigned long long)A);
+    if (b + A > cap) { b = -1; atomicAdd(&counters[1], 1ull); }
+    base = b;
+    mm[0] = 1 << 30; mm[1] = -1; mm[2] = 1 << 30; mm[3] = -1;
   }
   __syncthreads();
+  if (base < 0) return;
   const int L1 = bnd[0], L2 = bnd[1], b1 = bnd[2], b2 = bnd[3];
-  if (b1 > cap_side || b2 > cap_side) {
-    if (threadIdx.x == 0) atomicAdd(&counters[1], 1ull);
-    return;
-  }
-  for (int t = threadIdx.x; t < b1 * b2; t += blockDim.x) acc[t] = 0.0;
+  double* acc = pool_new + base;
+  for (int t = tid; t < b1 * b2; t += T) acc[t] = 0.0;
   __syncthreads();
   for (int k = 0; k < nsrc; ++k) {
     const int i = src[k];
     const double f = frac[k];
     const int r0 = off[2 * i] - L1, c0 = off[2 * i + 1] - L2, e1 = ext[2 * i], e2 = ext[2 * i + 1];
-    const double* d = pool + (long long)i * slot;
-    for (int t = threadIdx.x; t < e1 * e2; t += blockDim.x) {
+    const double* d = pool + pos[i];
+    for (int t = tid; t < e1 * e2; t += T) {
       const int r = t / e2, c = t - r * e2;
       double* a = &acc[(r0 + r) * b2 + c0 + c];
       *a = __dadd_rn(*a, __dmul_rn(f, d[t]));
     }
     __syncthreads();
   }
-  __shared__ int mm[4];
-  if (threadIdx.x == 0) { mm[0] = 1 << 30; mm[1] = -1; mm[2] = 1 << 30; mm[3] = -1; }
-  __syncthreads();
   double dr = 0.0;
-  for (int t = threadIdx.x; t < b1 * b2; t += blockDim.x) {
+  for (int t = tid; t < b1 * b2; t += T) {
     const double v = acc[t];
     const int r = t / b2, c = t - r * b2;
     if (v >= tau) {
@@ -165,47 +189,33 @@ __global__ void k_apply_flow(const long long* __restrict__ w, const long long* _
     }
   }
   for (int o = 16; o > 0; o >>= 1) dr += __shfl_xor_sync(0xffffffffu, dr, o);
-  if ((threadIdx.x & 31) == 0) dsum[threadIdx.x >> 5] = dr;
+  if ((tid & 31) == 0) dsum[tid >> 5] = dr;
   __syncthreads();
-  const int e1 = mm[1] - mm[0] + 1, e2 = mm[3] - mm[2] + 1;
-  if (mm[1] < mm[0] || (long long)e1 * e2 > slot) {
-    if (threadIdx.x == 0) atomicAdd(&counters[1], 1ull);
+  if (mm[1] < mm[0]) {
+    if (tid == 0) atomicAdd(&counters[1], 1ull);
     return;
   }
-  double* dst = pool_new + (long long)j * slot;
-  for (int t = threadIdx.x; t < e1 * e2; t += blockDim.x) {
-    const int r = t / e2, c = t - r * e2;
-    const double v = acc[(mm[0] + r) * b2 + mm[2] + c];
-    dst[t] = v >= tau ? v : 0.0;
+  const int e1 = mm[1] - mm[0] + 1, e2 = mm[3] - mm[2] + 1;
+  // in-place compaction to the minimal box, one row at a time through shared memory
+  for (int r = 0; r < e1; ++r) {
+    for (int c = tid; c < e2; c += T) {
+      const double v = acc[(mm[0] + r) * b2 + mm[2] + c];
+      rowbuf[c] = v >= tau ? v : 0.0;
+    }
+    __syncthreads();
+    for (int c = tid; c < e2; c += T) acc[r * e2 + c] = rowbuf[c];
+    __syncthreads();
   }
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
+    pos_new[j] = base;
     off_new[2 * j] = L1 + mm[0];
     off_new[2 * j + 1] = L2 + mm[2];
     ext_new[2 * j] = e1;
     ext_new[2 * j + 1] = e2;
     double s = 0;
-    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += dsum[k];
+    for (int k = 0; k < (int)(T >> 5); ++k) s += dsum[k];
     atomicAdd(dropped, s);
     atomicAdd(&counters[0], 1ull);
-  }
-}
-
-__global__ void k_copy_back(const long long* __restrict__ w, const long long* __restrict__ q,
-                            const double* __restrict__ pool_new, const int* __restrict__ off_new,
-                            const int* __restrict__ ext_new, double* __restrict__ pool, int* __restrict__ off,
-                            int* __restrict__ ext, long long slot, const unsigned long long* __restrict__ counters) {
-  const int j = blockIdx.x;
-  if (w[5LL * j] == q[j]) return;
-  if (counters[1] != 0) return;   // some cell failed: keep the old state everywhere
-  const int e1 = ext_new[2 * j], e2 = ext_new[2 * j + 1];
-  const double* s = pool_new + (long long)j * slot;
-  double* d = pool + (long long)j * slot;
-  for (int t = threadIdx.x; t < e1 * e2; t += blockDim.x) d[t] = s[t];
-  if (threadIdx.x == 0) {
-    off[2 * j] = off_new[2 * j];
-    off[2 * j + 1] = off_new[2 * j + 1];
-    ext[2 * j] = e1;
-    ext[2 * j + 1] = e2;
   }
 }
 
@@ -255,23 +265,20 @@ dd_status flow_init_static(dd_ctx* c) {
 
 static dd_status apply_w(dd_ctx* c, unsigned long long* d_counters, double* d_dropped) {
   const int I = c->I;
-  const int cap_side = (int)std::min<long long>(c->ccap_big + 8, 72);
-  const size_t smem = (size_t)cap_side * cap_side * 8;
+  const int cur = c->cur, spare = 1 - c->cur;
+  const size_t smem = (size_t)std::max(c->N1, c->N2) * 8;
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     DD_CUDA(cudaFuncSetAttribute(k_apply_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = smem;
   }
-  const int cur = c->cur, spare = 1 - c->cur;
+  DD_CUDA(cudaMemsetAsync(c->d_poolctr + spare, 0, 8, c->stream));
   k_apply_flow<<<I, 128, smem, c->stream>>>((const long long*)c->d_w, (const long long*)c->d_q, c->n1, c->n2,
-                                             c->d_pool[cur], c->d_off[cur], c->d_ext[cur], c->d_pool[spare],
-                                             c->d_off[spare], c->d_ext[spare], c->slot, cap_side, c->opt.trunc,
-                                             d_counters, d_dropped);
+                                             c->d_pool[cur], c->d_pos[cur], c->d_off[cur], c->d_ext[cur],
+                                             c->d_pool[spare], c->d_pos[spare], c->d_off[spare], c->d_ext[spare],
+                                             c->d_poolctr + spare, c->pool_cap, c->opt.trunc, d_counters, d_dropped);
   DD_CUDA(cudaGetLastError());
-  k_copy_back<<<I, 128, 0, c->stream>>>((const long long*)c->d_w, (const long long*)c->d_q, c->d_pool[spare],
-                                         c->d_off[spare], c->d_ext[spare], c->d_pool[cur], c->d_off[cur],
-                                         c->d_ext[cur], c->slot, d_counters);
-  DD_CUDA(cudaGetLastError());
+  c->cur = spare;   // the new state (failures are reported by counters[1])
   return DD_OK;
 }
 
@@ -310,7 +317,7 @@ dd_status flow_update_impl(dd_ctx* c, dd_flow_stats* stats) {
       return DD_ERR_NUMERIC;
     }
     if (cnt[1]) {
-      c->err = "flow apply exceeded the box capacity; state left unchanged";
+      c->err = "flow apply: pool capacity exceeded or a cell annihilated (state invalid)";
       return DD_ERR_NUMERIC;
     }
   }
@@ -363,7 +370,7 @@ dd_status flow_apply(dd_ctx* c, const int64_t* w) {
   DD_CUDA(cudaMemcpyAsync(cnt, ctr, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
   DD_CUDA(cudaStreamSynchronize(c->stream));
   if (cnt[1]) {
-    c->err = "flow apply exceeded the box capacity; state left unchanged";
+    c->err = "flow apply: pool capacity exceeded or a cell annihilated (state invalid)";
     return DD_ERR_NUMERIC;
   }
   return DD_OK;

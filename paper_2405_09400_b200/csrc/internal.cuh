@@ -49,13 +49,18 @@ struct SweepParams {
   const CompCell* __restrict__ cells;
   int ncells;
   const double* __restrict__ pool_in;
+  const long long* __restrict__ pos_in;   // [I] start of box i in pool_in
   const int* __restrict__ off_in;     // [I][2]
   const int* __restrict__ ext_in;     // [I][2]
   double* __restrict__ pool_out;
+  long long* __restrict__ pos_out;
   int* __restrict__ off_out;
   int* __restrict__ ext_out;
-  long long slot;                     // elements per basic-cell slot
-  int ccap;                           // max composite box side
+  unsigned long long* __restrict__ pool_ctr;   // bump allocator of pool_out (elements used)
+  long long pool_cap;                 // capacity of pool_out (elements)
+  int ccap;                           // composite box side of the current size class
+  unsigned char* scratch;             // global scratch of the huge class (mode 2)
+  size_t scratch_stride;              // bytes per CTA
   float* __restrict__ alpha;          // [N1*N2] base-2 local-gauge potential of this partition
   int* __restrict__ gauge;            // [ncells][2] gauge origin used for alpha
   int alpha_valid;
@@ -68,14 +73,19 @@ struct SweepParams {
   SweepTotals* __restrict__ totals;
   SweepTotals* __restrict__ cum;      // cumulative over all sweeps (not reset)
   int mode;                           // 0: one CTA per cell, defer cells with hull > ccap;
-                                      // 1: persistent CTAs over the deferred list (large ccap)
-  int* __restrict__ ovf_list;         // [ncells] deferred cells
+                                      // 1: persistent CTAs over list 1 (large ccap, shared mem),
+                                      //    defer hulls > ccap to list 2;
+                                      // 2: persistent CTAs over list 2 (global-memory scratch)
+  int* __restrict__ ovf_list;         // [ncells] list 1
   int* __restrict__ ovf_count;        // [1]
+  int* __restrict__ ovf2_list;        // [ncells] list 2
+  int* __restrict__ ovf2_count;       // [1]
   double* __restrict__ mom;           // [I][6] plan moments of the last sweep (reading R13):
                                       // M0, M1 (2), G0, G1, M2 about the cell centre, px units
 };
 
 size_t sweep_smem_bytes(int ccap, int s);
-cudaError_t launch_sweep(SweepParams p, int ccap_small, int ccap_big, cudaStream_t st);
+cudaError_t launch_sweep(SweepParams p, int ccap_small, int ccap_big, int ccap_huge, cudaStream_t st);
+size_t sweep_scratch_bytes(int ccap, int s);
 
 }  // namespace dd

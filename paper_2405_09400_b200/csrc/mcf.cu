@@ -97,15 +97,18 @@ __device__ void price_update(const McfArgs& A, cg::grid_group& grid, int par, lo
     A.dist[0][i] = A.eS[i] < 0 ? 0 : kInf;
     A.distT[0][i] = A.eT[i] < 0 ? 0 : kInf;
   }
-  if (gt == 0) { A.ctr[10] = 0; A.ctr[11] = 0; A.ctr[12] = 0; }
+  if (gt == 0) { A.ctr[10] = 0; A.ctr[11] = 0; A.ctr[12] = 0; A.ctr[13] = 0; }
   grid.sync();
   int r = 0;
   bool conv = false;
   for (; r < cap_rounds; ++r) {
+    // counters rotate over ctr[10..12] (one barrier per round, see kernel notes)
+    if (gt == 0) A.ctr[10 + (r + 1) % 3] = 0;
     const long long* dS0 = A.dist[r & 1];
     const long long* dT0 = A.distT[r & 1];
     long long* dS1 = A.dist[(r + 1) & 1];
     long long* dT1 = A.distT[(r + 1) & 1];
+    unsigned int changed = 0;
     for (long long i = gt; i < I; i += gs) {
       long long best = dS0[i];
       if (best > 0) {
@@ -136,24 +139,24 @@ __device__ void price_update(const McfArgs& A, cg::grid_group& grid, int par, lo
         }
       }
       dT1[i] = bt;
-      if (best != dS0[i] || bt != dT0[i]) atomicAdd(&A.ctr[10 + (r & 1)], 1ull);
+      if (best != dS0[i] || bt != dT0[i]) ++changed;
     }
+    changed = __reduce_add_sync(0xffffffffu, changed);
+    if ((threadIdx.x & 31) == 0 && changed) atomicAdd(&A.ctr[10 + r % 3], (unsigned long long)changed);
     grid.sync();
-    const unsigned long long ch = A.ctr[10 + (r & 1)];
-    grid.sync();
-    if (gt == 0) A.ctr[10 + ((r + 1) & 1)] = 0;
-    if (ch == 0) { conv = true; ++r; break; }
+    if (A.ctr[10 + r % 3] == 0) { conv = true; ++r; break; }
   }
+  if (gt == 0) A.ctr[13] = 0;
   grid.sync();
   if (!conv) return;
   const long long* dS = A.dist[r & 1];
   const long long* dT = A.distT[r & 1];
   for (long long i = gt; i < I; i += gs) {
-    if (dS[i] < kInf) atomicMax(&A.ctr[12], (unsigned long long)dS[i]);
-    if (dT[i] < kInf) atomicMax(&A.ctr[12], (unsigned long long)dT[i]);
+    if (dS[i] < kInf) atomicMax(&A.ctr[13], (unsigned long long)dS[i]);
+    if (dT[i] < kInf) atomicMax(&A.ctr[13], (unsigned long long)dT[i]);
   }
   grid.sync();
-  const long long Dmax = (long long)A.ctr[12];
+  const long long Dmax = (long long)A.ctr[13];
   for (long long i = gt; i < I; i += gs) {
     const long long a = dS[i] < kInf ? dS[i] : Dmax;
     const long long b = dT[i] < kInf ? dT[i] : Dmax;
@@ -202,8 +205,10 @@ __global__ void mcf_kernel(McfArgs A) {
   // ---- Bellman-Ford certificate on (I, 4-nbr arcs, C) -----------------------
   int cert = 0;
   for (int r = 0; r < A.bf_rounds; ++r) {
+    if (gt == 0) A.ctr[2 + (r + 1) % 3] = 0;
     const long long* d0 = A.dist[r & 1];
     long long* d1 = A.dist[(r + 1) & 1];
+    unsigned int changed = 0;
     for (long long j = gt; j < I; j += gs) {
       long long best = d0[j];
       for (int k = 1; k < 5; ++k) {
@@ -214,14 +219,12 @@ __global__ void mcf_kernel(McfArgs A) {
         if (cand < best) best = cand;
       }
       d1[j] = best;
-      if (best != d0[j]) atomicAdd(&A.ctr[2 + (r & 1)], 1ull);
+      if (best != d0[j]) ++changed;
     }
+    changed = __reduce_add_sync(0xffffffffu, changed);
+    if ((threadIdx.x & 31) == 0 && changed) atomicAdd(&A.ctr[2 + r % 3], (unsigned long long)changed);
     grid.sync();
-    const unsigned long long changed = A.ctr[2 + (r & 1)];
-    grid.sync();
-    if (gt == 0) A.ctr[2 + ((r + 1) & 1)] = 0;
-    grid.sync();
-    if (changed == 0) { cert = 1; break; }
+    if (A.ctr[2 + r % 3] == 0) { cert = 1; break; }
   }
   if (cert) {
     if (gt == 0) { A.info[0] = 0; A.info[1] = 1; A.info[2] = 1; A.info[3] = 0; A.info[4] = 0; }
@@ -274,7 +277,10 @@ __global__ void mcf_kernel(McfArgs A) {
       }
       const long long* pS = A.pS[par];
       const long long* pT = A.pT[par];
-      // push phase (prices frozen)
+      long long* pSn = A.pS[par ^ 1];
+      long long* pTn = A.pT[par ^ 1];
+      if (gt == 0) A.ctr[5 + (rounds + 1) % 3] = 0;   // counter of the next round
+      // phase A: push (prices frozen)
       for (long long i = gt; i < I; i += gs) {
         long long e = A.eS[i];
         if (e > 0) {
@@ -311,7 +317,9 @@ __global__ void mcf_kernel(McfArgs A) {
         }
       }
       grid.sync();
-      // merge incoming excess, count active nodes
+      // phase B: merge incoming excess, count active nodes, relabel the
+      // active nodes without admissible arcs (new prices from the frozen ones)
+      unsigned int act = 0;
       for (long long i = gt; i < I; i += gs) {
         const long long es = A.eS[i] + (long long)A.addS[i];
         const long long et = A.eT[i] + (long long)A.addT[i];
@@ -319,22 +327,9 @@ __global__ void mcf_kernel(McfArgs A) {
         A.addT[i] = 0;
         A.eS[i] = es;
         A.eT[i] = et;
-        if (es > 0) atomicAdd(&A.ctr[4 + (rounds & 1)], 1ull);
-        if (et > 0) atomicAdd(&A.ctr[4 + (rounds & 1)], 1ull);
-      }
-      grid.sync();
-      const unsigned long long active = A.ctr[4 + (rounds & 1)];
-      if (gt == 0) A.ctr[4 + ((rounds + 1) & 1)] = 0;
-      if (active == 0) {
-        grid.sync();
-        break;
-      }
-      // relabel phase: new prices from the frozen ones
-      long long* pSn = A.pS[par ^ 1];
-      long long* pTn = A.pT[par ^ 1];
-      for (long long i = gt; i < I; i += gs) {
         long long ps = pS[i];
-        if (A.eS[i] > 0) {
+        if (es > 0) {
+          ++act;
           bool adm = false;
           long long best = LLONG_MIN;
           for (int a = 0; a < 5; ++a) {
@@ -350,7 +345,8 @@ __global__ void mcf_kernel(McfArgs A) {
         }
         pSn[i] = ps;
         long long pt = pT[i];
-        if (A.eT[i] > 0) {
+        if (et > 0) {
+          ++act;
           bool adm = false;
           long long best = LLONG_MIN;
           for (int k = 0; k < 5; ++k) {
@@ -367,8 +363,11 @@ __global__ void mcf_kernel(McfArgs A) {
         }
         pTn[i] = pt;
       }
+      act = __reduce_add_sync(0xffffffffu, act);
+      if ((threadIdx.x & 31) == 0 && act) atomicAdd(&A.ctr[5 + rounds % 3], (unsigned long long)act);
       grid.sync();
       par ^= 1;
+      if (A.ctr[5 + rounds % 3] == 0) break;
     }
     if (eps == 1) break;
   }
@@ -452,11 +451,12 @@ dd_status mcf_solve_device(int n1, int n2, const int64_t* d_q, const int64_t* d_
   cudaGetDevice(&dev);
   int nsm = 0, per = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int threads = 256;
+  // one CTA per SM at most: grid barriers get cheaper with fewer CTAs
+  const int threads = 512;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mcf_kernel, threads, 0);
   if (per <= 0) { err = "mcf kernel cannot be resident"; return DD_ERR_CUDA; }
   long long want = (I + threads - 1) / threads;
-  long long blocks = (long long)nsm * per;
+  long long blocks = (long long)nsm;
   if (want < blocks) blocks = want;
   if (blocks < 1) blocks = 1;
   void* args[] = {&A};

@@ -141,7 +141,7 @@ __host__ __device__ inline SolveLayout solve_layout(int ccap, int s) {
   L.V = take(2 * NX * ccap * 4);
   L.X = take(5 * NX * NX * 4);
   L.fred = take(64 * 4);
-  L.ints = take(32 * 4);
+  L.ints = take(64 * 4);
   L.total = o;
   return L;
 }
@@ -203,7 +203,7 @@ __device__ __forceinline__ void assemble(const SweepParams& p, const CompCell& c
     const int i = cc.mem[k];
     const int e1 = ints[8 + k], e2 = ints[12 + k];
     const int d1 = ints[k] - L1, d2 = ints[4 + k] - L2;
-    const double* src = p.pool_in + (long long)i * p.slot;
+    const double* src = p.pool_in + p.pos_in[i];
     for (int t = tid; t < e1 * e2; t += T) {
       const int r = t / e2, c = t - r * e2;
       nuJ[(d1 + r) * b2 + d2 + c] += src[t];
@@ -243,10 +243,10 @@ __device__ void solve_cell(const SweepParams& p, const int J, unsigned char* sme
   const int o1 = (b1 - n1) >> 1, o2 = (b2 - n2) >> 1;
   const int G1 = L1 + o1, G2 = L2 + o2;
   if (b1 > p.ccap || b2 > p.ccap) {
-    if (p.mode == 0) {   // defer to the large size class (second launch)
-      if (tid == 0) p.ovf_list[atomicAdd(p.ovf_count, 1)] = J;
-    } else if (tid == 0) {
-      p.stats[J].overflow = 1;   // split_kernel leaves the cell unchanged
+    if (tid == 0) {
+      if (p.mode == 0) p.ovf_list[atomicAdd(p.ovf_count, 1)] = J;        // large class
+      else if (p.mode == 1) p.ovf2_list[atomicAdd(p.ovf2_count, 1)] = J;  // huge class
+      else p.stats[J].overflow = 1;   // cannot happen: the huge class covers the grid
     }
     return;
   }
@@ -579,9 +579,11 @@ __global__ void __launch_bounds__(kSweepThreads, DD_SOLVE_MINB) solve_kernel(Swe
   if (p.mode == 0) {
     if ((int)blockIdx.x < p.ncells) solve_cell<NX>(p, blockIdx.x, smem);
   } else {
-    const int n = *p.ovf_count;
+    const int n = p.mode == 1 ? *p.ovf_count : *p.ovf2_count;
+    const int* list = p.mode == 1 ? p.ovf_list : p.ovf2_list;
+    unsigned char* base = p.mode == 1 ? smem : p.scratch + (size_t)blockIdx.x * p.scratch_stride;
     for (int k = blockIdx.x; k < n; k += gridDim.x) {
-      solve_cell<NX>(p, p.ovf_list[k], smem);
+      solve_cell<NX>(p, list[k], base);
       __syncthreads();
     }
   }
@@ -657,25 +659,36 @@ __device__ void split_cell(const SweepParams& p, const int J, unsigned char* sme
   const CompCell cc = p.cells[J];
   const int nmem = cc.nmem, n1 = cc.n1, n2 = cc.n2, s = p.s;
   const float w = p.w;
-  const long long slot = p.slot;
   const int4 hull = cell_hull(p, cc, ints);
   const int L1 = hull.x, L2 = hull.y, b1 = hull.z, b2 = hull.w, BB = b1 * b2;
   const int o1 = (b1 - n1) >> 1, o2 = (b2 - n2) >> 1;
   const float fo1 = (float)o1, fo2 = (float)o2;
 
   auto copy_unchanged = [&](int reason) {
+    long long* base = (long long*)(ints + 48);
+    if (tid == 0) {
+      long long tot = 0;
+      for (int k = 0; k < nmem; ++k) tot += (long long)ints[8 + k] * ints[12 + k];
+      base[0] = (long long)atomicAdd(p.pool_ctr, (unsigned long long)tot);
+      if (base[0] + tot > p.pool_cap) { base[0] = -1; atomicAdd(&p.totals->overflow, 1ull); }
+    }
+    __syncthreads();
+    long long at = base[0];
+    if (at < 0) return;
     for (int k = 0; k < nmem; ++k) {
       const int i = cc.mem[k];
       const long long len = (long long)ints[8 + k] * ints[12 + k];
-      const double* src = p.pool_in + (long long)i * slot;
-      double* dst = p.pool_out + (long long)i * slot;
+      const double* src = p.pool_in + p.pos_in[i];
+      double* dst = p.pool_out + at;
       for (long long t = tid; t < len; t += T) dst[t] = src[t];
       if (tid == 0) {
+        p.pos_out[i] = at;
         p.off_out[2 * i] = ints[k];
         p.off_out[2 * i + 1] = ints[4 + k];
         p.ext_out[2 * i] = ints[8 + k];
         p.ext_out[2 * i + 1] = ints[12 + k];
       }
+      at += len;
     }
     if (tid == 0) {
       p.stats[J].overflow = reason;
@@ -685,8 +698,8 @@ __device__ void split_cell(const SweepParams& p, const int J, unsigned char* sme
   };
 
   if (b1 > p.ccap || b2 > p.ccap) {
-    if (p.mode == 1) copy_unchanged(1);
-    return;   // mode 0: handled by the large size class launch
+    if (p.mode == 2) copy_unchanged(1);
+    return;   // handled by the next size class
   }
   if (p.stats[J].overflow) {
     copy_unchanged(1);
@@ -936,7 +949,6 @@ __device__ void split_cell(const SweepParams& p, const int J, unsigned char* sme
     const int mn1 = ints[16 + 4 * k], mx1 = ints[16 + 4 * k + 1];
     const int mn2 = ints[16 + 4 * k + 2], mx2 = ints[16 + 4 * k + 3];
     if (mx1 < mn1 || mx2 < mn2) { ok = false; break; }   // annihilated cell
-    if ((long long)(mx1 - mn1 + 1) * (mx2 - mn2 + 1) > slot) { ok = false; break; }
   }
   if (!ok) {
     copy_unchanged(2);
@@ -957,6 +969,26 @@ __device__ void split_cell(const SweepParams& p, const int J, unsigned char* sme
       wbytes += (unsigned long long)(bx[q][1] - bx[q][0] + 1) * (bx[q][3] - bx[q][2] + 1) * 8ull;
     }
   }
+  // allocate the member boxes consecutively in the output pool
+  long long* pbase = (long long*)(ints + 48);
+  if (tid == 0) {
+    long long tot = 0;
+    for (int q = 0; q < nmem; ++q) tot += (long long)(bx[q][1] - bx[q][0] + 1) * (bx[q][3] - bx[q][2] + 1);
+    long long b0 = (long long)atomicAdd(p.pool_ctr, (unsigned long long)tot);
+    if (b0 + tot > p.pool_cap) { b0 = -1; atomicAdd(&p.totals->overflow, 1ull); }
+    pbase[0] = b0;
+  }
+  __syncthreads();
+  if (pbase[0] < 0) return;   // pool exhausted: reported as overflow (state invalid)
+  long long mbase[4];
+  {
+    long long at = pbase[0];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      mbase[q] = at;
+      if (q < nmem) at += (long long)(bx[q][1] - bx[q][0] + 1) * (bx[q][3] - bx[q][2] + 1);
+    }
+  }
   {
     const int ue2 = umx2 - umn2 + 1, un = (umx1 - umn1 + 1) * ue2;
     for (int t = tid; t < un; t += T) {
@@ -969,14 +1001,14 @@ __device__ void split_cell(const SweepParams& p, const int J, unsigned char* sme
       for (int q = 0; q < 4; ++q) {
         if (q < nmem && l1 >= bx[q][0] && l1 <= bx[q][1] && l2 >= bx[q][2] && l2 <= bx[q][3]) {
           const int e2q = bx[q][3] - bx[q][2] + 1;
-          p.pool_out[(long long)cc.mem[q] * slot + (l1 - bx[q][0]) * e2q + (l2 - bx[q][2])] =
-              v[q] >= p.tau ? v[q] : 0.0;
+          p.pool_out[mbase[q] + (l1 - bx[q][0]) * e2q + (l2 - bx[q][2])] = v[q] >= p.tau ? v[q] : 0.0;
         }
       }
     }
   }
   if (tid < nmem) {
     const int q = tid, i = cc.mem[q];
+    p.pos_out[i] = mbase[q];
     p.off_out[2 * i] = L1 + bx[q][0];
     p.off_out[2 * i + 1] = L2 + bx[q][2];
     p.ext_out[2 * i] = bx[q][1] - bx[q][0] + 1;
@@ -1015,9 +1047,11 @@ __global__ void __launch_bounds__(kSweepThreads, DD_SPLIT_MINB) split_kernel(Swe
   if (p.mode == 0) {
     if ((int)blockIdx.x < p.ncells) split_cell<NX>(p, blockIdx.x, smem);
   } else {
-    const int n = *p.ovf_count;
+    const int n = p.mode == 1 ? *p.ovf_count : *p.ovf2_count;
+    const int* list = p.mode == 1 ? p.ovf_list : p.ovf2_list;
+    unsigned char* base = p.mode == 1 ? smem : p.scratch + (size_t)blockIdx.x * p.scratch_stride;
     for (int k = blockIdx.x; k < n; k += gridDim.x) {
-      split_cell<NX>(p, p.ovf_list[k], smem);
+      split_cell<NX>(p, list[k], base);
       __syncthreads();
     }
   }
@@ -1029,7 +1063,7 @@ __global__ void __launch_bounds__(kSweepThreads, DD_SPLIT_MINB) split_kernel(Swe
 // cells; pass 1 runs persistent CTAs with shared memory for hulls <= ccap_big
 // over the queue.  No host synchronisation anywhere in the sweep.
 template <int NX>
-static cudaError_t launch_sweep_t(SweepParams p, int ccap_small, int ccap_big, cudaStream_t st) {
+static cudaError_t launch_sweep_t(SweepParams p, int ccap_small, int ccap_big, int ccap_huge, cudaStream_t st) {
   static size_t conf_solve = 0, conf_split = 0;
   const size_t s0 = solve_layout(ccap_small, p.s).total, s1 = solve_layout(ccap_big, p.s).total;
   const size_t t0 = split_layout(ccap_small, p.s).total, t1 = split_layout(ccap_big, p.s).total;
@@ -1049,37 +1083,48 @@ static cudaError_t launch_sweep_t(SweepParams p, int ccap_small, int ccap_big, c
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   e = cudaMemsetAsync(p.ovf_count, 0, sizeof(int), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(p.ovf2_count, 0, sizeof(int), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(p.pool_ctr, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
-  p.mode = 0;
-  p.ccap = ccap_small;
+  const int nhuge = (int)(p.scratch_stride ? 16 : 0);
+  // solve: small / large / huge
+  p.mode = 0; p.ccap = ccap_small;
   solve_kernel<NX><<<p.ncells, kSweepThreads, s0, st>>>(p);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  const bool big = ccap_big > ccap_small;
-  if (big) {
-    p.mode = 1;
-    p.ccap = ccap_big;
-    solve_kernel<NX><<<nsm, kSweepThreads, s1, st>>>(p);
+  p.mode = 1; p.ccap = ccap_big;
+  solve_kernel<NX><<<nsm, kSweepThreads, s1, st>>>(p);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (nhuge) {
+    p.mode = 2; p.ccap = ccap_huge;
+    solve_kernel<NX><<<nhuge, kSweepThreads, 0, st>>>(p);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  p.mode = 0;
-  p.ccap = ccap_small;
+  // split: small / large / huge
+  p.mode = 0; p.ccap = ccap_small;
   split_kernel<NX><<<p.ncells, kSweepThreads, t0, st>>>(p);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if (big) {
-    p.mode = 1;
-    p.ccap = ccap_big;
-    split_kernel<NX><<<nsm, kSweepThreads, t1, st>>>(p);
+  p.mode = 1; p.ccap = ccap_big;
+  split_kernel<NX><<<nsm, kSweepThreads, t1, st>>>(p);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (nhuge) {
+    p.mode = 2; p.ccap = ccap_huge;
+    split_kernel<NX><<<nhuge, kSweepThreads, 0, st>>>(p);
     e = cudaGetLastError();
   }
   return e;
 }
 
-cudaError_t launch_sweep(SweepParams p, int ccap_small, int ccap_big, cudaStream_t st) {
+size_t sweep_scratch_bytes(int ccap, int s) {
+  const size_t a = solve_layout(ccap, s).total, b = split_layout(ccap, s).total;
+  return (a > b ? a : b) + 256;
+}
+
+cudaError_t launch_sweep(SweepParams p, int ccap_small, int ccap_big, int ccap_huge, cudaStream_t st) {
   switch (p.s) {
-    case 1: return launch_sweep_t<2>(p, ccap_small, ccap_big, st);
-    case 2: return launch_sweep_t<4>(p, ccap_small, ccap_big, st);
-    case 4: return launch_sweep_t<8>(p, ccap_small, ccap_big, st);
-    case 8: return launch_sweep_t<16>(p, ccap_small, ccap_big, st);
+    case 1: return launch_sweep_t<2>(p, ccap_small, ccap_big, ccap_huge, st);
+    case 2: return launch_sweep_t<4>(p, ccap_small, ccap_big, ccap_huge, st);
+    case 4: return launch_sweep_t<8>(p, ccap_small, ccap_big, ccap_huge, st);
+    case 8: return launch_sweep_t<16>(p, ccap_small, ccap_big, ccap_huge, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -92,7 +92,11 @@ void solve(bool warm) {
       // push
       for (int i = 0; i < I; ++i) {
         ll e = eS[i];
-        if (e > 0) { for (int a = 0; a < 5 && e > 0; ++a) { int j = nbr(i, a); if (j < 0) continue; ll r = q[i] - w[5*i+a];
+        if (e > 0) {
+          int ord[5] = {0,1,2,3,4};
+          if (getenv("ORDER")) { ll key[5]; for (int a = 0; a < 5; ++a) { int j = nbr(i, a); key[a] = j < 0 ? LLONG_MAX : cs[5*i+a] + pS[i] - pT[j]; }
+            std::sort(ord, ord + 5, [&](int x, int y){ return key[x] < key[y]; }); }
+          for (int t = 0; t < 5 && e > 0; ++t) { int a = ord[t]; int j = nbr(i, a); if (j < 0) continue; ll r = q[i] - w[5*i+a];
           if (r <= 0) continue; if (cs[5*i+a] + pS[i] - pT[j] < 0) { ll d = std::min(e, r); w[5*i+a] += d; e -= d; addT[j] += d; } } eS[i] = e; }
         ll fe = eT[i];
         if (fe > 0) { for (int k = 0; k < 5 && fe > 0; ++k) { int a; int s = in_arc(i, k, &a); if (s < 0) continue; ll r = w[5LL*s+a];

@@ -1,0 +1,12 @@
+"""Time the GPU min-cost-flow solver on dumped flow-update instances (dev aid)."""
+import glob, os, sys, time
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np
+from paper_2405_09400_b200 import mincost_flow
+for f in sorted(glob.glob(os.path.join(ROOT, "tools", "data", "mcf_N*_c*.npz"))):
+    d = np.load(f)
+    n = int(d["n"])
+    t = time.time()
+    w, obj, st = mincost_flow(n, n, d["q"], d["C"])
+    print(os.path.basename(f), f"{time.time()-t:.3f}s", obj, st, flush=True)
