@@ -4,7 +4,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import numpy as np
 from paper_2405_09400_b200 import mincost_flow
-for f in sorted(glob.glob(os.path.join(ROOT, "tools", "data", "mcf_N*_c*.npz"))):
+for f in sorted(glob.glob(os.path.join(ROOT, "tools", "data", os.environ.get("MCF_GLOB", "mcf_N*_c*.npz")))):
     d = np.load(f)
     n = int(d["n"])
     t = time.time()
