@@ -73,6 +73,38 @@ __device__ __forceinline__ double block_sum1_d(double v, double* scratch) {
 // transpose butterfly leaves lane l with the warp total of value l (31
 // shuffles of doubles instead of 160), then the warps are summed in a fixed
 // order.  Fully unrolled so v stays in registers.  scratch >= 32 * nw.
+// Generic deterministic block sum of NV (power of two <= 32) values of type T
+// per thread: transpose butterfly inside the warp (NV - 1 + log2(32/NV)
+// shuffles), then a fixed-order sum over the warps.  out[0..NV) in shared memory.
+template <typename T, int NV>
+__device__ __forceinline__ void block_xsum(T (&v)[NV], T* scratch, T* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int idx = 0, o = 16;
+#pragma unroll
+  for (int n = NV; n > 1; n >>= 1) {
+    const int h = n >> 1;
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const T send = up ? v[i] : v[i + h];
+      const T keep = up ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+    if (up) idx += h;
+    o >>= 1;
+  }
+  T t = v[0];
+  for (int oo = o; oo > 0; oo >>= 1) t += __shfl_xor_sync(0xffffffffu, t, oo);
+  if ((lane & (32 / NV - 1)) == 0) scratch[wid * NV + idx] = t;   // one writer per output
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    T s = T(0);
+    for (int q = 0; q < nw; ++q) s += scratch[q * NV + threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+  __syncthreads();
+}
+
 template <int N>
 __device__ __forceinline__ void block_sum32_d(double (&v)[N], double* scratch, double* out) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -599,8 +631,8 @@ __global__ void __launch_bounds__(kSweepThreads, DD_SOLVE_MINB) solve_kernel(Swe
 // f (1 - theta) / M_d; see oracle/domdec.py:balance for the definition).
 // Balance coefficients live in shared memory: bc[0] = active flag,
 // bc[1 + 4k + j] = O_kj, bc[17 + 4k + j] = P_kj.
-__device__ __forceinline__ void member_values(double nuj, const float* p, int nmem, const double* bc,
-                                              double* out) {
+__device__ __forceinline__ void member_values(double nuj, const float (&p)[4], int nmem, const double* bc,
+                                              double (&out)[4]) {
   int am = 0;
 #pragma unroll
   for (int k = 1; k < 4; ++k)
@@ -753,9 +785,15 @@ __device__ void split_cell(const SweepParams& p, const int J, unsigned char* sme
   for (int k = 0; k < 4; ++k) mq[k] = cc.quad[k];
   // acc[0..3]: split masses (= moment M0); acc[4 + 5k + .]: M1a, M1b, G0, G1,
   // M2 of member k; acc[24 + pair]: overlaps sum parts_a parts_b / nu_J (R8)
-  double acc[32];
+  // masses and overlaps need fp64 per thread (balance); the plan moments are
+  // summed over only ~BB/128 entries per thread and are kept in fp32 until the
+  // (fp64) cross-thread reduction.
+  double da[16];    // per thread: masses [0..3], overlaps [4 + pair], fp64
+  float mf[32];     // per thread: plan moments [5 q + c], fp32
 #pragma unroll
-  for (int q = 0; q < 32; ++q) acc[q] = 0.0;
+  for (int q = 0; q < 16; ++q) da[q] = 0.0;
+#pragma unroll
+  for (int q = 0; q < 32; ++q) mf[q] = 0.f;
   for (int o = tid; o < BB; o += T) {
     const int l1 = o / b2, l2 = o - l1 * b2;
     const float lt = (float)l1 - fo1;
@@ -823,32 +861,36 @@ __device__ void split_cell(const SweepParams& p, const int J, unsigned char* sme
       const double invj = 1.0 / nj;
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
-        acc[a] += v[a];
+        da[a] += v[a];
 #pragma unroll
-        for (int b = a + 1; b < 4; ++b) acc[24 + pair_id(a, b)] += v[a] * v[b] * invj;
+        for (int b = a + 1; b < 4; ++b) da[4 + pair_id(a, b)] += v[a] * v[b] * invj;
       }
       // plan moments of the pre-balance marginals nu_k^pre = nu_J p_k (R13)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         if (q < nmem) {
           const int h1 = mq[q] >> 1, h2 = mq[q] & 1;
-          const double vv = nj * (double)pk[q];
-          const double y1 = (double)(L1 + l1 - cc.r0 - h1 * s) - (double)cen;
-          const double y2 = (double)(L2 + l2 - cc.c0 - h2 * s) - (double)cen;
-          acc[4 + 5 * q + 0] += vv * y1;
-          acc[4 + 5 * q + 1] += vv * y2;
-          acc[4 + 5 * q + 2] += vv * (double)Exx[q];
-          acc[4 + 5 * q + 3] += vv * (y1 * (double)Ex1[q] + y2 * (double)Ex2[q]);
-          acc[4 + 5 * q + 4] += vv * (y1 * y1 + y2 * y2);
+          const float vv = (float)nj * pk[q];
+          const float y1 = (float)(L1 + l1 - cc.r0 - h1 * s) - cen;
+          const float y2 = (float)(L2 + l2 - cc.c0 - h2 * s) - cen;
+          mf[5 * q + 0] += vv * y1;
+          mf[5 * q + 1] += vv * y2;
+          mf[5 * q + 2] += vv * Exx[q];
+          mf[5 * q + 3] += vv * (y1 * Ex1[q] + y2 * Ex2[q]);
+          mf[5 * q + 4] += vv * (y1 * y1 + y2 * y2);
         }
       }
     }
   }
   __syncthreads();
-  block_sum32_d(acc, red, red + 160);
-#pragma unroll
-  for (int q = 0; q < 32; ++q) acc[q] = red[160 + q];
-  const double massJ = acc[0] + acc[1] + acc[2] + acc[3];
+  block_xsum<double, 16>(da, red, red + 160);
+  block_xsum<float, 32>(mf, (float*)(red + 64), (float*)(red + 200));
+  // reduced values live in shared memory: masses red[160..163], overlaps
+  // red[164 + pair], plan moments (float) at red + 200
+  const double* Rm = red + 160;
+  const double* Rov = red + 164;
+  const float* Rmom = (const float*)(red + 200);
+  const double massJ = Rm[0] + Rm[1] + Rm[2] + Rm[3];
   // ---- a4: balance coefficients (reading R8), in shared memory -----------
   // Warp 0 computes them lane-parallel: lane 4 d + r -> O_dr, lane 16 + 4 k +
   // j -> P_kj (see oracle/domdec.py:balance for the definition).
@@ -860,7 +902,7 @@ __device__ void split_cell(const SweepParams& p, const int J, unsigned char* sme
     for (int q = 0; q < 4; ++q) {
       delta[q] = 0.0;
       if (q < nmem) {
-        delta[q] = acc[q] - p.m[cc.mem[q]] * massJ / muXJ;
+        delta[q] = Rm[q] - p.m[cc.mem[q]] * massJ / muXJ;
         if (delta[q] > 0) { any_d = true; Dsum += delta[q]; }
         if (delta[q] < 0) any_r = true;
       }
@@ -877,12 +919,12 @@ __device__ void split_cell(const SweepParams& p, const int J, unsigned char* sme
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           if (r < nmem && r != d && delta[r] < 0) {
-            const double T = acc[24 + (d < r ? pair_id(d, r) : pair_id(r, d))];
+            const double T = Rov[d < r ? pair_id(d, r) : pair_id(r, d)];
             if (!(T > 0.0)) zeroT = true;
             else L += delta[d] * (-delta[r]) / Dsum / T;
           }
         }
-        const double l = delta[d] / acc[d];
+        const double l = delta[d] / Rm[d];
         theta[d] = zeroT ? 0.0 : (L <= 1.0 ? 1.0 : (1.0 - l) / (L - l));
       }
     }
@@ -896,14 +938,14 @@ __device__ void split_cell(const SweepParams& p, const int J, unsigned char* sme
           if (d < nmem && r < nmem && delta[d] > 0 && delta[r] < 0) {
             const double f = delta[d] * (-delta[r]) / Dsum;
             if (tid < 16) {            // O: O_dr -= f theta / T, O_rd += f theta / T
-              const double T = acc[24 + (d < r ? pair_id(d, r) : pair_id(r, d))];
+              const double T = Rov[d < r ? pair_id(d, r) : pair_id(r, d)];
               if (theta[d] > 0.0) {
                 const double x = f * theta[d] / T;
                 if (a == d && b == r) val -= x;
                 if (a == r && b == d) val += x;
               }
             } else {                   // P: P_dd -= f (1 - theta) / M_d, P_rd += same
-              const double x = f * (1.0 - theta[d]) / acc[d];
+              const double x = f * (1.0 - theta[d]) / Rm[d];
               if (a == d && b == d) val -= x;
               if (a == r && b == d) val += x;
             }
@@ -1017,8 +1059,8 @@ __device__ void split_cell(const SweepParams& p, const int J, unsigned char* sme
   if (tid == 0) {
     for (int q = 0; q < nmem; ++q)
     {
-      p.mom[6 * cc.mem[q]] = acc[q];
-      for (int c = 0; c < 5; ++c) p.mom[6 * cc.mem[q] + 1 + c] = acc[4 + 5 * q + c];
+      p.mom[6 * cc.mem[q]] = Rm[q];
+      for (int c = 0; c < 5; ++c) p.mom[6 * cc.mem[q] + 1 + c] = (double)Rmom[5 * q + c];
     }
   }
   if (tid == 0) {
