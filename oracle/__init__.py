@@ -24,5 +24,5 @@ from .domdec import OracleState, init_state, domdec_sweep, basic_to_composite, b
 from .flow import (edge_costs, integer_instance, min_cost_flow, mcf_bruteforce,  # noqa: F401
                    apply_flow, flow_update, flow_objective)
 from .diagnostics import (marginal_errors, transport_cost, primal_score, dual_score,  # noqa: F401
-                          stitch_alpha, pd_gap, dense_state_plan)
+                          stitch_alpha, pd_gap, y_response, dense_state_plan)
 from .schedule import run  # noqa: F401

@@ -6,11 +6,8 @@ and eps = eps' h^2 (reading R2).
 """
 from __future__ import annotations
 
-from collections import deque
-
 import numpy as np
 
-from .partitions import composite_partition
 from .sinkhorn import lse, sqdist
 
 
@@ -45,9 +42,28 @@ def dense_state_plan(st):
 
 def primal_score(st, P=None):
     """E(pi) = <c, pi> + eps KL(pi | mu (x) nu) (Eq. KL
-    PAPER.md:154-167 with phi(0) = 1) of the materialised plan."""
-    if P is None:
-        P = dense_state_plan(st)
+    PAPER.md:154-167 with phi(0) = 1) of the last sweep's plan pi = sum_J
+    pi_J (needs keep_plans=True).  With P given, of that dense plan instead.
+    The X-blocks of a partition are disjoint, so the sum over cells below is
+    the same sum as over the materialised plan (checked in the pins)."""
+    if P is not None:
+        return _primal_dense(st, P)
+    nu = st.nu
+    s_pi = s_cost = s_kl = 0.0
+    for (R, C, ly, a, b, plan) in st.last["plans"].values():
+        d2 = (R[:, None] - ly[None, :, 0]) ** 2 + (C[:, None] - ly[None, :, 1]) ** 2
+        ref = st.mu[R, C][:, None] * nu[ly[:, 0], ly[:, 1]][None, :]
+        pos = plan > 0
+        if np.any(pos & (ref <= 0)):
+            return float("inf")
+        s_cost += float(np.sum(d2 * plan)) * st.h * st.h
+        s_kl += float(np.sum(plan[pos] * np.log(plan[pos] / ref[pos])))
+        s_pi += float(plan.sum())
+    kl = s_kl - s_pi + float(st.mu.sum()) * float(nu.sum())
+    return s_cost + st.eps * kl
+
+
+def _primal_dense(st, P):
     N1, N2 = st.N1, st.N2
     k = np.stack(np.meshgrid(np.arange(N1), np.arange(N2), indexing="ij"), -1).reshape(-1, 2)
     c = sqdist(k, k) * st.h * st.h
@@ -77,41 +93,36 @@ def stitch_alpha(st):
     """Global X-potential alpha† from the cell potentials of the last A and B
     sweeps, following the proof of Prop. convergence-hybrid
     as the stitching of BoSch2020 §6.3 (not reproduced in the paper,
-    PAPER.md:1413; reading R15): BFS spanning tree of the partition graph from
-    A-cell 0; across an edge (J, J') sharing basic cell i the offset changes by
-    the mu-weighted mean of (a_J' - a_J) over X_i; alpha† = a_J - s_J on
+    PAPER.md:1413; reading R15): walk a fixed spanning tree of the partition
+    graph (the "comb": A-cell (a1, a2) hangs off A-cell (a1, a2-1) through
+    B-cell (a1, a2); A-cell (a1, 0) off A-cell (a1-1, 0) through B-cell
+    (a1, 0)).  Across an edge (J, J') sharing basic cell i the offset changes
+    by the mu-weighted mean of (a_J' - a_J) over X_i; alpha† = a_J - s_J on
     A-cells.  Returns a† per pixel (nat units)."""
     n1, n2, s = st.n1, st.n2, st.s
-    A = composite_partition(n1, n2, "A")
-    B = composite_partition(n1, n2, "B")
+    na1, na2 = (n1 + 1) // 2, (n2 + 1) // 2
+    nb2 = n2 // 2 + 1
     fa, fb = st.alpha["A"], st.alpha["B"]
-    cells = {("A", k): J for k, J in enumerate(A)}
-    cells.update({("B", k): J for k, J in enumerate(B)})
-    pot = {"A": fa, "B": fb}
-    owner = {}
-    for key, J in cells.items():
-        for i in J:
-            owner.setdefault(i, []).append(key)
-    off = {("A", 0): 0.0}
-    dq = deque([("A", 0)])
-    while dq:
-        u = dq.popleft()
-        for i in cells[u]:
-            for v in owner[i]:
-                if v in off:
-                    continue
-                i1, i2 = divmod(i, n2)
-                sl = (slice(i1 * s, (i1 + 1) * s), slice(i2 * s, (i2 + 1) * s))
-                wgt = st.mu[sl]
-                diff = pot[v[0]][sl] - pot[u[0]][sl]
-                off[v] = off[u] + float(np.sum(wgt * diff) / np.sum(wgt))
-                dq.append(v)
+
+    def wmean_diff(pv, pu, i1, i2):
+        sl = (slice(i1 * s, (i1 + 1) * s), slice(i2 * s, (i2 + 1) * s))
+        wgt = st.mu[sl]
+        return float(np.sum(wgt * (pv[sl] - pu[sl])) / np.sum(wgt))
+
+    off = np.zeros((na1, na2))
+    for a1 in range(na1):
+        if a1 > 0:   # A(a1-1, 0) -> B(a1, 0) -> A(a1, 0)
+            off[a1, 0] = (off[a1 - 1, 0] + wmean_diff(fb, fa, 2 * a1 - 1, 0)
+                          + wmean_diff(fa, fb, 2 * a1, 0))
+        for a2 in range(1, na2):   # A(a1, a2-1) -> B(a1, a2) -> A(a1, a2)
+            off[a1, a2] = (off[a1, a2 - 1] + wmean_diff(fb, fa, 2 * a1, 2 * a2 - 1)
+                           + wmean_diff(fa, fb, 2 * a1, 2 * a2))
+    assert nb2 >= na2
     a = np.zeros((st.N1, st.N2))
-    for k, J in enumerate(A):
-        for i in J:
-            i1, i2 = divmod(i, n2)
-            sl = (slice(i1 * s, (i1 + 1) * s), slice(i2 * s, (i2 + 1) * s))
-            a[sl] = fa[sl] - off[("A", k)]
+    for a1 in range(na1):
+        for a2 in range(na2):
+            sl = (slice(2 * a1 * s, min(2 * a1 + 2, n1) * s), slice(2 * a2 * s, min(2 * a2 + 2, n2) * s))
+            a[sl] = fa[sl] - off[a1, a2]
     return a
 
 
@@ -120,7 +131,9 @@ def y_response(st, a: np.ndarray):
     N1, N2 = st.N1, st.N2
     k = np.stack(np.meshgrid(np.arange(N1), np.arange(N2), indexing="ij"), -1).reshape(-1, 2)
     Ce = sqdist(k, k) / st.eps_p
-    return (-lse(a.ravel()[:, None] + np.log(st.mu.ravel())[:, None] - Ce, axis=0)).reshape(N1, N2)
+    with np.errstate(divide="ignore"):
+        logmu = np.log(st.mu.ravel())
+    return (-lse(a.ravel()[:, None] + logmu[:, None] - Ce, axis=0)).reshape(N1, N2)
 
 
 def pd_gap(st, P=None):
