@@ -36,7 +36,7 @@ class _Problem(C.Structure):
 class _Options(C.Structure):
     _fields_ = [("err", C.c_double), ("max_iter", C.c_int32), ("fixed_iter", C.c_int32),
                 ("trunc", C.c_double), ("slot_cap", C.c_int32), ("comp_cap", C.c_int32),
-                ("device", C.c_int32), ("stream", C.c_void_p)]
+                ("device", C.c_int32), ("stream", C.c_void_p), ("track_primal", C.c_int32)]
 
 
 class SweepStats(C.Structure):
@@ -130,7 +130,7 @@ class DomDec:
 
     def __init__(self, mu, nu, cell_size, eps, h, init_off, init_ext, init_pos, init_data, mass_exponent,
                  err=1e-4, max_iter=2000, fixed_iter=0, trunc=1e-15, slot_cap=0, comp_cap=0, device=0,
-                 stream=None):
+                 stream=None, track_primal=False):
         self._keep = [np.ascontiguousarray(mu, np.float64), np.ascontiguousarray(nu, np.float64),
                       np.ascontiguousarray(init_off, np.int32), np.ascontiguousarray(init_ext, np.int32),
                       np.ascontiguousarray(init_pos, np.int64), np.ascontiguousarray(init_data, np.float64)]
@@ -143,7 +143,7 @@ class DomDec:
                      _ptr(off_, C.c_int32), _ptr(ext_, C.c_int32), _ptr(pos_, C.c_int64), _ptr(data_, C.c_double),
                      int(mass_exponent))
         O = _Options(float(err), int(max_iter), int(fixed_iter), float(trunc), int(slot_cap), int(comp_cap),
-                     int(device), C.c_void_p(stream) if stream else None)
+                     int(device), C.c_void_p(stream) if stream else None, int(bool(track_primal)))
         ctx = C.c_void_p()
         _check(lib().domdec_init(C.byref(P), C.byref(O), C.byref(ctx)), None)
         self._ctx = ctx

@@ -147,7 +147,7 @@ void free_ctx(dd_ctx* c) {
                   c->d_off[1], c->d_ext[0], c->d_ext[1], c->d_cells[0], c->d_cells[1], c->d_alpha[0],
                   c->d_alpha[1], c->d_gauge[0], c->d_gauge[1], c->d_stats[0], c->d_stats[1], c->d_totals[0],
                   c->d_totals[1], c->d_mom, c->d_xbar, c->d_var, c->d_cbar, c->d_C, c->d_w, c->d_mcf,
-                  c->d_flow_info, c->d_scratch, c->d_red, c->d_ovf, c->d_cum};
+                  c->d_flow_info, c->d_scratch, c->d_red, c->d_ovf, c->d_cum, c->d_ecell, c->d_pd};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -318,6 +318,7 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c) 
     TRY(dalloc(c, &c->d_gauge[b], (size_t)c->ncells[b] * 2));
     TRY(dalloc(c, &c->d_stats[b], c->ncells[b]));
     if (b == 1) TRY(dalloc(c, &c->d_ovf, 2 * (size_t)std::max(c->ncells[0], c->ncells[1]) + 8));
+    if (b == 1) TRY(dalloc(c, &c->d_ecell, (size_t)std::max(c->ncells[0], c->ncells[1])));
     TRY(dalloc(c, &c->d_totals[b], 1));
     DD_CUDA(cudaMemcpyAsync(c->d_cells[b], c->h_cells[b].data(), sizeof(CompCell) * c->ncells[b],
                             cudaMemcpyHostToDevice, st));
@@ -421,6 +422,9 @@ dd_status domdec_sweep(dd_ctx* c, dd_partition part, dd_sweep_stats* stats) {
   p.totals = c->d_totals[b];
   p.cum = c->d_cum;
   p.mom = c->d_mom;
+  p.nu = c->d_nu;
+  p.ecell = c->opt.track_primal ? c->d_ecell : nullptr;
+  p.eps_p = c->eps_p;
   DD_CUDA(cudaMemsetAsync(c->d_totals[b], 0, sizeof(SweepTotals), c->stream));
   const int mc = std::max(c->ncells[0], c->ncells[1]);
   p.ovf_count = c->d_ovf;
@@ -433,6 +437,7 @@ dd_status domdec_sweep(dd_ctx* c, dd_partition part, dd_sweep_stats* stats) {
   c->alpha_valid[b] = 1;
   c->last_part = b;
   c->swept |= (1 << b);
+  c->primal_valid = c->opt.track_primal != 0;
   if (stats) {
     SweepTotals t{};
     DD_CUDA(cudaMemcpyAsync(&t, c->d_totals[b], sizeof(t), cudaMemcpyDeviceToHost, c->stream));
@@ -582,6 +587,10 @@ dd_status primal_dual_gap(dd_ctx* c, double* primal, double* dual, double* rel_g
   if (!c) return DD_ERR_ARG;
   if (c->swept != 3) {
     c->err = "primal_dual_gap needs at least one A and one B sweep";
+    return DD_ERR_PRECOND;
+  }
+  if (!c->primal_valid) {
+    c->err = "primal_dual_gap needs the last sweep run with options.track_primal = 1";
     return DD_ERR_PRECOND;
   }
   DD_CUDA(cudaSetDevice(c->device));

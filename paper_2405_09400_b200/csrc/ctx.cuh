@@ -47,7 +47,10 @@ struct dd_ctx {
   long long n_sweeps = 0, n_flows = 0;
   int last_part = -1;
   int swept = 0;
+  bool primal_valid = false;   // the last sweep recorded d_ecell
   double* d_mom = nullptr;   // [I][6] plan moments of the last sweep (R13)
+  double* d_ecell = nullptr; // [max ncells] primal score per composite cell of the last sweep / h^2
+  double* d_pd = nullptr;    // [4 N1 N2 + ...] primal-dual gap scratch (allocated on first use)
   // flow update
   double* d_xbar = nullptr;   // [I][2] mu-mean of X_i (pixel units)
   double* d_var = nullptr;    // [I] trace of the covariance of mu_i / m_i

@@ -324,11 +324,6 @@ dd_status flow_update_impl(dd_ctx* c, dd_flow_stats* stats) {
   return DD_OK;
 }
 
-dd_status pd_gap_impl(dd_ctx* c, double*, double*, double*, double*) {
-  c->err = "primal_dual_gap: not implemented in this build";
-  return DD_ERR_ARG;
-}
-
 }  // namespace dd
 
 using namespace dd;

@@ -82,6 +82,9 @@ struct SweepParams {
   int* __restrict__ ovf2_count;       // [1]
   double* __restrict__ mom;           // [I][6] plan moments of the last sweep (reading R13):
                                       // M0, M1 (2), G0, G1, M2 about the cell centre, px units
+  const double* __restrict__ nu;      // [N1*N2] global nu (primal score only)
+  double* __restrict__ ecell;         // [ncells] primal score of each returned plan / h^2
+  double eps_p;                       // eps' = eps / h^2
 };
 
 size_t sweep_smem_bytes(int ccap, int s);

@@ -159,7 +159,7 @@ __device__ __forceinline__ float block_sum_f(float v, float* scratch, int parity
 // ---------------------------------------------------------------------------
 // Shared-memory layouts.  BB = ccap^2 box entries, NX = 2 s.
 struct SolveLayout {
-  size_t B, LN, BK, U, V, X, fred, ints, total;   // X: A2, A2n, LM, MU, AL
+  size_t B, LN, BK, U, V, X, fred, ints, dred, total;   // X: A2, A2n, LM, MU, AL
 };
 __host__ __device__ inline SolveLayout solve_layout(int ccap, int s) {
   SolveLayout L;
@@ -174,6 +174,9 @@ __host__ __device__ inline SolveLayout solve_layout(int ccap, int s) {
   L.X = take(5 * NX * NX * 4);
   L.fred = take(64 * 4);
   L.ints = take(64 * 4);
+  // fp64 reduction scratch of the primal epilogue: the U/V stage buffers are
+  // free after the Sinkhorn loop; a separate slot only if they are too small
+  L.dred = (4 * NX * ccap * 4 >= 80 * 8) ? L.U : take(80 * 8);
   L.total = o;
   return L;
 }
@@ -244,9 +247,60 @@ __device__ __forceinline__ void assemble(const SweepParams& p, const CompCell& c
   }
 }
 
+// Primal score of the plan a solve returns (diagnostic):
+// pi(k, l) = 2^(A(k) + B(l) - w |kappa - lt|^2) mu(k) nu_J(l) in the local
+// gauge, k = K + kappa, l = G + lt, D = K - G.  Its Y-marginal is nu_J, its
+// X-marginal PX = mu 2^(A - A').  With c = h^2 |k - l|^2 and eps = eps' h^2,
+//   (<c, pi> + eps KL(pi | mu (x) nu) + eps sum pi) / h^2
+//     = |D|^2 S0 + 2 D.(S_kappa - S_lt) + eps' (ln2 (S_A + S_B + S_L) - S0),
+// S0 = sum nu_J, S_kappa = sum kappa PX, S_lt = sum lt nu_J, S_A = sum A PX,
+// S_B = sum B nu_J, S_L = sum nu_J log2(nu_J / nu).
+// nu_J is re-assembled in fp64 (the BK region is free after the loop).
+template <int NX>
+__device__ __forceinline__ void primal_terms(const SweepParams& p, const CompCell& cc, const int J, const int* ints,
+                                          const int L1, const int L2, const int b1, const int b2, const int o1,
+                                          const int o2, const int G1, const int G2, const float* A2,
+                                          const float* A2n, const float* MU, const float* Bp, double* nuJ,
+                                          double* red) {
+  const int tid = threadIdx.x, T = blockDim.x;
+  __syncthreads();
+  assemble(p, cc, ints, L1, L2, b2, b1 * b2, nuJ);
+  double v[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  constexpr int NXX = NX * NX;
+  for (int t = tid; t < NXX; t += T) {
+    const int k1 = t / NX, k2 = t % NX;
+    if (k1 < cc.n1 && k2 < cc.n2) {
+      const double a = (double)A2[t];
+      const double px = (double)MU[t] * exp2(a - (double)A2n[t]);
+      v[0] += a * px;
+      v[1] += (double)k1 * px;
+      v[2] += (double)k2 * px;
+    }
+  }
+  for (int t = tid; t < b1 * b2; t += T) {
+    const double nj = nuJ[t];
+    if (nj > 0.0) {
+      const int l1 = t / b2, l2 = t - l1 * b2;
+      const double ng = p.nu[(long long)(L1 + l1) * p.N2 + L2 + l2];
+      v[3] += nj;
+      v[4] += (double)Bp[t] * nj;
+      v[5] += ng > 0.0 ? nj * log2(nj / ng) : (double)INFINITY;   // pi not << mu (x) nu
+      v[6] += (double)(l1 - o1) * nj;
+      v[7] += (double)(l2 - o2) * nj;
+    }
+  }
+  block_xsum<double, 8>(v, red, red + 64);
+  if (tid == 0) {
+    const double* S = red + 64;
+    const double D1 = (double)(cc.r0 - G1), D2 = (double)(cc.c0 - G2);
+    p.ecell[J] = (D1 * D1 + D2 * D2) * S[3] + 2.0 * (D1 * (S[1] - S[6]) + D2 * (S[2] - S[7])) +
+                 p.eps_p * (0.69314718055994531 * (S[0] + S[4] + S[5]) - S[3]);
+  }
+}
+
 // ===========================================================================
 // solve_kernel: a1 (log2 nu_J) + a2 (Sinkhorn), one CTA per composite cell.
-template <int NX>
+template <int NX, bool PR>
 __device__ void solve_cell(const SweepParams& p, const int J, unsigned char* smem) {
   const int tid = threadIdx.x, T = blockDim.x;
   const SolveLayout Ls = solve_layout(p.ccap, p.s);
@@ -573,6 +627,9 @@ __device__ void solve_cell(const SweepParams& p, const int J, unsigned char* sme
     float* tmp = A2; A2 = A2n; A2n = tmp;   // A <- A'
     first = false;
   }
+  if (PR)
+    primal_terms<NX>(p, cc, J, ints, L1, L2, b1, b2, o1, o2, G1, G2, A2, A2n, MU, P0, nuJ,
+                     (double*)(smem + Ls.dred));
   // ---- outputs: the plan's potential (next warm start, R7) and stats -----
   for (int t = tid; t < NN; t += T) {
     const int k1 = t / n2, k2 = t - k1 * n2;
@@ -605,17 +662,17 @@ __device__ void solve_cell(const SweepParams& p, const int J, unsigned char* sme
   }
 }
 
-template <int NX>
+template <int NX, bool PR>
 __global__ void __launch_bounds__(kSweepThreads, DD_SOLVE_MINB) solve_kernel(SweepParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   if (p.mode == 0) {
-    if ((int)blockIdx.x < p.ncells) solve_cell<NX>(p, blockIdx.x, smem);
+    if ((int)blockIdx.x < p.ncells) solve_cell<NX, PR>(p, blockIdx.x, smem);
   } else {
     const int n = p.mode == 1 ? *p.ovf_count : *p.ovf2_count;
     const int* list = p.mode == 1 ? p.ovf_list : p.ovf2_list;
     unsigned char* base = p.mode == 1 ? smem : p.scratch + (size_t)blockIdx.x * p.scratch_stride;
     for (int k = blockIdx.x; k < n; k += gridDim.x) {
-      solve_cell<NX>(p, list[k], base);
+      solve_cell<NX, PR>(p, list[k], base);
       __syncthreads();
     }
   }
@@ -1106,15 +1163,19 @@ __global__ void __launch_bounds__(kSweepThreads, DD_SPLIT_MINB) split_kernel(Swe
 // over the queue.  No host synchronisation anywhere in the sweep.
 template <int NX>
 static cudaError_t launch_sweep_t(SweepParams p, int ccap_small, int ccap_big, int ccap_huge, cudaStream_t st) {
-  static size_t conf_solve = 0, conf_split = 0;
+  static size_t conf_solve[2] = {0, 0}, conf_split = 0;
+  // the primal-score epilogue is a separate instantiation so the timed
+  // variant carries none of its code (options.track_primal)
+  void (*solve)(SweepParams) = p.ecell ? solve_kernel<NX, true> : solve_kernel<NX, false>;
+  const int pr = p.ecell ? 1 : 0;
   const size_t s0 = solve_layout(ccap_small, p.s).total, s1 = solve_layout(ccap_big, p.s).total;
   const size_t t0 = split_layout(ccap_small, p.s).total, t1 = split_layout(ccap_big, p.s).total;
   const size_t ns = s0 > s1 ? s0 : s1, nt = t0 > t1 ? t0 : t1;
   cudaError_t e;
-  if (ns > 48 * 1024 && ns > conf_solve) {
-    e = cudaFuncSetAttribute(solve_kernel<NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ns);
+  if (ns > 48 * 1024 && ns > conf_solve[pr]) {
+    e = cudaFuncSetAttribute(solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ns);
     if (e != cudaSuccess) return e;
-    conf_solve = ns;
+    conf_solve[pr] = ns;
   }
   if (nt > 48 * 1024 && nt > conf_split) {
     e = cudaFuncSetAttribute(split_kernel<NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nt);
@@ -1131,14 +1192,14 @@ static cudaError_t launch_sweep_t(SweepParams p, int ccap_small, int ccap_big, i
   const int nhuge = (int)(p.scratch_stride ? 16 : 0);
   // solve: small / large / huge
   p.mode = 0; p.ccap = ccap_small;
-  solve_kernel<NX><<<p.ncells, kSweepThreads, s0, st>>>(p);
+  solve<<<p.ncells, kSweepThreads, s0, st>>>(p);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   p.mode = 1; p.ccap = ccap_big;
-  solve_kernel<NX><<<nsm, kSweepThreads, s1, st>>>(p);
+  solve<<<nsm, kSweepThreads, s1, st>>>(p);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (nhuge) {
     p.mode = 2; p.ccap = ccap_huge;
-    solve_kernel<NX><<<nhuge, kSweepThreads, 0, st>>>(p);
+    solve<<<nhuge, kSweepThreads, 0, st>>>(p);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   // split: small / large / huge

@@ -229,3 +229,46 @@ def test_full_size_sampled_first_sweep(part):
             c = compare_cell(gb[i], ob)
             assert c["box_equal"] or c["guard_ok"], (k, i, c)
             assert c["rel_bulk"] < 5e-3, (k, i, c)
+
+
+@gpu
+@pytest.mark.parametrize("cfg", ["cfg1_gm", "cfg1_bumps_small_eps", "cfg2_gm"])
+def test_primal_dual_gap_parity(cfg):
+    """primal_dual_gap (App. A.2.2; stitching reading R15)
+    against the oracle's pd_gap on the same parity-mode trajectory.  The fp32
+    potentials carry ~1e-6 (log2 units) absolute error, so E and D each carry
+    ~eps * 1e-6 absolute, and both are sums of terms of size ~E: tolerance
+    1e-6 (|E| + eps) on E, D and the transport cost, times max(1, 4/eps') as
+    for every parity tolerance (the exponents scale like 1/eps'), propagated
+    to the gap."""
+    p = CONFIGS[cfg]()
+    K = 20
+    st = oracle_state(p)
+    dd = gpu_ctx(p, fixed_iter=K, track_primal=True)
+    for k in range(8):
+        part = "AB"[k % 2]
+        O.domdec_sweep(st, part, fixed_iter=K, keep_plans=True)
+        dd.sweep(part)
+        if k in (1, 4, 7):
+            E, D, gap = O.pd_gap(st)
+            oc = O.transport_cost(st)
+            gE, gD, ggap, gc = dd.primal_dual_gap()
+            print(cfg, k, (E, gE), (D, gD), (gap, ggap), (oc, gc))
+            tol = 1e-6 * max(1.0, 4.0 / p.eps_prime) * (abs(E) + p.eps)   # rel_tols scaling
+            assert abs(gE - E) <= tol, (gE, E)
+            assert abs(gD - D) <= tol, (gD, D)
+            assert abs(gc - oc) <= tol, (gc, oc)
+            assert abs(ggap - gap) <= 2 * tol * (1 + abs(gap)) / abs(D), (ggap, gap)
+
+
+@gpu
+def test_primal_dual_gap_requires_tracking():
+    """Without options.track_primal the last sweep has no primal score:
+    DD_ERR_PRECOND, not a silent value."""
+    from paper_2405_09400_b200 import DomDecError
+    p = CONFIGS["cfg1_gm"]()
+    dd = gpu_ctx(p)
+    dd.sweep("A")
+    dd.sweep("B")
+    with pytest.raises(DomDecError):
+        dd.primal_dual_gap()
