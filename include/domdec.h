@@ -116,6 +116,9 @@ typedef struct {
   int32_t certificate;    /* 1: stationarity proven by the negative-cycle test */
   int32_t refines;        /* cost-scaling refine phases run by the solver      */
   int32_t rounds;         /* push/relabel rounds run by the solver             */
+  int32_t label_rounds;   /* Bellman-Ford rounds (certificate, global price    */
+                          /* updates, price refinement); each is one grid-wide */
+                          /* barrier like a push/relabel round                 */
   int64_t objective;      /* optimal sum_ij w_ij C_ij (integer costs, R11)     */
   int64_t changed_cells;  /* basic cells whose marginal was rewritten          */
 } dd_flow_stats;

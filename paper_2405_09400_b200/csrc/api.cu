@@ -10,6 +10,9 @@
 using namespace dd;
 
 static std::string g_last_error;   // errors with no ctx (init / standalone solver)
+namespace dd {
+void set_global_error(const std::string& m) { g_last_error = m; }
+}  // namespace dd
 
 namespace {
 

@@ -311,6 +311,7 @@ dd_status flow_update_impl(dd_ctx* c, dd_flow_stats* stats) {
     stats->certificate = (int32_t)info[2];
     stats->refines = (int32_t)info[3];
     stats->rounds = (int32_t)info[4];
+    stats->label_rounds = (int32_t)info[5];
     stats->changed_cells = (int64_t)cnt[0];
     if (info[6]) {
       c->err = "min-cost flow did not converge (round cap)";
@@ -407,6 +408,7 @@ dd_status dd_mincost_flow(int32_t n1, int32_t n2, const int64_t* q, const int64_
           stats->certificate = (int32_t)info[2];
           stats->refines = (int32_t)info[3];
           stats->rounds = (int32_t)info[4];
+          stats->label_rounds = (int32_t)info[5];
           stats->changed_cells = 0;
         }
         if (info[6]) s = DD_ERR_NUMERIC;
@@ -417,6 +419,11 @@ dd_status dd_mincost_flow(int32_t n1, int32_t n2, const int64_t* q, const int64_
   if (dC) cudaFree(dC);
   if (dw) cudaFree(dw);
   if (ws) cudaFree(ws);
+  if (s != DD_OK) {
+    if (err.empty()) err = s == DD_ERR_NUMERIC ? "min-cost flow did not finish within the round cap"
+                                                : std::string("CUDA: ") + cudaGetErrorString(cudaGetLastError());
+    set_global_error(err);
+  }
   return s;
 }
 

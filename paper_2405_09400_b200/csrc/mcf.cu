@@ -23,6 +23,7 @@
 // atomics commute, so the result is deterministic.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
 #include <string>
 
 #include "../../include/domdec.h"
@@ -50,6 +51,7 @@ struct McfArgs {
   long long* info;        // [16] results: 0 objective, 1 stationary, 2 certificate, 3 refines, 4 rounds, 6 error
   int bf_rounds;
   int max_rounds;
+  int gu_every;           // push/relabel rounds between global price updates
 };
 
 __device__ __forceinline__ int nbr(int i, int a, int n1, int n2) {
@@ -83,74 +85,168 @@ __device__ __forceinline__ long long floor_div(long long a, long long b) {   // 
   return q;
 }
 
-// Global price update (Goldberg's set-relabel, parallel Bellman-Ford): d(v) =
-// length of the shortest residual path from v to a deficit node with arc
-// lengths l(v,u) = floor(c_p(v,u)/eps) + 1; then p(v) -= eps * d(v).  Keeps
+// ---------------------------------------------------------------------------
+// Tiled Bellman-Ford.  All label computations of the solver (certificate,
+// global price update, price refinement) are shortest-path fixpoints, which
+// are unique whatever the relaxation order, so they run as chaotic
+// relaxation: each CTA owns a TH x TW tile of cells (both nodes S_i and T_i of
+// a cell), keeps the tile's labels plus a one-cell halo in shared memory,
+// precomputes its arc lengths in registers and relaxes in place for up to
+// kSweeps local sweeps (block barriers only) before one grid-wide barrier.
+// Labels only decrease and are always lengths of real paths, so the result
+// equals synchronous Bellman-Ford; a grid round in which no tile changed a
+// label proves the fixpoint.  Paths cross a tile in one grid round instead of
+// one hop per round.
+//   mode 0 (price update): d(v) = distance from v to a deficit node along
+//     residual arcs v -> u with l = max(0, floor(c_p/eps) + 1);
+//   mode 1 (price refinement): d(u) = distance from a virtual source (0 at
+//     every node) along residual arcs v -> u with l = c_p + epsT;
+//   mode 2 (certificate): one node per cell, d(j) over the 4-neighbour arcs
+//     i -> j with the integer costs C (no negative cycle <=> converges).
+constexpr int TH = 16, TW = 32, TP = TW + 2, kSweeps = 32;
+
+__device__ bool tiled_bf(const McfArgs& A, cg::grid_group& grid, const int mode, const int par, const long long eps,
+                         const int cap, long long gt, long long gs, int* rounds_used) {
+  const int n1 = A.n1, n2 = A.n2, I = A.I;
+  const long long* pS = A.pS[par];
+  const long long* pT = A.pT[par];
+  long long* dS = A.dist[0];
+  long long* dT = A.distT[0];
+  __shared__ long long sS[(TH + 2) * TP], sT[(TH + 2) * TP];
+  const int nt2 = (n2 + TW - 1) / TW, ntiles = ((n1 + TH - 1) / TH) * nt2;
+  const int ty = threadIdx.x / TW, tx = threadIdx.x % TW;
+  const int offs[5] = {0, -TP, TP, -1, 1};   // self, up, down, left, right (arc order of nbr / in_arc)
+  for (long long i = gt; i < I; i += gs) {
+    if (mode == 0) {
+      dS[i] = A.eS[i] < 0 ? 0 : kInf;
+      dT[i] = A.eT[i] < 0 ? 0 : kInf;
+    } else {
+      dS[i] = 0;
+      dT[i] = mode == 1 ? 0 : kInf;
+    }
+  }
+  if (gt == 0) { A.ctr[10] = 0; A.ctr[11] = 0; A.ctr[12] = 0; }
+  grid.sync();
+  // One tile per CTA (the usual case): arc lengths stay in registers and the
+  // tile interior stays in shared memory across grid rounds (only this CTA
+  // writes it); only the halo is re-read.  Otherwise CTAs loop over tiles and
+  // reload everything per tile.
+  const bool single = ntiles <= (int)gridDim.x;
+  long long LS[5], LT[5];
+  bool conv = false;
+  int r = 0;
+  for (; r < cap; ++r) {
+    if (gt == 0) A.ctr[10 + (r + 1) % 3] = 0;
+    bool changed_any = false;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int r0 = (tile / nt2) * TH, c0 = (tile % nt2) * TW;
+      const bool full = !single || r == 0;
+      for (int e = threadIdx.x; e < (TH + 2) * TP; e += blockDim.x) {
+        const int ey = e / TP, ex = e % TP;
+        if (!full && ey > 0 && ey < TH + 1 && ex > 0 && ex < TP - 1) continue;   // interior kept
+        const int y = ey - 1 + r0, x = ex - 1 + c0;
+        long long vs = kInf, vt = kInf;
+        if (y >= 0 && y < n1 && x >= 0 && x < n2) {
+          const long long g = (long long)y * n2 + x;
+          vs = __ldcg(dS + g);
+          vt = __ldcg(dT + g);
+        }
+        sS[e] = vs;
+        sT[e] = vt;
+      }
+      const int y = r0 + ty, x = c0 + tx;
+      const bool mine = y < n1 && x < n2;
+      const long long i = (long long)y * n2 + x;
+      if (full) {
+#pragma unroll
+        for (int a = 0; a < 5; ++a) { LS[a] = kInf; LT[a] = kInf; }
+        if (mine) {
+#pragma unroll
+          for (int a = 0; a < 5; ++a) {
+            const int j = nbr((int)i, a, n1, n2);
+            if (j >= 0) {
+              if (mode == 0) {
+                if (A.q[i] - A.w[5 * i + a] > 0) {
+                  long long l = floor_div(A.cs[5 * i + a] + pS[i] - pT[j], eps) + 1;
+                  LS[a] = l < 0 ? 0 : (l > (1LL << 40) ? (1LL << 40) : l);
+                }
+              } else if (mode == 1) {
+                if (A.w[5 * i + a] > 0) LS[a] = -(A.cs[5 * i + a] + pS[i] - pT[j]) + eps;
+              }
+            }
+            int b;
+            const int src = in_arc((int)i, a, n1, n2, &b);
+            if (src >= 0) {
+              if (mode == 0) {
+                if (A.w[5LL * src + b] > 0) {
+                  long long l = floor_div(-(A.cs[5LL * src + b] + pS[src] - pT[i]), eps) + 1;
+                  LT[a] = l < 0 ? 0 : (l > (1LL << 40) ? (1LL << 40) : l);
+                }
+              } else if (mode == 1) {
+                if (A.q[src] - A.w[5LL * src + b] > 0) LT[a] = A.cs[5LL * src + b] + pS[src] - pT[i] + eps;
+              } else if (a > 0) {
+                LS[a] = A.C[5LL * src + b];   // certificate: arc src -> i, label of S only
+              }
+            }
+          }
+        }
+      }
+      __syncthreads();
+      const int c = (ty + 1) * TP + tx + 1;
+      bool ch_tile = false;
+      for (int sw = 0; sw < kSweeps; ++sw) {
+        bool ch = false;
+        if (mine) {
+          long long bs = sS[c], bt = sT[c];
+#pragma unroll
+          for (int a = 0; a < 5; ++a) {
+            if (LS[a] < kInf) {
+              const long long u = mode == 2 ? sS[c + offs[a]] : sT[c + offs[a]];
+              if (u < kInf && u + LS[a] < bs) bs = u + LS[a];
+            }
+            if (LT[a] < kInf) {
+              const long long u = sS[c + offs[a]];
+              if (u < kInf && u + LT[a] < bt) bt = u + LT[a];
+            }
+          }
+          if (bs < sS[c]) { sS[c] = bs; ch = true; }
+          if (bt < sT[c]) { sT[c] = bt; ch = true; }
+        }
+        if (!__syncthreads_or(ch)) break;
+        ch_tile = true;
+      }
+      if (mine && ch_tile) {
+        dS[i] = sS[c];
+        dT[i] = sT[c];
+      }
+      changed_any |= ch_tile;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0 && changed_any) atomicAdd(&A.ctr[10 + r % 3], 1ull);
+    grid.sync();
+    if (A.ctr[10 + r % 3] == 0) { conv = true; ++r; break; }
+  }
+  *rounds_used = r;
+  if (gt == 0) A.ctr[14] += r;
+  return conv;
+}
+
+// Global price update (Goldberg's set-relabel): d(v) = length of the
+// shortest residual path from v to a deficit node with arc lengths
+// l(v,u) = floor(c_p(v,u)/eps) + 1; then p(v) -= eps * d(v).  Keeps
 // eps-optimality and makes every shortest path admissible.  Applied only if
 // the labels converged within the round cap.  Uniform control flow.
 __device__ void price_update(const McfArgs& A, cg::grid_group& grid, int par, long long eps, long long gt,
                              long long gs, int cap_rounds) {
-  const int n1 = A.n1, n2 = A.n2, I = A.I;
+  const int I = A.I;
+  int r = 0;
+  if (gt == 0) A.ctr[13] = 0;
+  const bool conv = tiled_bf(A, grid, 0, par, eps, cap_rounds, gt, gs, &r);
+  if (!conv) return;
   long long* pS = A.pS[par];
   long long* pT = A.pT[par];
-  for (long long i = gt; i < I; i += gs) {
-    A.dist[0][i] = A.eS[i] < 0 ? 0 : kInf;
-    A.distT[0][i] = A.eT[i] < 0 ? 0 : kInf;
-  }
-  if (gt == 0) { A.ctr[10] = 0; A.ctr[11] = 0; A.ctr[12] = 0; A.ctr[13] = 0; }
-  grid.sync();
-  int r = 0;
-  bool conv = false;
-  for (; r < cap_rounds; ++r) {
-    // counters rotate over ctr[10..12] (one barrier per round, see kernel notes)
-    if (gt == 0) A.ctr[10 + (r + 1) % 3] = 0;
-    const long long* dS0 = A.dist[r & 1];
-    const long long* dT0 = A.distT[r & 1];
-    long long* dS1 = A.dist[(r + 1) & 1];
-    long long* dT1 = A.distT[(r + 1) & 1];
-    unsigned int changed = 0;
-    for (long long i = gt; i < I; i += gs) {
-      long long best = dS0[i];
-      if (best > 0) {
-        for (int a = 0; a < 5; ++a) {
-          const int j = nbr((int)i, a, n1, n2);
-          if (j < 0 || A.q[i] - A.w[5 * i + a] <= 0) continue;
-          const long long du = dT0[j];
-          if (du >= kInf) continue;
-          long long l = floor_div(A.cs[5 * i + a] + pS[i] - pT[j], eps) + 1;
-          if (l < 0) l = 0;
-          if (l > (1LL << 40)) l = (1LL << 40);
-          if (du + l < best) best = du + l;
-        }
-      }
-      dS1[i] = best;
-      long long bt = dT0[i];
-      if (bt > 0) {
-        for (int k = 0; k < 5; ++k) {
-          int a;
-          const int src = in_arc((int)i, k, n1, n2, &a);
-          if (src < 0 || A.w[5LL * src + a] <= 0) continue;
-          const long long du = dS0[src];
-          if (du >= kInf) continue;
-          long long l = floor_div(-(A.cs[5LL * src + a] + pS[src] - pT[i]), eps) + 1;
-          if (l < 0) l = 0;
-          if (l > (1LL << 40)) l = (1LL << 40);
-          if (du + l < bt) bt = du + l;
-        }
-      }
-      dT1[i] = bt;
-      if (best != dS0[i] || bt != dT0[i]) ++changed;
-    }
-    changed = __reduce_add_sync(0xffffffffu, changed);
-    if ((threadIdx.x & 31) == 0 && changed) atomicAdd(&A.ctr[10 + r % 3], (unsigned long long)changed);
-    grid.sync();
-    if (A.ctr[10 + r % 3] == 0) { conv = true; ++r; break; }
-  }
-  if (gt == 0) A.ctr[13] = 0;
-  grid.sync();
-  if (!conv) return;
-  const long long* dS = A.dist[r & 1];
-  const long long* dT = A.distT[r & 1];
+  const long long* dS = A.dist[0];
+  const long long* dT = A.distT[0];
   for (long long i = gt; i < I; i += gs) {
     if (dS[i] < kInf) atomicMax(&A.ctr[13], (unsigned long long)dS[i]);
     if (dT[i] < kInf) atomicMax(&A.ctr[13], (unsigned long long)dT[i]);
@@ -166,7 +262,29 @@ __device__ void price_update(const McfArgs& A, cg::grid_group& grid, int par, lo
   grid.sync();
 }
 
-__global__ void mcf_kernel(McfArgs A) {
+// Price refinement (Goldberg's CS2 heuristic): if the current flow admits
+// prices that make it epsT-optimal (no residual cycle of mean reduced cost
+// < -epsT), Bellman-Ford from a virtual source (d = 0 at every node) with
+// arc lengths c_p(v,u) + epsT converges and p += d achieves it; otherwise the
+// labels keep decreasing and the cap stops the attempt with the prices
+// unchanged.  With epsT = 1 on costs scaled by SC = 2I + 1 a success proves
+// the current flow optimal.  Uniform control flow.
+__device__ bool price_refine(const McfArgs& A, cg::grid_group& grid, int par, long long epsT, long long gt,
+                             long long gs, int cap_rounds) {
+  const int I = A.I;
+  int r = 0;
+  if (!tiled_bf(A, grid, 1, par, epsT, cap_rounds, gt, gs, &r)) return false;
+  long long* pS = A.pS[par];
+  long long* pT = A.pT[par];
+  for (long long i = gt; i < I; i += gs) {
+    pS[i] += A.dist[0][i];
+    pT[i] += A.distT[0][i];
+  }
+  grid.sync();
+  return true;
+}
+
+__global__ void __launch_bounds__(512, 1) mcf_kernel(McfArgs A) {
   cg::grid_group grid = cg::this_grid();
   const int n1 = A.n1, n2 = A.n2, I = A.I;
   const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -203,41 +321,31 @@ __global__ void mcf_kernel(McfArgs A) {
     return;
   }
   // ---- Bellman-Ford certificate on (I, 4-nbr arcs, C) -----------------------
-  int cert = 0;
-  for (int r = 0; r < A.bf_rounds; ++r) {
-    if (gt == 0) A.ctr[2 + (r + 1) % 3] = 0;
-    const long long* d0 = A.dist[r & 1];
-    long long* d1 = A.dist[(r + 1) & 1];
-    unsigned int changed = 0;
-    for (long long j = gt; j < I; j += gs) {
-      long long best = d0[j];
-      for (int k = 1; k < 5; ++k) {
-        int a;
-        const int i = in_arc((int)j, k, n1, n2, &a);
-        if (i < 0) continue;
-        const long long cand = d0[i] + A.C[5LL * i + a];
-        if (cand < best) best = cand;
-      }
-      d1[j] = best;
-      if (best != d0[j]) ++changed;
-    }
-    changed = __reduce_add_sync(0xffffffffu, changed);
-    if ((threadIdx.x & 31) == 0 && changed) atomicAdd(&A.ctr[2 + r % 3], (unsigned long long)changed);
-    grid.sync();
-    if (A.ctr[2 + r % 3] == 0) { cert = 1; break; }
-  }
+  int rb = 0;
+  const int cert = tiled_bf(A, grid, 2, 0, 0, A.bf_rounds, gt, gs, &rb) ? 1 : 0;
   if (cert) {
-    if (gt == 0) { A.info[0] = 0; A.info[1] = 1; A.info[2] = 1; A.info[3] = 0; A.info[4] = 0; }
+    if (gt == 0) { A.info[0] = 0; A.info[1] = 1; A.info[2] = 1; A.info[3] = 0; A.info[4] = 0; A.info[5] = rb; }
     return;
   }
   // ---- cost scaling -----------------------------------------------------------
   long long eps = (long long)A.ctr[0] * SC;
   int refines = 0, rounds = 0, par = 0;
+  const int pr_cap = 4 * (n1 + n2) + 128;
   bool failed = false;
   while (eps >= 1 && !failed) {
     eps = (eps + 15) / 16;   // alpha = 16
     if (eps < 1) eps = 1;
     ++refines;
+    // price refinement: after the first phase the flow is often already
+    // optimal (degenerate instances) or eps-optimal for the next eps; then
+    // the phase is skipped instead of rebuilt from saturated arcs
+    if (refines > 1) {
+      if (price_refine(A, grid, par, 1, gt, gs, pr_cap)) break;
+      if (price_refine(A, grid, par, eps, gt, gs, pr_cap)) {
+        if (eps == 1) break;
+        continue;
+      }
+    }
     const long long* pSo = A.pS[par];
     const long long* pTo = A.pT[par];
     // saturate arcs with negative reduced cost (both directions)
@@ -264,7 +372,7 @@ __global__ void mcf_kernel(McfArgs A) {
       A.eT[i] = in - A.q[i];
     }
     grid.sync();
-    const int gu_every = 2 * (n1 + n2) + 32;
+    const int gu_every = A.gu_every;
     const int gu_cap = 8 * (n1 + n2) + 256;
     price_update(A, grid, par, eps, gt, gs, gu_cap);
     int since_gu = 0;
@@ -392,6 +500,7 @@ __global__ void mcf_kernel(McfArgs A) {
     A.info[2] = 0;
     A.info[3] = refines;
     A.info[4] = rounds;
+    A.info[5] = (long long)A.ctr[14];
     A.info[6] = failed ? 1 : 0;
   }
   if (failed) {
@@ -445,6 +554,10 @@ dd_status mcf_solve_device(int n1, int n2, const int64_t* d_q, const int64_t* d_
   A.info = p;
   A.bf_rounds = 2 * (n1 + n2) + 8;
   A.max_rounds = 2000000;
+  // rounds between global price updates: tuned on dumped flow-update
+  // instances (tools/mcf_time.py); DD_MCF_GU overrides (development knob)
+  A.gu_every = 50;
+  if (const char* env = getenv("DD_MCF_GU")) A.gu_every = atoi(env) > 0 ? atoi(env) : A.gu_every;
   cudaError_t e = cudaMemsetAsync(A.ctr, 0, 32 * sizeof(long long), st);
   if (e != cudaSuccess) { err = cudaGetErrorString(e); return DD_ERR_CUDA; }
   int dev = 0;

@@ -139,7 +139,7 @@ int main(int argc, char** argv) {
     ll SC = 2LL * I + 1;
     srand(1);
     for (int i = 0; i < I; ++i) { pS[i] += (ll)(noise * SC * ((rand() / (double)RAND_MAX) - 0.5)); pT[i] += (ll)(noise * SC * ((rand() / (double)RAND_MAX) - 0.5)); }
-    for (int i = 0; i < I; ++i) for (int a = 0; a < 5; ++a) w[5*i+a] = a == 0 ? q[i] : 0;
+    if (!getenv("KEEPW")) for (int i = 0; i < I; ++i) for (int a = 0; a < 5; ++a) w[5*i+a] = a == 0 ? q[i] : 0;
     solve(true);
   } else if (argc > 2 && argv[2][0] != '-') { load(argv[2]); solve(true); }
 }
