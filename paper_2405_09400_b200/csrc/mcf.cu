@@ -52,6 +52,9 @@ struct McfArgs {
   int bf_rounds;
   int max_rounds;
   int gu_every;           // push/relabel rounds between global price updates
+  int tiled;              // 1: checkerboard tile phases instead of grid-wide rounds
+  int tile_rounds;        // local rounds per tile phase
+  int gu_tiled;           // tile phases between global price updates
 };
 
 __device__ __forceinline__ int nbr(int i, int a, int n1, int n2) {
@@ -227,6 +230,9 @@ __device__ bool tiled_bf(const McfArgs& A, cg::grid_group& grid, const int mode,
     if (A.ctr[10 + r % 3] == 0) { conv = true; ++r; break; }
   }
   *rounds_used = r;
+  // every CTA must have read the last round's counter before anyone reuses
+  // ctr[10..12] (a following call resets them)
+  grid.sync();
   if (gt == 0) A.ctr[14] += r;
   return conv;
 }
@@ -284,7 +290,203 @@ __device__ bool price_refine(const McfArgs& A, cg::grid_group& grid, int par, lo
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// Checkerboard tile discharge.  The cell grid is cut into TH x TW tiles
+// coloured like a checkerboard; edge-adjacent tiles have different colours
+// and every arc joins edge-adjacent (or equal) cells, so while the tiles of
+// one colour work, the nodes, prices and incident arcs they touch are touched
+// by no other working tile.  A working tile runs up to R synchronous
+// push / merge+relabel rounds (the same rounds as the grid-wide loop) on its
+// own nodes with block barriers only; neighbours outside the tile are frozen:
+// their prices are read once, pushes into them go to their global excess
+// (atomics), and the arcs between a working and a frozen tile are written by
+// the working side only.  Every operation is therefore a valid push or
+// relabel of the generic algorithm and eps-optimality is kept exactly as in
+// the grid-wide rounds; one grid barrier per colour phase instead of two per
+// round.
+struct TileSmem {
+  long long *pSa, *pTa, *pSb, *pTb;   // prices with halo, two buffers [(TH + 2) * TP]
+  long long *w;                       // [TH * TW][5] out-arc flows of the tile's sources
+  long long *eS, *eT, *addS, *addT;   // [TH * TW]
+};
+
+__device__ __forceinline__ TileSmem tile_smem(unsigned char* base) {
+  TileSmem t;
+  long long* p = (long long*)base;
+  const int H = (TH + 2) * TP, C = TH * TW;
+  t.pSa = p; p += H;
+  t.pTa = p; p += H;
+  t.pSb = p; p += H;
+  t.pTb = p; p += H;
+  t.w = p; p += 5 * C;
+  t.eS = p; p += C;
+  t.eT = p; p += C;
+  t.addS = p; p += C;
+  t.addT = p; p += C;
+  return t;
+}
+constexpr size_t kTileSmemBytes = sizeof(long long) * (4 * (TH + 2) * TP + 9 * TH * TW);
+
+// returns the number of local rounds run (block-uniform)
+__device__ int tile_discharge(const McfArgs& A, const int tile, const int par, const long long eps, const int R,
+                              unsigned char* smem_raw) {
+  const int n1 = A.n1, n2 = A.n2;
+  TileSmem S = tile_smem(smem_raw);
+  const int nt2 = (n2 + TW - 1) / TW;
+  const int r0 = (tile / nt2) * TH, c0 = (tile % nt2) * TW;
+  const int t = threadIdx.x, ty = t / TW, tx = t % TW;
+  const long long* gpS = A.pS[par];
+  const long long* gpT = A.pT[par];
+  for (int e = t; e < (TH + 2) * TP; e += blockDim.x) {
+    const int y = e / TP - 1 + r0, x = e % TP - 1 + c0;
+    long long vs = 0, vt = 0;
+    if (y >= 0 && y < n1 && x >= 0 && x < n2) {
+      const long long g = (long long)y * n2 + x;
+      vs = __ldcg(gpS + g);
+      vt = __ldcg(gpT + g);
+    }
+    S.pSa[e] = vs; S.pTa[e] = vt; S.pSb[e] = vs; S.pTb[e] = vt;
+  }
+  const int y = r0 + ty, x = c0 + tx;
+  const bool mine = y < n1 && x < n2;
+  const long long i = (long long)y * n2 + x;
+  const int c = (ty + 1) * TP + tx + 1;
+  const int offs[5] = {0, -TP, TP, -1, 1};
+  const int toff[5] = {0, -TW, TW, -1, 1};
+  long long qi = 0, csr[5];
+  bool inS[5];   // neighbour cell of arc a lies inside the tile
+#pragma unroll
+  for (int a = 0; a < 5; ++a) {
+    csr[a] = 0;
+    const int yy = ty + (a == 1 ? -1 : a == 2 ? 1 : 0), xx = tx + (a == 3 ? -1 : a == 4 ? 1 : 0);
+    inS[a] = yy >= 0 && yy < TH && xx >= 0 && xx < TW && r0 + yy < n1 && c0 + xx < n2;
+  }
+  if (mine) {
+    qi = A.q[i];
+#pragma unroll
+    for (int a = 0; a < 5; ++a) {
+      csr[a] = A.cs[5 * i + a];
+      S.w[5 * t + a] = __ldcg(A.w + 5 * i + a);
+    }
+    S.eS[t] = __ldcg(A.eS + i);
+    S.eT[t] = __ldcg(A.eT + i);
+  } else {
+    S.eS[t] = 0;
+    S.eT[t] = 0;
+  }
+  S.addS[t] = 0;
+  S.addT[t] = 0;
+  __syncthreads();
+  long long *pS = S.pSa, *pT = S.pTa, *pSn = S.pSb, *pTn = S.pTb;
+  int rr = 0;
+  for (; rr < R; ++rr) {
+    // phase A: push (prices frozen)
+    if (mine) {
+      long long e = S.eS[t];
+      if (e > 0) {
+        for (int a = 0; a < 5 && e > 0; ++a) {
+          const int j = nbr((int)i, a, n1, n2);
+          if (j < 0) continue;
+          const long long r = qi - S.w[5 * t + a];
+          if (r <= 0) continue;
+          if (csr[a] + pS[c] - pT[c + offs[a]] < 0) {
+            const long long d = e < r ? e : r;
+            S.w[5 * t + a] += d;
+            e -= d;
+            if (inS[a]) atomicAdd((unsigned long long*)&S.addT[t + toff[a]], (unsigned long long)d);
+            else atomicAdd((unsigned long long*)&A.eT[j], (unsigned long long)d);
+          }
+        }
+        S.eS[t] = e;
+      }
+      long long f = S.eT[t];
+      if (f > 0) {
+        for (int k = 0; k < 5 && f > 0; ++k) {
+          int b;
+          const int src = in_arc((int)i, k, n1, n2, &b);
+          if (src < 0) continue;
+          long long* wp = inS[k] ? &S.w[5 * (t + toff[k]) + b] : &A.w[5LL * src + b];
+          const long long r = *wp;
+          if (r <= 0) continue;
+          if (A.cs[5LL * src + b] + pS[c + offs[k]] - pT[c] > 0) {   // reverse arc admissible
+            const long long d = f < r ? f : r;
+            *wp = r - d;
+            f -= d;
+            if (inS[k]) atomicAdd((unsigned long long*)&S.addS[t + toff[k]], (unsigned long long)d);
+            else atomicAdd((unsigned long long*)&A.eS[src], (unsigned long long)d);
+          }
+        }
+        S.eT[t] = f;
+      }
+    }
+    __syncthreads();
+    // phase B: merge, relabel active nodes without admissible arcs (from the
+    // frozen prices of this round), count
+    bool act = false;
+    long long ps = pS[c], pt = pT[c];
+    if (mine) {
+      const long long es = S.eS[t] + S.addS[t];
+      const long long et = S.eT[t] + S.addT[t];
+      S.addS[t] = 0;
+      S.addT[t] = 0;
+      S.eS[t] = es;
+      S.eT[t] = et;
+      if (es > 0) {
+        act = true;
+        bool adm = false;
+        long long best = LLONG_MIN;
+        for (int a = 0; a < 5; ++a) {
+          if (nbr((int)i, a, n1, n2) < 0) continue;
+          if (qi - S.w[5 * t + a] <= 0) continue;
+          const long long cp = csr[a] + pS[c] - pT[c + offs[a]];
+          if (cp < 0) { adm = true; break; }
+          const long long cand = pT[c + offs[a]] - csr[a];
+          if (cand > best) best = cand;
+        }
+        if (!adm && best != LLONG_MIN) ps = best - eps;
+      }
+      if (et > 0) {
+        act = true;
+        bool adm = false;
+        long long best = LLONG_MIN;
+        for (int k = 0; k < 5; ++k) {
+          int b;
+          const int src = in_arc((int)i, k, n1, n2, &b);
+          if (src < 0) continue;
+          const long long wv = inS[k] ? S.w[5 * (t + toff[k]) + b] : A.w[5LL * src + b];
+          if (wv <= 0) continue;
+          const long long cs = A.cs[5LL * src + b];
+          const long long cp = cs + pS[c + offs[k]] - pT[c];
+          if (cp > 0) { adm = true; break; }
+          const long long cand = pS[c + offs[k]] + cs;
+          if (cand > best) best = cand;
+        }
+        if (!adm && best != LLONG_MIN) pt = best - eps;
+      }
+    }
+    pSn[c] = ps;
+    pTn[c] = pt;
+    const int nact = __syncthreads_count(act);
+    long long* tmp = pS; pS = pSn; pSn = tmp;
+    tmp = pT; pT = pTn; pTn = tmp;
+    if (nact == 0) { ++rr; break; }
+  }
+  // write back (no other working tile touches these nodes or arcs)
+  if (mine) {
+    A.pS[par][i] = pS[c];
+    A.pT[par][i] = pT[c];
+    A.eS[i] = S.eS[t];
+    A.eT[i] = S.eT[t];
+#pragma unroll
+    for (int a = 0; a < 5; ++a) A.w[5 * i + a] = S.w[5 * t + a];
+  }
+  __syncthreads();
+  return rr;
+}
+
 __global__ void __launch_bounds__(512, 1) mcf_kernel(McfArgs A) {
+  extern __shared__ __align__(16) unsigned char dsmem[];
+  long long local_rounds = 0;
   cg::grid_group grid = cg::this_grid();
   const int n1 = A.n1, n2 = A.n2, I = A.I;
   const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -376,6 +578,37 @@ __global__ void __launch_bounds__(512, 1) mcf_kernel(McfArgs A) {
     const int gu_cap = 8 * (n1 + n2) + 256;
     price_update(A, grid, par, eps, gt, gs, gu_cap);
     int since_gu = 0;
+    if (A.tiled) {
+      // checkerboard tile phases (see tile_discharge); one grid barrier per
+      // phase.  The active-node count taken at the start of phase g is read
+      // at the start of phase g + 1: zero means phase g had nothing to do.
+      const int nt2 = (n2 + TW - 1) / TW, ntiles = ((n1 + TH - 1) / TH) * nt2;
+      for (int g = 0;; ++g) {
+        if (g > 0 && A.ctr[5 + (g - 1) % 3] == 0) break;
+        if (rounds >= A.max_rounds) { failed = true; break; }
+        ++rounds;
+        if (++since_gu >= A.gu_tiled) {
+          since_gu = 0;
+          price_update(A, grid, par, eps, gt, gs, gu_cap);
+        }
+        if (gt == 0) A.ctr[5 + (g + 1) % 3] = 0;
+        unsigned int act = 0;
+        for (long long i = gt; i < I; i += gs) act += (A.eS[i] > 0) + (A.eT[i] > 0);
+        act = __reduce_add_sync(0xffffffffu, act);
+        if ((threadIdx.x & 31) == 0 && act) atomicAdd(&A.ctr[5 + g % 3], (unsigned long long)act);
+        grid.sync();   // counts complete, and no tile starts before every count has read the state
+        if (A.ctr[5 + g % 3] != 0) {
+          const int color = g & 1;
+          for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            if ((((tile / nt2) + (tile % nt2)) & 1) != color) continue;
+            local_rounds += tile_discharge(A, tile, par, eps, A.tile_rounds, dsmem);
+          }
+        }
+        grid.sync();
+      }
+      if (eps == 1) break;
+      continue;
+    }
     for (;;) {
       if (rounds >= A.max_rounds) { failed = true; break; }
       ++rounds;
@@ -501,6 +734,7 @@ __global__ void __launch_bounds__(512, 1) mcf_kernel(McfArgs A) {
     A.info[3] = refines;
     A.info[4] = rounds;
     A.info[5] = (long long)A.ctr[14];
+    A.info[7] = local_rounds;   // thread 0's CTA only (diagnostic)
     A.info[6] = failed ? 1 : 0;
   }
   if (failed) {
@@ -557,7 +791,14 @@ dd_status mcf_solve_device(int n1, int n2, const int64_t* d_q, const int64_t* d_
   // rounds between global price updates: tuned on dumped flow-update
   // instances (tools/mcf_time.py); DD_MCF_GU overrides (development knob)
   A.gu_every = 50;
+  A.tiled = 1;
+  A.tile_rounds = 16;
+  A.gu_tiled = 8;
   if (const char* env = getenv("DD_MCF_GU")) A.gu_every = atoi(env) > 0 ? atoi(env) : A.gu_every;
+  if (const char* env = getenv("DD_MCF_TILED")) A.tiled = atoi(env);
+  if (const char* env = getenv("DD_MCF_MAXR")) A.max_rounds = atoi(env) > 0 ? atoi(env) : A.max_rounds;
+  if (const char* env = getenv("DD_MCF_R")) A.tile_rounds = atoi(env) > 0 ? atoi(env) : A.tile_rounds;
+  if (const char* env = getenv("DD_MCF_GUT")) A.gu_tiled = atoi(env) > 0 ? atoi(env) : A.gu_tiled;
   cudaError_t e = cudaMemsetAsync(A.ctr, 0, 32 * sizeof(long long), st);
   if (e != cudaSuccess) { err = cudaGetErrorString(e); return DD_ERR_CUDA; }
   int dev = 0;
@@ -566,14 +807,20 @@ dd_status mcf_solve_device(int n1, int n2, const int64_t* d_q, const int64_t* d_
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   // one CTA per SM at most: grid barriers get cheaper with fewer CTAs
   const int threads = 512;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mcf_kernel, threads, 0);
+  static bool smem_set = false;
+  if (!smem_set) {
+    e = cudaFuncSetAttribute(mcf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmemBytes);
+    if (e != cudaSuccess) { err = std::string("mcf smem: ") + cudaGetErrorString(e); return DD_ERR_CUDA; }
+    smem_set = true;
+  }
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mcf_kernel, threads, kTileSmemBytes);
   if (per <= 0) { err = "mcf kernel cannot be resident"; return DD_ERR_CUDA; }
   long long want = (I + threads - 1) / threads;
   long long blocks = (long long)nsm;
   if (want < blocks) blocks = want;
   if (blocks < 1) blocks = 1;
   void* args[] = {&A};
-  e = cudaLaunchCooperativeKernel((void*)mcf_kernel, dim3((unsigned)blocks), dim3(threads), args, 0, st);
+  e = cudaLaunchCooperativeKernel((void*)mcf_kernel, dim3((unsigned)blocks), dim3(threads), args, kTileSmemBytes, st);
   if (e != cudaSuccess) { err = std::string("mcf launch: ") + cudaGetErrorString(e); return DD_ERR_CUDA; }
   return DD_OK;
 }
