@@ -1,3 +1,5 @@
+#include <cstdio>
+#include <cstdlib>
 // flow.cu — flow update steps 1 and 3 (§5.1) and the
 // flow-related C-ABI entry points.
 //
@@ -412,6 +414,9 @@ dd_status dd_mincost_flow(int32_t n1, int32_t n2, const int64_t* q, const int64_
           stats->changed_cells = 0;
         }
         if (info[6]) s = DD_ERR_NUMERIC;
+        if (getenv("DD_MCF_TIMERS"))
+          fprintf(stderr, "mcf timers (ms): refine %.1f update %.1f phase %.1f wait %.1f total %.1f local_rounds %lld\n",
+                  info[8] * 1e-6, info[9] * 1e-6, info[10] * 1e-6, info[11] * 1e-6, info[12] * 1e-6, info[7]);
       }
     }
   }

@@ -82,6 +82,12 @@ __device__ __forceinline__ int in_arc(int j, int k, int n1, int n2, int* a_out) 
 
 constexpr long long kInf = (1LL << 60);
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ long long floor_div(long long a, long long b) {   // b > 0
   long long q = a / b;
   if ((a % b != 0) && (a < 0)) --q;
@@ -108,7 +114,7 @@ __device__ __forceinline__ long long floor_div(long long a, long long b) {   // 
 //     i -> j with the integer costs C (no negative cycle <=> converges).
 constexpr int TH = 16, TW = 32, TP = TW + 2, kSweeps = 32;
 
-__device__ bool tiled_bf(const McfArgs& A, cg::grid_group& grid, const int mode, const int par, const long long eps,
+__device__ __noinline__ bool tiled_bf(const McfArgs& A, cg::grid_group& grid, const int mode, const int par, const long long eps,
                          const int cap, long long gt, long long gs, int* rounds_used) {
   const int n1 = A.n1, n2 = A.n2, I = A.I;
   const long long* pS = A.pS[par];
@@ -307,6 +313,8 @@ __device__ bool price_refine(const McfArgs& A, cg::grid_group& grid, int par, lo
 struct TileSmem {
   long long *pSa, *pTa, *pSb, *pTb;   // prices with halo, two buffers [(TH + 2) * TP]
   long long *w;                       // [TH * TW][5] out-arc flows of the tile's sources
+  long long *cin;                     // [TH * TW][5] scaled costs of the sinks' in-arcs
+  long long *win;                     // [TH * TW][5] flows of in-arcs from sources outside the tile
   long long *eS, *eT, *addS, *addT;   // [TH * TW]
 };
 
@@ -319,16 +327,18 @@ __device__ __forceinline__ TileSmem tile_smem(unsigned char* base) {
   t.pSb = p; p += H;
   t.pTb = p; p += H;
   t.w = p; p += 5 * C;
+  t.cin = p; p += 5 * C;
+  t.win = p; p += 5 * C;
   t.eS = p; p += C;
   t.eT = p; p += C;
   t.addS = p; p += C;
   t.addT = p; p += C;
   return t;
 }
-constexpr size_t kTileSmemBytes = sizeof(long long) * (4 * (TH + 2) * TP + 9 * TH * TW);
+constexpr size_t kTileSmemBytes = sizeof(long long) * (4 * (TH + 2) * TP + 19 * TH * TW);
 
 // returns the number of local rounds run (block-uniform)
-__device__ int tile_discharge(const McfArgs& A, const int tile, const int par, const long long eps, const int R,
+__device__ __noinline__ int tile_discharge(const McfArgs& A, const int tile, const int par, const long long eps, const int R,
                               unsigned char* smem_raw) {
   const int n1 = A.n1, n2 = A.n2;
   TileSmem S = tile_smem(smem_raw);
@@ -370,6 +380,13 @@ __device__ int tile_discharge(const McfArgs& A, const int tile, const int par, c
     }
     S.eS[t] = __ldcg(A.eS + i);
     S.eT[t] = __ldcg(A.eT + i);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      int b;
+      const int src = in_arc((int)i, k, n1, n2, &b);
+      S.cin[5 * t + k] = src >= 0 ? A.cs[5LL * src + b] : 0;
+      S.win[5 * t + k] = (src >= 0 && !inS[k]) ? __ldcg(A.w + 5LL * src + b) : 0;
+    }
   } else {
     S.eS[t] = 0;
     S.eT[t] = 0;
@@ -405,10 +422,10 @@ __device__ int tile_discharge(const McfArgs& A, const int tile, const int par, c
           int b;
           const int src = in_arc((int)i, k, n1, n2, &b);
           if (src < 0) continue;
-          long long* wp = inS[k] ? &S.w[5 * (t + toff[k]) + b] : &A.w[5LL * src + b];
+          long long* wp = inS[k] ? &S.w[5 * (t + toff[k]) + b] : &S.win[5 * t + k];
           const long long r = *wp;
           if (r <= 0) continue;
-          if (A.cs[5LL * src + b] + pS[c + offs[k]] - pT[c] > 0) {   // reverse arc admissible
+          if (S.cin[5 * t + k] + pS[c + offs[k]] - pT[c] > 0) {   // reverse arc admissible
             const long long d = f < r ? f : r;
             *wp = r - d;
             f -= d;
@@ -453,9 +470,9 @@ __device__ int tile_discharge(const McfArgs& A, const int tile, const int par, c
           int b;
           const int src = in_arc((int)i, k, n1, n2, &b);
           if (src < 0) continue;
-          const long long wv = inS[k] ? S.w[5 * (t + toff[k]) + b] : A.w[5LL * src + b];
+          const long long wv = inS[k] ? S.w[5 * (t + toff[k]) + b] : S.win[5 * t + k];
           if (wv <= 0) continue;
-          const long long cs = A.cs[5LL * src + b];
+          const long long cs = S.cin[5 * t + k];
           const long long cp = cs + pS[c + offs[k]] - pT[c];
           if (cp > 0) { adm = true; break; }
           const long long cand = pS[c + offs[k]] + cs;
@@ -479,6 +496,13 @@ __device__ int tile_discharge(const McfArgs& A, const int tile, const int par, c
     A.eT[i] = S.eT[t];
 #pragma unroll
     for (int a = 0; a < 5; ++a) A.w[5 * i + a] = S.w[5 * t + a];
+#pragma unroll
+    for (int k = 1; k < 5; ++k) {
+      if (inS[k]) continue;
+      int b;
+      const int src = in_arc((int)i, k, n1, n2, &b);
+      if (src >= 0) A.w[5LL * src + b] = S.win[5 * t + k];
+    }
   }
   __syncthreads();
   return rr;
@@ -487,6 +511,8 @@ __device__ int tile_discharge(const McfArgs& A, const int tile, const int par, c
 __global__ void __launch_bounds__(512, 1) mcf_kernel(McfArgs A) {
   extern __shared__ __align__(16) unsigned char dsmem[];
   long long local_rounds = 0;
+  unsigned long long tm_refine = 0, tm_update = 0, tm_phase = 0, tm_wait = 0;
+  const unsigned long long tm_start = gtimer();
   cg::grid_group grid = cg::this_grid();
   const int n1 = A.n1, n2 = A.n2, I = A.I;
   const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -542,8 +568,14 @@ __global__ void __launch_bounds__(512, 1) mcf_kernel(McfArgs A) {
     // optimal (degenerate instances) or eps-optimal for the next eps; then
     // the phase is skipped instead of rebuilt from saturated arcs
     if (refines > 1) {
-      if (price_refine(A, grid, par, 1, gt, gs, pr_cap)) break;
-      if (price_refine(A, grid, par, eps, gt, gs, pr_cap)) {
+      const unsigned long long t0 = gtimer();
+      const bool opt = price_refine(A, grid, par, 1, gt, gs, pr_cap);
+      tm_refine += gtimer() - t0;
+      if (opt) break;
+      const unsigned long long t1 = gtimer();
+      const bool ok = price_refine(A, grid, par, eps, gt, gs, pr_cap);
+      tm_refine += gtimer() - t1;
+      if (ok) {
         if (eps == 1) break;
         continue;
       }
@@ -589,8 +621,11 @@ __global__ void __launch_bounds__(512, 1) mcf_kernel(McfArgs A) {
         ++rounds;
         if (++since_gu >= A.gu_tiled) {
           since_gu = 0;
+          const unsigned long long t0 = gtimer();
           price_update(A, grid, par, eps, gt, gs, gu_cap);
+          tm_update += gtimer() - t0;
         }
+        const unsigned long long t2 = gtimer();
         if (gt == 0) A.ctr[5 + (g + 1) % 3] = 0;
         unsigned int act = 0;
         for (long long i = gt; i < I; i += gs) act += (A.eS[i] > 0) + (A.eT[i] > 0);
@@ -604,7 +639,10 @@ __global__ void __launch_bounds__(512, 1) mcf_kernel(McfArgs A) {
             local_rounds += tile_discharge(A, tile, par, eps, A.tile_rounds, dsmem);
           }
         }
+        const unsigned long long t3 = gtimer();
         grid.sync();
+        tm_phase += t3 - t2;
+        tm_wait += gtimer() - t3;
       }
       if (eps == 1) break;
       continue;
@@ -735,6 +773,11 @@ __global__ void __launch_bounds__(512, 1) mcf_kernel(McfArgs A) {
     A.info[4] = rounds;
     A.info[5] = (long long)A.ctr[14];
     A.info[7] = local_rounds;   // thread 0's CTA only (diagnostic)
+    A.info[8] = (long long)tm_refine;   // ns, thread 0 (diagnostic timers)
+    A.info[9] = (long long)tm_update;
+    A.info[10] = (long long)tm_phase;
+    A.info[11] = (long long)tm_wait;
+    A.info[12] = (long long)(gtimer() - tm_start);
     A.info[6] = failed ? 1 : 0;
   }
   if (failed) {
@@ -793,7 +836,7 @@ dd_status mcf_solve_device(int n1, int n2, const int64_t* d_q, const int64_t* d_
   A.gu_every = 50;
   A.tiled = 1;
   A.tile_rounds = 16;
-  A.gu_tiled = 8;
+  A.gu_tiled = 16;
   if (const char* env = getenv("DD_MCF_GU")) A.gu_every = atoi(env) > 0 ? atoi(env) : A.gu_every;
   if (const char* env = getenv("DD_MCF_TILED")) A.tiled = atoi(env);
   if (const char* env = getenv("DD_MCF_MAXR")) A.max_rounds = atoi(env) > 0 ? atoi(env) : A.max_rounds;
