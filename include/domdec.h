@@ -94,6 +94,14 @@ typedef struct {
                        /* default stream)                                       */
   int32_t track_primal; /* 1: every sweep also records the primal score of its */
                        /* plans (needed by primal_dual_gap; ~5% sweep time)    */
+  int32_t row_begin;   /* stripe mode: this context owns basic-  */
+  int32_t row_end;     /* cell rows [row_begin, row_end) (even, or row_end =   */
+                       /* n1) and solves only the A-cells of those rows and the */
+                       /* B-cells with 2 b1 in [row_begin, row_end) (+ the last */
+                       /* B row when row_end = n1).  0, 0 = the whole grid.     */
+                       /* The caller exchanges halo rows (domdec_halo_pack /    */
+                       /* _unpack) and runs the flow update through the hooks  */
+                       /* (flow_edge_costs, dd_mincost_flow, flow_apply).       */
 } dd_options;
 
 /* Filled by domdec_sweep when a non-NULL pointer is passed (synchronises). */
@@ -212,6 +220,20 @@ dd_status domdec_reset_counters(dd_ctx *ctx);
  * kernel of independent MUFU chains — the denominator of the sweep roofline
  * (DESIGN.md "Roofline"). */
 dd_status dd_mufu_peak(int32_t device, double *ops_per_s);
+
+/* Stripe halo exchange: serialise the basic-cell marginals of
+ * basic-cell row `row` (n2 cells) into the DEVICE buffer buf (layout: int32
+ * off[n2][2], int32 ext[n2][2], then the fp64 boxes in cell order, row-major).
+ * buf = NULL: only *bytes is set (required size).  cap < size: DD_ERR_ARG.
+ * Synchronises the context stream.  Valid for any row whose marginals are
+ * current in this context. */
+dd_status domdec_halo_pack(dd_ctx *ctx, int32_t row, void *buf, int64_t cap, int64_t *bytes);
+
+/* Replace the marginals of basic-cell row `row` by the content of the DEVICE
+ * buffer buf (as written by domdec_halo_pack of another context of the same
+ * problem).  The boxes are appended to the current pool (DD_ERR_NUMERIC if it
+ * is full).  Synchronises. */
+dd_status domdec_halo_unpack(dd_ctx *ctx, int32_t row, const void *buf, int64_t bytes);
 
 /* Release all device memory of ctx.  NULL is a no-op. */
 dd_status domdec_destroy(dd_ctx *ctx);

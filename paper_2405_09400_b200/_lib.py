@@ -36,7 +36,8 @@ class _Problem(C.Structure):
 class _Options(C.Structure):
     _fields_ = [("err", C.c_double), ("max_iter", C.c_int32), ("fixed_iter", C.c_int32),
                 ("trunc", C.c_double), ("slot_cap", C.c_int32), ("comp_cap", C.c_int32),
-                ("device", C.c_int32), ("stream", C.c_void_p), ("track_primal", C.c_int32)]
+                ("device", C.c_int32), ("stream", C.c_void_p), ("track_primal", C.c_int32),
+                ("row_begin", C.c_int32), ("row_end", C.c_int32)]
 
 
 class SweepStats(C.Structure):
@@ -91,6 +92,8 @@ def lib():
         L.dd_mincost_flow.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                       C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(FlowStats),
                                       C.c_int32, vp]
+        L.domdec_halo_pack.argtypes = [vp, C.c_int32, vp, C.c_int64, C.POINTER(C.c_int64)]
+        L.domdec_halo_unpack.argtypes = [vp, C.c_int32, vp, C.c_int64]
         L.domdec_destroy.argtypes = [vp]
         L.domdec_counters.argtypes = [vp, C.POINTER(Counters)]
         L.domdec_reset_counters.argtypes = [vp]
@@ -101,7 +104,7 @@ def lib():
         for fn in ("domdec_init", "domdec_sweep", "flow_update", "marginal_error", "primal_dual_gap",
                    "domdec_export_cells", "domdec_export_alpha", "domdec_export_plan_cost",
                    "flow_edge_costs", "flow_apply", "dd_mincost_flow", "domdec_destroy", "domdec_counters",
-                   "domdec_reset_counters", "dd_mufu_peak"):
+                   "domdec_reset_counters", "dd_mufu_peak", "domdec_halo_pack", "domdec_halo_unpack"):
             getattr(L, fn).restype = C.c_int
         _lib = L
     return _lib
@@ -110,7 +113,7 @@ def lib():
 EXPORTED = ("domdec_init", "domdec_sweep", "flow_update", "marginal_error", "primal_dual_gap",
             "domdec_export_cells", "domdec_export_alpha", "domdec_export_plan_cost", "flow_edge_costs",
             "flow_apply", "dd_mincost_flow", "domdec_destroy", "dd_last_error", "dd_version", "domdec_counters",
-            "domdec_reset_counters", "dd_mufu_peak")
+            "domdec_reset_counters", "dd_mufu_peak", "domdec_halo_pack", "domdec_halo_unpack")
 
 
 def _ptr(a, ctype):
@@ -131,7 +134,7 @@ class DomDec:
 
     def __init__(self, mu, nu, cell_size, eps, h, init_off, init_ext, init_pos, init_data, mass_exponent,
                  err=1e-4, max_iter=2000, fixed_iter=0, trunc=1e-15, slot_cap=0, comp_cap=0, device=0,
-                 stream=None, track_primal=False):
+                 stream=None, track_primal=False, row_begin=0, row_end=0):
         self._keep = [np.ascontiguousarray(mu, np.float64), np.ascontiguousarray(nu, np.float64),
                       np.ascontiguousarray(init_off, np.int32), np.ascontiguousarray(init_ext, np.int32),
                       np.ascontiguousarray(init_pos, np.int64), np.ascontiguousarray(init_data, np.float64)]
@@ -144,7 +147,8 @@ class DomDec:
                      _ptr(off_, C.c_int32), _ptr(ext_, C.c_int32), _ptr(pos_, C.c_int64), _ptr(data_, C.c_double),
                      int(mass_exponent))
         O = _Options(float(err), int(max_iter), int(fixed_iter), float(trunc), int(slot_cap), int(comp_cap),
-                     int(device), C.c_void_p(stream) if stream else None, int(bool(track_primal)))
+                     int(device), C.c_void_p(stream) if stream else None, int(bool(track_primal)),
+                     int(row_begin), int(row_end))
         ctx = C.c_void_p()
         _check(lib().domdec_init(C.byref(P), C.byref(O), C.byref(ctx)), None)
         self._ctx = ctx
@@ -175,6 +179,22 @@ class DomDec:
         v = [C.c_double() for _ in range(4)]
         _check(lib().primal_dual_gap(self._ctx, *[C.byref(a) for a in v]), self._ctx)
         return tuple(a.value for a in v)
+
+    def halo_size(self, row):
+        """Bytes of the serialised marginals of basic-cell row `row`."""
+        n = C.c_int64()
+        _check(lib().domdec_halo_pack(self._ctx, int(row), None, 0, C.byref(n)), self._ctx)
+        return n.value
+
+    def halo_pack(self, row, dev_ptr, cap):
+        """Serialise row `row` into the device buffer at dev_ptr (cap bytes)."""
+        n = C.c_int64()
+        _check(lib().domdec_halo_pack(self._ctx, int(row), C.c_void_p(dev_ptr), int(cap), C.byref(n)), self._ctx)
+        return n.value
+
+    def halo_unpack(self, row, dev_ptr, nbytes):
+        """Replace row `row` by a buffer written by halo_pack (device pointer)."""
+        _check(lib().domdec_halo_unpack(self._ctx, int(row), C.c_void_p(dev_ptr), int(nbytes)), self._ctx)
 
     def export_cells(self):
         I = self.I

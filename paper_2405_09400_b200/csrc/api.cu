@@ -29,14 +29,22 @@ __global__ void k_init_mu(const double* __restrict__ mu, float* __restrict__ muf
 // Y-marginal of the stored state: scatter-add all boxes (diagnostic, fp64).
 __global__ void k_scatter_boxes(const double* __restrict__ pool, const long long* __restrict__ pos,
                                 const int* __restrict__ off, const int* __restrict__ ext, int N2,
-                                double* __restrict__ acc) {
-  const int i = blockIdx.x;
+                                double* __restrict__ acc, int i0) {
+  const int i = i0 + blockIdx.x;
   const int r0 = off[2 * i], c0 = off[2 * i + 1], e1 = ext[2 * i], e2 = ext[2 * i + 1];
   const double* src = pool + pos[i];
   for (int t = threadIdx.x; t < e1 * e2; t += blockDim.x) {
     const int r = t / e2, c = t - r * e2;
     atomicAdd(&acc[(long long)(r0 + r) * N2 + c0 + c], src[t]);
   }
+}
+
+// Halo pack / unpack: one CTA per cell of the row; meta[3 k .. 3 k + 2] =
+// (source element offset, destination element offset, length).
+__global__ void k_copy_boxes(const double* __restrict__ src, double* __restrict__ dst,
+                             const long long* __restrict__ meta) {
+  const long long s0 = meta[3 * blockIdx.x], d0 = meta[3 * blockIdx.x + 1], len = meta[3 * blockIdx.x + 2];
+  for (long long t = threadIdx.x; t < len; t += blockDim.x) dst[d0 + t] = src[s0 + t];
 }
 
 // Deterministic single-block reductions for the diagnostics.
@@ -150,7 +158,7 @@ void free_ctx(dd_ctx* c) {
                   c->d_off[1], c->d_ext[0], c->d_ext[1], c->d_cells[0], c->d_cells[1], c->d_alpha[0],
                   c->d_alpha[1], c->d_gauge[0], c->d_gauge[1], c->d_stats[0], c->d_stats[1], c->d_totals[0],
                   c->d_totals[1], c->d_mom, c->d_xbar, c->d_var, c->d_cbar, c->d_C, c->d_w, c->d_mcf,
-                  c->d_flow_info, c->d_scratch, c->d_red, c->d_ovf, c->d_cum, c->d_ecell, c->d_pd};
+                  c->d_flow_info, c->d_scratch, c->d_red, c->d_ovf, c->d_cum, c->d_ecell, c->d_pd, c->d_halo};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -206,6 +214,19 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c) 
   }
   if (O == nullptr) c->opt.trunc = 1e-15;
   c->device = c->opt.device;
+  // stripe mode: owned basic-cell rows [rb, re)
+  if (c->opt.row_begin == 0 && c->opt.row_end == 0) {
+    c->rb = 0;
+    c->re = c->n1;
+  } else {
+    c->rb = c->opt.row_begin;
+    c->re = c->opt.row_end;
+    if (c->rb < 0 || c->re > c->n1 || c->rb >= c->re || (c->rb & 1) || ((c->re & 1) && c->re != c->n1)) {
+      c->err = "row range must satisfy 0 <= row_begin < row_end <= n1 with even boundaries (A-cell rows)";
+      return DD_ERR_ARG;
+    }
+  }
+  c->stripe = !(c->rb == 0 && c->re == c->n1);
   const long long NN = (long long)c->N1 * c->N2;
   const int I = c->I, s = c->s;
   // ---- host validation (PAPER.md:233 m_i > 0; feasibility of pi^0) ----------
@@ -314,7 +335,17 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c) 
     TRY(dalloc(c, &c->d_pos[b], (size_t)I));
     TRY(dalloc(c, &c->d_off[b], (size_t)I * 2));
     TRY(dalloc(c, &c->d_ext[b], (size_t)I * 2));
-    c->h_cells[b] = build_partition(c->n1, c->n2, s, b);
+    {
+      // stripe mode keeps the A-cells of the owned rows and the B-cells whose
+      // lower row 2 b1 is owned (+ the last B row when the stripe ends the grid)
+      std::vector<CompCell> all = build_partition(c->n1, c->n2, s, b), kept;
+      for (const CompCell& cc : all) {
+        const int row = cc.r0 / s;
+        const int key = b == 0 ? row : 2 * ((row + 1) / 2);
+        if ((key >= c->rb && key < c->re) || (b == 1 && c->re == c->n1 && key >= c->n1)) kept.push_back(cc);
+      }
+      c->h_cells[b] = kept;
+    }
     c->ncells[b] = (int)c->h_cells[b].size();
     TRY(dalloc(c, &c->d_cells[b], c->ncells[b]));
     TRY(dalloc(c, &c->d_alpha[b], NN));
@@ -474,8 +505,10 @@ dd_status marginal_error(dd_ctx* c, double* l1_x, double* l1_y) {
     DD_CUDA(cudaMemcpyAsync(&hx, c->d_red, 8, cudaMemcpyDeviceToHost, c->stream));
   }
   DD_CUDA(cudaMemsetAsync(c->d_scratch, 0, NN * 8, c->stream));
-  k_scatter_boxes<<<c->I, 128, 0, c->stream>>>(c->d_pool[c->cur], c->d_pos[c->cur], c->d_off[c->cur],
-                                               c->d_ext[c->cur], c->N2, c->d_scratch);
+  // owned rows only (stripe mode: a partial sum of the global Y-marginal)
+  k_scatter_boxes<<<(c->re - c->rb) * c->n2, 128, 0, c->stream>>>(c->d_pool[c->cur], c->d_pos[c->cur],
+                                                                  c->d_off[c->cur], c->d_ext[c->cur], c->N2,
+                                                                  c->d_scratch, c->rb * c->n2);
   DD_CUDA(cudaGetLastError());
   k_l1_diff<<<1, 1024, 0, c->stream>>>(c->d_scratch, c->d_nu, NN, c->d_red + 8);
   DD_CUDA(cudaGetLastError());
@@ -495,6 +528,8 @@ dd_status domdec_export_cells(dd_ctx* c, int32_t* off, int32_t* ext, int64_t* po
   DD_CUDA(cudaMemcpyAsync(ho.data(), c->d_off[c->cur], I * 8, cudaMemcpyDeviceToHost, c->stream));
   DD_CUDA(cudaMemcpyAsync(he.data(), c->d_ext[c->cur], I * 8, cudaMemcpyDeviceToHost, c->stream));
   DD_CUDA(cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < I; ++i)   // stripe mode: cells outside the owned rows are not current here
+    if (i < c->rb * c->n2 || i >= c->re * c->n2) ho[2 * i] = ho[2 * i + 1] = he[2 * i] = he[2 * i + 1] = 0;
   int64_t total = 0;
   for (int i = 0; i < I; ++i) total += (int64_t)he[2 * i] * he[2 * i + 1];
   if (data_len) *data_len = total;
@@ -523,7 +558,7 @@ dd_status domdec_export_cells(dd_ctx* c, int32_t* off, int32_t* ext, int64_t* po
   int64_t p = 0;
   for (int i = 0; i < I; ++i) {
     const int64_t len = (int64_t)he[2 * i] * he[2 * i + 1];
-    std::memcpy(data + p, &pool[(size_t)hp[i]], len * 8);
+    if (len) std::memcpy(data + p, &pool[(size_t)hp[i]], len * 8);
     p += len;
   }
   return DD_OK;
@@ -582,12 +617,20 @@ dd_status flow_update(dd_ctx* c, dd_flow_stats* stats) {
     c->err = "flow_update needs a previous sweep (plan costs, reading R13)";
     return DD_ERR_PRECOND;
   }
+  if (c->stripe) {
+    c->err = "stripe mode: run the flow update through flow_edge_costs / dd_mincost_flow / flow_apply";
+    return DD_ERR_ARG;
+  }
   DD_CUDA(cudaSetDevice(c->device));
   return flow_update_impl(c, stats);
 }
 
 dd_status primal_dual_gap(dd_ctx* c, double* primal, double* dual, double* rel_gap, double* transport_cost) {
   if (!c) return DD_ERR_ARG;
+  if (c->stripe) {
+    c->err = "primal_dual_gap is not available in stripe mode";
+    return DD_ERR_ARG;
+  }
   if (c->swept != 3) {
     c->err = "primal_dual_gap needs at least one A and one B sweep";
     return DD_ERR_PRECOND;
@@ -664,6 +707,92 @@ dd_status dd_mufu_peak(int32_t device, double* ops_per_s) {
   cudaFree(d);
   if (cudaGetLastError() != cudaSuccess || ms <= 0) return DD_ERR_CUDA;
   *ops_per_s = (double)blocks * threads * iters * 8.0 / (ms * 1e-3);
+  return DD_OK;
+}
+
+dd_status domdec_halo_pack(dd_ctx* c, int32_t row, void* buf, int64_t cap, int64_t* bytes) {
+  if (!c || row < 0 || row >= c->n1) return DD_ERR_ARG;
+  DD_CUDA(cudaSetDevice(c->device));
+  const int n2 = c->n2, i0 = row * n2;
+  std::vector<int> ho(2 * n2), he(2 * n2);
+  std::vector<long long> hp(n2);
+  DD_CUDA(cudaMemcpyAsync(ho.data(), c->d_off[c->cur] + 2 * i0, n2 * 8, cudaMemcpyDeviceToHost, c->stream));
+  DD_CUDA(cudaMemcpyAsync(he.data(), c->d_ext[c->cur] + 2 * i0, n2 * 8, cudaMemcpyDeviceToHost, c->stream));
+  DD_CUDA(cudaMemcpyAsync(hp.data(), c->d_pos[c->cur] + i0, n2 * 8, cudaMemcpyDeviceToHost, c->stream));
+  DD_CUDA(cudaStreamSynchronize(c->stream));
+  const long long head = 16LL * n2;   // off + ext, int32; a multiple of 8
+  std::vector<long long> meta(3 * (size_t)n2);
+  long long at = 0;
+  for (int k = 0; k < n2; ++k) {
+    const long long len = (long long)he[2 * k] * he[2 * k + 1];
+    meta[3 * k] = hp[k];
+    meta[3 * k + 1] = head / 8 + at;
+    meta[3 * k + 2] = len;
+    at += len;
+  }
+  const long long total = head + 8 * at;
+  if (bytes) *bytes = total;
+  if (!buf) return DD_OK;
+  if (cap < total) {
+    c->err = "halo buffer too small";
+    return DD_ERR_ARG;
+  }
+  if (!c->d_halo) TRY(dalloc(c, &c->d_halo, 3 * (size_t)n2));
+  char* b = (char*)buf;
+  DD_CUDA(cudaMemcpyAsync(b, ho.data(), 8LL * n2, cudaMemcpyHostToDevice, c->stream));
+  DD_CUDA(cudaMemcpyAsync(b + 8LL * n2, he.data(), 8LL * n2, cudaMemcpyHostToDevice, c->stream));
+  DD_CUDA(cudaMemcpyAsync(c->d_halo, meta.data(), meta.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  k_copy_boxes<<<n2, 128, 0, c->stream>>>(c->d_pool[c->cur], (double*)b, c->d_halo);
+  DD_CUDA(cudaGetLastError());
+  DD_CUDA(cudaStreamSynchronize(c->stream));
+  return DD_OK;
+}
+
+dd_status domdec_halo_unpack(dd_ctx* c, int32_t row, const void* buf, int64_t bytes) {
+  if (!c || !buf || row < 0 || row >= c->n1) return DD_ERR_ARG;
+  DD_CUDA(cudaSetDevice(c->device));
+  const int n2 = c->n2, i0 = row * n2;
+  const long long head = 16LL * n2;
+  std::vector<int> ho(2 * n2), he(2 * n2);
+  const char* b = (const char*)buf;
+  DD_CUDA(cudaMemcpyAsync(ho.data(), b, 8LL * n2, cudaMemcpyDeviceToHost, c->stream));
+  DD_CUDA(cudaMemcpyAsync(he.data(), b + 8LL * n2, 8LL * n2, cudaMemcpyDeviceToHost, c->stream));
+  unsigned long long used = 0;
+  DD_CUDA(cudaMemcpyAsync(&used, c->d_poolctr + c->cur, 8, cudaMemcpyDeviceToHost, c->stream));
+  DD_CUDA(cudaStreamSynchronize(c->stream));
+  std::vector<long long> meta(3 * (size_t)n2), hp(n2);
+  long long at = 0;
+  for (int k = 0; k < n2; ++k) {
+    const long long len = (long long)he[2 * k] * he[2 * k + 1];
+    if (he[2 * k] < 0 || he[2 * k + 1] < 0 || ho[2 * k] < 0 || ho[2 * k] + he[2 * k] > c->N1 || ho[2 * k + 1] < 0 ||
+        ho[2 * k + 1] + he[2 * k + 1] > c->N2) {
+      c->err = "halo buffer: box outside the grid";
+      return DD_ERR_ARG;
+    }
+    meta[3 * k] = head / 8 + at;
+    meta[3 * k + 1] = (long long)used + at;
+    meta[3 * k + 2] = len;
+    hp[k] = (long long)used + at;
+    at += len;
+  }
+  if (head + 8 * at != bytes) {
+    c->err = "halo buffer size does not match its header";
+    return DD_ERR_ARG;
+  }
+  if ((long long)used + at > c->pool_cap) {
+    c->err = "pool full while unpacking a halo row";
+    return DD_ERR_NUMERIC;
+  }
+  if (!c->d_halo) TRY(dalloc(c, &c->d_halo, 3 * (size_t)n2));
+  const unsigned long long nu = used + (unsigned long long)at;
+  DD_CUDA(cudaMemcpyAsync(c->d_halo, meta.data(), meta.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  k_copy_boxes<<<n2, 128, 0, c->stream>>>((const double*)b, c->d_pool[c->cur], c->d_halo);
+  DD_CUDA(cudaGetLastError());
+  DD_CUDA(cudaMemcpyAsync(c->d_off[c->cur] + 2 * i0, ho.data(), n2 * 8, cudaMemcpyHostToDevice, c->stream));
+  DD_CUDA(cudaMemcpyAsync(c->d_ext[c->cur] + 2 * i0, he.data(), n2 * 8, cudaMemcpyHostToDevice, c->stream));
+  DD_CUDA(cudaMemcpyAsync(c->d_pos[c->cur] + i0, hp.data(), n2 * 8, cudaMemcpyHostToDevice, c->stream));
+  DD_CUDA(cudaMemcpyAsync(c->d_poolctr + c->cur, &nu, 8, cudaMemcpyHostToDevice, c->stream));
+  DD_CUDA(cudaStreamSynchronize(c->stream));
   return DD_OK;
 }
 

@@ -47,6 +47,9 @@ struct dd_ctx {
   long long n_sweeps = 0, n_flows = 0;
   int last_part = -1;
   int swept = 0;
+  int rb = 0, re = 0;          // owned basic-cell rows [rb, re) (stripe mode if not the whole grid)
+  bool stripe = false;
+  long long* d_halo = nullptr; // [3 * n2] halo pack/unpack metadata
   bool primal_valid = false;   // the last sweep recorded d_ecell
   double* d_mom = nullptr;   // [I][6] plan moments of the last sweep (R13)
   double* d_ecell = nullptr; // [max ncells] primal score per composite cell of the last sweep / h^2

@@ -104,7 +104,7 @@ __global__ void k_apply_flow(const long long* __restrict__ w, const long long* _
                              const int* __restrict__ off, const int* __restrict__ ext, double* __restrict__ pool_new,
                              long long* __restrict__ pos_new, int* __restrict__ off_new, int* __restrict__ ext_new,
                              unsigned long long* __restrict__ ctr, long long cap, double tau,
-                             unsigned long long* __restrict__ counters, double* __restrict__ dropped) {
+                             unsigned long long* __restrict__ counters, double* __restrict__ dropped, int j0) {
   extern __shared__ __align__(16) double rowbuf[];
   __shared__ int src[5];
   __shared__ double frac[5];
@@ -113,7 +113,7 @@ __global__ void k_apply_flow(const long long* __restrict__ w, const long long* _
   __shared__ long long base;
   __shared__ int mm[4];
   __shared__ double dsum[32];
-  const int j = blockIdx.x, tid = threadIdx.x, T = blockDim.x;
+  const int j = j0 + blockIdx.x, tid = threadIdx.x, T = blockDim.x;
   if (w[5LL * j] == q[j]) {   // no inflow from a neighbour: nu_j unchanged
     const long long len = (long long)ext[2 * j] * ext[2 * j + 1];
     if (tid == 0) {
@@ -275,10 +275,12 @@ static dd_status apply_w(dd_ctx* c, unsigned long long* d_counters, double* d_dr
     configured = smem;
   }
   DD_CUDA(cudaMemsetAsync(c->d_poolctr + spare, 0, 8, c->stream));
-  k_apply_flow<<<I, 128, smem, c->stream>>>((const long long*)c->d_w, (const long long*)c->d_q, c->n1, c->n2,
-                                             c->d_pool[cur], c->d_pos[cur], c->d_off[cur], c->d_ext[cur],
-                                             c->d_pool[spare], c->d_pos[spare], c->d_off[spare], c->d_ext[spare],
-                                             c->d_poolctr + spare, c->pool_cap, c->opt.trunc, d_counters, d_dropped);
+  // owned rows only (stripe mode: their neighbours' rows must be current)
+  (void)I;
+  k_apply_flow<<<(c->re - c->rb) * c->n2, 128, smem, c->stream>>>(
+      (const long long*)c->d_w, (const long long*)c->d_q, c->n1, c->n2, c->d_pool[cur], c->d_pos[cur],
+      c->d_off[cur], c->d_ext[cur], c->d_pool[spare], c->d_pos[spare], c->d_off[spare], c->d_ext[spare],
+      c->d_poolctr + spare, c->pool_cap, c->opt.trunc, d_counters, d_dropped, c->rb * c->n2);
   DD_CUDA(cudaGetLastError());
   c->cur = spare;   // the new state (failures are reported by counters[1])
   return DD_OK;

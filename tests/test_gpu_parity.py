@@ -272,3 +272,35 @@ def test_primal_dual_gap_requires_tracking():
     dd.sweep("B")
     with pytest.raises(DomDecError):
         dd.primal_dual_gap()
+
+
+@gpu
+@pytest.mark.parametrize("cfg,world", [("cfg2_gm", 2), ("cfg2_gm", 4), ("cfg2_bumps", 3)])
+def test_stripes_bit_identical_to_single_context(cfg, world):
+    """SURVEY §8(e) correctness invariant: the striped state (stripe contexts,
+    halo rows exchanged, global flow instance all-gathered, replicated exact
+    min-cost flow) is bit-identical to the unstriped one after hybrid cycles.
+    All ranks run in one process on one GPU, one after the other (loopback
+    transport: no kernel waits on another rank)."""
+    from paper_2405_09400_b200.stripes import GpuEngine, cycle_program, run_sequential, stripe_rows
+    p = CONFIGS[cfg]()
+    dd = gpu_ctx(p)
+    n1, n2 = dd.n1, dd.n2
+    rows = stripe_rows(n1, world)
+    engs = [GpuEngine(p, rows[r], rows[r + 1]) for r in range(world)]
+    moved = 0
+    for _ in range(3):
+        dd.sweep("A")
+        dd.sweep("B")
+        st = dd.flow_update(stats=True)
+        moved += st["changed_cells"]
+        run_sequential([cycle_program(engs[r], r, world, rows, n1, n2) for r in range(world)])
+    assert moved > 0       # the flow updates did move mass
+    ref = dd.boxes()
+    for r in range(world):
+        got = engs[r].boxes(rows[r], rows[r + 1])
+        for k, (g, o) in enumerate(zip(got, ref[rows[r] * n2:rows[r + 1] * n2])):
+            assert (g[0], g[1]) == (o[0], o[1]), (r, k)
+            np.testing.assert_array_equal(g[2], o[2])
+    for e in engs:
+        e.close()
