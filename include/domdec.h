@@ -129,6 +129,8 @@ typedef struct {
                           /* barrier like a push/relabel round                 */
   int64_t objective;      /* optimal sum_ij w_ij C_ij (integer costs, R11)     */
   int64_t changed_cells;  /* basic cells whose marginal was rewritten          */
+  double solver_ms;       /* device time of the min-cost-flow kernel (its own  */
+                          /* %globaltimer; 0 when the certificate held)        */
 } dd_flow_stats;
 
 /* Create a context: validate (DD_ERR_ARG / DD_ERR_PRECOND), copy the problem to

@@ -53,7 +53,7 @@ class SweepStats(C.Structure):
 class FlowStats(C.Structure):
     _fields_ = [("stationary", C.c_int32), ("certificate", C.c_int32), ("refines", C.c_int32),
                 ("rounds", C.c_int32), ("label_rounds", C.c_int32), ("objective", C.c_int64),
-                ("changed_cells", C.c_int64)]
+                ("changed_cells", C.c_int64), ("solver_ms", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

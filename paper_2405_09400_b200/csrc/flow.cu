@@ -317,6 +317,7 @@ dd_status flow_update_impl(dd_ctx* c, dd_flow_stats* stats) {
     stats->rounds = (int32_t)info[4];
     stats->label_rounds = (int32_t)info[5];
     stats->changed_cells = (int64_t)cnt[0];
+    stats->solver_ms = info[12] * 1e-6;
     if (info[6]) {
       c->err = "min-cost flow did not converge (round cap)";
       return DD_ERR_NUMERIC;
@@ -414,6 +415,7 @@ dd_status dd_mincost_flow(int32_t n1, int32_t n2, const int64_t* q, const int64_
           stats->rounds = (int32_t)info[4];
           stats->label_rounds = (int32_t)info[5];
           stats->changed_cells = 0;
+          stats->solver_ms = info[12] * 1e-6;
         }
         if (info[6]) s = DD_ERR_NUMERIC;
         if (getenv("DD_MCF_TIMERS"))

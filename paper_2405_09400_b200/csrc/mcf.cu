@@ -55,6 +55,9 @@ struct McfArgs {
   int tiled;              // 1: checkerboard tile phases instead of grid-wide rounds
   int tile_rounds;        // local rounds per tile phase
   int gu_tiled;           // tile phases between global price updates
+  int alpha;              // cost-scaling factor between refine phases
+  int bf_sweeps;          // local sweeps per grid round of the tiled Bellman-Ford
+  int pr_cap;             // grid rounds allowed to a price refinement (0: 64 + (n1 + n2) / 8)
 };
 
 __device__ __forceinline__ int nbr(int i, int a, int n1, int n2) {
@@ -203,7 +206,7 @@ __device__ __noinline__ bool tiled_bf(const McfArgs& A, cg::grid_group& grid, co
       __syncthreads();
       const int c = (ty + 1) * TP + tx + 1;
       bool ch_tile = false;
-      for (int sw = 0; sw < kSweeps; ++sw) {
+      for (int sw = 0; sw < A.bf_sweeps; ++sw) {
         bool ch = false;
         if (mine) {
           long long bs = sS[c], bt = sT[c];
@@ -558,10 +561,12 @@ __global__ void __launch_bounds__(512, 1) mcf_kernel(McfArgs A) {
   // ---- cost scaling -----------------------------------------------------------
   long long eps = (long long)A.ctr[0] * SC;
   int refines = 0, rounds = 0, par = 0;
-  const int pr_cap = 4 * (n1 + n2) + 128;
+  // a feasible refinement converges in a few dozen tiled rounds; a failing one
+  // runs to the cap, so keep it small
+  const int pr_cap = A.pr_cap > 0 ? A.pr_cap : 64 + (n1 + n2) / 8;
   bool failed = false;
   while (eps >= 1 && !failed) {
-    eps = (eps + 15) / 16;   // alpha = 16
+    eps = (eps + A.alpha - 1) / A.alpha;   // cost-scaling factor
     if (eps < 1) eps = 1;
     ++refines;
     // price refinement: after the first phase the flow is often already
@@ -837,6 +842,12 @@ dd_status mcf_solve_device(int n1, int n2, const int64_t* d_q, const int64_t* d_
   A.tiled = 1;
   A.tile_rounds = 16;
   A.gu_tiled = 16;
+  A.alpha = 16;
+  A.bf_sweeps = kSweeps;
+  A.pr_cap = 0;
+  if (const char* env = getenv("DD_MCF_PRCAP")) A.pr_cap = atoi(env);
+  if (const char* env = getenv("DD_MCF_ALPHA")) A.alpha = atoi(env) > 1 ? atoi(env) : A.alpha;
+  if (const char* env = getenv("DD_MCF_SWEEPS")) A.bf_sweeps = atoi(env) > 0 ? atoi(env) : A.bf_sweeps;
   if (const char* env = getenv("DD_MCF_GU")) A.gu_every = atoi(env) > 0 ? atoi(env) : A.gu_every;
   if (const char* env = getenv("DD_MCF_TILED")) A.tiled = atoi(env);
   if (const char* env = getenv("DD_MCF_MAXR")) A.max_rounds = atoi(env) > 0 ? atoi(env) : A.max_rounds;
