@@ -73,7 +73,7 @@ dd_status flow_update_impl(dd_ctx* c, dd_flow_stats* stats);
 dd_status flow_costs_impl(dd_ctx* c);
 dd_status flow_apply_impl(dd_ctx* c);
 dd_status mcf_solve_device(int n1, int n2, const int64_t* d_q, const int64_t* d_C, int64_t* d_w,
-                           void** d_ws, size_t* ws_bytes, int* d_info, cudaStream_t st, std::string& err);
+                           void** d_ws, size_t* ws_bytes, int warm, cudaStream_t st, std::string& err);
 dd_status flow_init_static(dd_ctx* c);
 dd_status pd_gap_impl(dd_ctx* c, double* primal, double* dual, double* rel_gap, double* transport);
 void set_global_error(const std::string& m);   // dd_last_error(NULL)

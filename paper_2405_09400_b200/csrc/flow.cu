@@ -297,7 +297,7 @@ dd_status flow_update_impl(dd_ctx* c, dd_flow_stats* stats) {
   ++c->n_flows;
   dd_status s = flow_costs_impl(c);
   if (s) return s;
-  s = mcf_solve_device(c->n1, c->n2, c->d_q, c->d_C, c->d_w, &c->d_mcf, &c->mcf_bytes, nullptr, c->stream, c->err);
+  s = mcf_solve_device(c->n1, c->n2, c->d_q, c->d_C, c->d_w, &c->d_mcf, &c->mcf_bytes, 1, c->stream, c->err);
   if (s) return s;
   unsigned long long* ctr = (unsigned long long*)c->d_flow_info;   // [0] changed, [1] failed
   double* dropped = (double*)(c->d_flow_info + 8);
@@ -398,7 +398,7 @@ dd_status dd_mincost_flow(int32_t n1, int32_t n2, const int64_t* q, const int64_
   } else {
     cudaMemcpyAsync(dq, q, I * 8, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(dC, C, I * 40, cudaMemcpyHostToDevice, st);
-    s = mcf_solve_device(n1, n2, dq, dC, dw, &ws, &wsb, nullptr, st, err);
+    s = mcf_solve_device(n1, n2, dq, dC, dw, &ws, &wsb, 0, st, err);
     if (s == DD_OK) {
       long long info[16];
       cudaMemcpyAsync(w, dw, I * 40, cudaMemcpyDeviceToHost, st);

@@ -58,6 +58,16 @@ struct McfArgs {
   int alpha;              // cost-scaling factor between refine phases
   int bf_sweeps;          // local sweeps per grid round of the tiled Bellman-Ford
   int pr_cap;             // grid rounds allowed to a price refinement (0: 64 + (n1 + n2) / 8)
+  // warm start (flow_update of a context): the supplies q are static across
+  // flow updates (q_i = m_i 2^E), so the previous optimal flow is feasible
+  // for the next instance and its prices are a good start; only the costs
+  // change (reading R11)
+  int warm;               // 1: start from (wW, wpS, wpT) when *wvalid, and store the result there
+  long long warm_div;     // first phase runs at eps = ceil(violation / warm_div)
+  long long* wW;          // [I][5] last optimal flow
+  long long* wpS;         // [I] its prices (scaled costs)
+  long long* wpT;         // [I]
+  long long* wvalid;      // [1]
 };
 
 __device__ __forceinline__ int nbr(int i, int a, int n1, int n2) {
@@ -523,10 +533,11 @@ __global__ void __launch_bounds__(512, 1) mcf_kernel(McfArgs A) {
   const long long SC = 2LL * I + 1;
 
   // ---- init: stationary flow, scaled costs, max |C| -------------------------
+  const bool warm = A.warm && *A.wvalid;
   for (long long i = gt; i < I; i += gs) {
     for (int a = 0; a < 5; ++a) {
       const int j = nbr((int)i, a, n1, n2);
-      A.w[5 * i + a] = (a == 0) ? A.q[i] : 0;
+      A.w[5 * i + a] = warm ? A.wW[5 * i + a] : ((a == 0) ? A.q[i] : 0);
       const long long c = (j >= 0 && a > 0) ? A.C[5 * i + a] : 0;
       A.cs[5 * i + a] = c * SC;
       if (j >= 0 && a > 0) {
@@ -536,8 +547,8 @@ __global__ void __launch_bounds__(512, 1) mcf_kernel(McfArgs A) {
       }
     }
     A.dist[0][i] = 0;
-    A.pS[0][i] = 0;
-    A.pT[0][i] = 0;
+    A.pS[0][i] = warm ? A.wpS[i] : 0;
+    A.pT[0][i] = warm ? A.wpT[i] : 0;
     A.eS[i] = 0;
     A.eT[i] = 0;
     A.addS[i] = 0;
@@ -560,14 +571,39 @@ __global__ void __launch_bounds__(512, 1) mcf_kernel(McfArgs A) {
   }
   // ---- cost scaling -----------------------------------------------------------
   long long eps = (long long)A.ctr[0] * SC;
+  long long warm_eps = 0;
+  if (warm) {
+    // smallest eps for which the warm (flow, prices) pair is eps-optimal
+    for (long long i = gt; i < I; i += gs) {
+      for (int a = 1; a < 5; ++a) {
+        const int j = nbr((int)i, a, n1, n2);
+        if (j < 0) continue;
+        const long long cp = A.cs[5 * i + a] + A.pS[0][i] - A.pT[0][j];
+        unsigned long long v = 0;
+        if (A.q[i] - A.w[5 * i + a] > 0 && cp < 0) v = (unsigned long long)(-cp);
+        if (A.w[5 * i + a] > 0 && cp > 0 && (unsigned long long)cp > v) v = (unsigned long long)cp;
+        if (v) atomicMax(&A.ctr[15], v);
+      }
+    }
+    grid.sync();
+    const long long viol = (long long)A.ctr[15];
+    warm_eps = (viol + A.warm_div - 1) / A.warm_div;
+    if (warm_eps < 1) warm_eps = 1;
+  }
+  bool first_phase = true;
   int refines = 0, rounds = 0, par = 0;
   // a feasible refinement converges in a few dozen tiled rounds; a failing one
   // runs to the cap, so keep it small
   const int pr_cap = A.pr_cap > 0 ? A.pr_cap : 64 + (n1 + n2) / 8;
   bool failed = false;
   while (eps >= 1 && !failed) {
-    eps = (eps + A.alpha - 1) / A.alpha;   // cost-scaling factor
-    if (eps < 1) eps = 1;
+    if (first_phase && warm) {
+      eps = warm_eps;
+    } else {
+      eps = (eps + A.alpha - 1) / A.alpha;   // cost-scaling factor
+      if (eps < 1) eps = 1;
+    }
+    first_phase = false;
     ++refines;
     // price refinement: after the first phase the flow is often already
     // optimal (degenerate instances) or eps-optimal for the next eps; then
@@ -766,6 +802,15 @@ __global__ void __launch_bounds__(512, 1) mcf_kernel(McfArgs A) {
   }
   grid.sync();
   const long long obj = (long long)A.ctr[8];
+  if (A.warm && !failed) {   // keep the optimal flow and its prices for the next flow update
+    for (long long i = gt; i < I; i += gs) {
+      for (int a = 0; a < 5; ++a) A.wW[5 * i + a] = A.w[5 * i + a];
+      A.wpS[i] = A.pS[par][i];
+      A.wpT[i] = A.pT[par][i];
+    }
+    if (gt == 0) *A.wvalid = 1;
+    grid.sync();
+  }
   if (obj >= 0 && !failed) {   // stationary flow is optimal: keep it exactly
     for (long long i = gt; i < I; i += gs)
       for (int a = 0; a < 5; ++a) A.w[5 * i + a] = (a == 0) ? A.q[i] : 0;
@@ -792,15 +837,16 @@ __global__ void __launch_bounds__(512, 1) mcf_kernel(McfArgs A) {
 }
 
 static size_t ws_size(int I) {
-  // cs, w handled by caller for w; workspace: cs[5I] eS eT addS addT pS0 pS1 pT0 pT1 d0 d1 ctr[16]
-  return sizeof(long long) * (5ull * I + 12ull * I) + 16 * sizeof(unsigned long long) + 256;
+  // cs, w handled by caller for w; workspace: cs[5I] eS eT addS addT pS0 pS1 pT0 pT1 d0 d1 ctr[16],
+  // info[16], warm state wW[5I] wpS[I] wpT[I] wvalid
+  return sizeof(long long) * (5ull * I + 12ull * I) + 16 * sizeof(unsigned long long) + 16 * sizeof(long long) +
+         sizeof(long long) * (7ull * I + 1) + 256;
 }
 
 dd_status mcf_solve_device(int n1, int n2, const int64_t* d_q, const int64_t* d_C, int64_t* d_w, void** d_ws,
-                           size_t* ws_bytes, int* d_info_unused, cudaStream_t st, std::string& err) {
-  (void)d_info_unused;
+                           size_t* ws_bytes, int warm, cudaStream_t st, std::string& err) {
   const int I = n1 * n2;
-  const size_t need = ws_size(I) + 16 * sizeof(long long);
+  const size_t need = ws_size(I);
   if (*ws_bytes < need) {
     if (*d_ws) cudaFree(*d_ws);
     *d_ws = nullptr;
@@ -809,6 +855,10 @@ dd_status mcf_solve_device(int n1, int n2, const int64_t* d_q, const int64_t* d_
       return DD_ERR_OOM;
     }
     *ws_bytes = need;
+    if (cudaMemsetAsync(*d_ws, 0, need, st) != cudaSuccess) {   // warm state invalid
+      err = "mcf workspace init failed";
+      return DD_ERR_CUDA;
+    }
   }
   char* base = (char*)*d_ws;
   McfArgs A;
@@ -833,7 +883,15 @@ dd_status mcf_solve_device(int n1, int n2, const int64_t* d_q, const int64_t* d_
   A.distT[0] = p; p += I;
   A.distT[1] = p; p += I;
   A.ctr = (unsigned long long*)p; p += 16;
-  A.info = p;
+  A.info = p; p += 16;
+  A.wW = p; p += 5LL * I;
+  A.wpS = p; p += I;
+  A.wpT = p; p += I;
+  A.wvalid = p;
+  A.warm = warm;
+  A.warm_div = 1LL << 40;   // warm start: one eps = 1 phase (tools/mcf_sim.cpp: 3x fewer rounds than cold)
+  if (const char* env = getenv("DD_MCF_WDIV")) A.warm_div = atoll(env) > 0 ? atoll(env) : A.warm_div;
+  if (const char* env = getenv("DD_MCF_WARM")) A.warm = warm && atoi(env);
   A.bf_rounds = 2 * (n1 + n2) + 8;
   A.max_rounds = 2000000;
   // rounds between global price updates: tuned on dumped flow-update

@@ -75,6 +75,7 @@ void solve(bool warm) {
       ll cp = cs[5*i+a] + pS[i] - pT[j];
       if (q[i] - w[5*i+a] > 0) viol = std::max(viol, -cp);
       if (w[5*i+a] > 0) viol = std::max(viol, cp); }
+    if (getenv("WALPHA")) alpha = atoi(getenv("WALPHA"));
     eps = viol * alpha;  // first refine runs at viol
     printf("warm start: initial violation %lld (cold eps %lld)\n", viol, cmax * SC);
   }
