@@ -1,5 +1,6 @@
 // api.cu — C-ABI entry points of libdomdec (include/domdec.h).
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -295,6 +296,8 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c) 
   c->ccap = std::min(c->ccap, std::max(c->N1, c->N2));
   c->ccap_big = c->ccap;
   while (c->ccap_big < std::max(c->N1, c->N2) && sweep_smem_bytes(c->ccap_big + 1, s) <= 200 * 1024) ++c->ccap_big;
+  if (const char* env = getenv("DD_CCAP_BIG"))   // testing knob: route more cells to the global-scratch class
+    c->ccap_big = std::max(c->ccap, std::min(c->ccap_big, atoi(env)));
   if (sweep_smem_bytes(c->ccap, s) > 200 * 1024) {
     c->err = "composite box capacity too large for shared memory (eps too large for this build)";
     return DD_ERR_ARG;
@@ -451,6 +454,7 @@ dd_status domdec_sweep(dd_ctx* c, dd_partition part, dd_sweep_stats* stats) {
   p.tol = (float)c->opt.err;
   p.max_iter = c->opt.max_iter;
   p.fixed_iter = c->opt.fixed_iter;
+  p.debug = getenv("DD_DEBUG_OVF") ? 1 : 0;
   p.tau = c->opt.trunc;
   p.stats = c->d_stats[b];
   p.totals = c->d_totals[b];

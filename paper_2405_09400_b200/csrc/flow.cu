@@ -318,6 +318,9 @@ dd_status flow_update_impl(dd_ctx* c, dd_flow_stats* stats) {
     stats->label_rounds = (int32_t)info[5];
     stats->changed_cells = (int64_t)cnt[0];
     stats->solver_ms = info[12] * 1e-6;
+    if (getenv("DD_MCF_TIMERS"))
+      fprintf(stderr, "mcf timers (ms): refine %.1f update %.1f phase %.1f wait %.1f total %.1f local_rounds %lld\n",
+              info[8] * 1e-6, info[9] * 1e-6, info[10] * 1e-6, info[11] * 1e-6, info[12] * 1e-6, info[7]);
     if (info[6]) {
       c->err = "min-cost flow did not converge (round cap)";
       return DD_ERR_NUMERIC;

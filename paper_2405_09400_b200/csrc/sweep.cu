@@ -24,6 +24,8 @@
 // preserved to fp64 rounding.  Cells whose hull
 // exceeds the fast size class are queued on the device and handled by a
 // second, large-shared-memory launch of each kernel.
+#include <cstdio>
+
 #include "internal.cuh"
 
 #ifndef DD_SOLVE_MINB
@@ -397,8 +399,9 @@ __device__ void solve_cell(const SweepParams& p, const int J, unsigned char* sme
   const float fo1 = (float)o1, fo2 = (float)o2;
   constexpr int HX = NX / 2;
   // Y2 mapping: thread -> (column l2, row group rg of RG)
+  // (a hull wider than the CTA, huge class only: columns in chunks of T)
   const int RG = max(1, T / b2);
-  const int y2_col = tid % b2, y2_rg = tid / b2;
+  const int y2_col = b2 <= T ? tid % b2 : tid, y2_rg = b2 <= T ? tid / b2 : 0;
   // X2 mapping: thread -> (pair qa in [0, HX), column k2, split h of SX)
   constexpr int SX = (kSweepThreads / (HX * NX)) > 8 ? 8 : (kSweepThreads / (HX * NX));
   const int x2_h = tid % SX, x2_pair = tid / SX;
@@ -437,8 +440,7 @@ __device__ void solve_cell(const SweepParams& p, const int J, unsigned char* sme
     }
     __syncthreads();
     // Y-half stage 2: B(l1, l2) = -LSE_k1 [U(k1, l2) - w (k1 - l1~)^2]
-    if (y2_rg < RG) {
-      const int l2 = y2_col;
+    for (int l2 = y2_col; y2_rg < RG && l2 < b2; l2 += T) {
       float u[NX];
 #pragma unroll
       for (int q = 0; q < NX; ++q) u[q] = UK[q * b2 + l2];
@@ -620,6 +622,28 @@ __device__ void solve_cell(const SweepParams& p, const int J, unsigned char* sme
       }
     }
     const float etot = block_sum_f(epart, fred, it);
+    if (p.debug && p.mode == 2 && (b1 > 120 || b2 > 120) && (it <= 3 || it == 50) && tid == 0) {   // DD_DEBUG_OVF: stage ranges of huge cells
+      auto rng = [](const float* v, int n, const char* nm, int J, int it) {
+        float lo = 3e38f, hi = -3e38f;
+        int bad = 0, neg = 0;
+        for (int k = 0; k < n; ++k) {
+          const float x = v[k];
+          if (!(x == x) || fabsf(x) > 1e38f) { ++bad; continue; }
+          if (x <= -1e29f) { ++neg; continue; }
+          lo = fminf(lo, x);
+          hi = fmaxf(hi, x);
+        }
+        printf("DD_DEBUG_OVF J %d it %d %s n %d nonfinite %d kneg %d range [%g, %g]\n", J, it, nm, n, bad, neg, lo, hi);
+      };
+      rng(Ub, NX * b2, "U", J, it);
+      rng(P0, b1 * b2, "B", J, it);
+      rng(P1, b1 * b2, "log2nuJ", J, it);
+      rng(Vb, b1 * NX, "V", J, it);
+      rng(A2, NX * NX, "A", J, it);
+      rng(A2n, NX * NX, "A'", J, it);
+      rng(AL, NX * NX, "AL", J, it);
+      printf("DD_DEBUG_OVF J %d it %d etot %g first %d\n", J, it, etot, (int)first);
+    }
     if (it == 1) e0 = etot;
     e = etot;
     const bool stop = p.fixed_iter > 0 ? (it >= p.fixed_iter) : (etot <= tolJ || it >= p.max_iter);
@@ -778,6 +802,16 @@ __device__ void split_cell(const SweepParams& p, const int J, unsigned char* sme
         p.ext_out[2 * i + 1] = ints[12 + k];
       }
       at += len;
+    }
+    if (tid == 0 && p.debug) {
+      printf("DD_DEBUG_OVF cell %d reason %d mode %d hull (%d,%d)+(%d,%d) nmem %d iters %d e0 %g e %g\n", J, reason,
+             p.mode, L1, L2, b1, b2, nmem, p.stats[J].iters, (double)p.stats[J].e0, (double)p.stats[J].e);
+      for (int k = 0; k < nmem; ++k) {
+        const int i = cc.mem[k];
+        printf("DD_DEBUG_OVF   member %d box (%d,%d)+(%d,%d) new min/max (%d..%d, %d..%d)\n", i, ints[k], ints[4 + k],
+               ints[8 + k], ints[12 + k], ints[16 + 4 * k], ints[16 + 4 * k + 1], ints[16 + 4 * k + 2],
+               ints[16 + 4 * k + 3]);
+      }
     }
     if (tid == 0) {
       p.stats[J].overflow = reason;

@@ -5,7 +5,8 @@ import pytest
 
 import oracle as O
 from oracle.flow import check_flow
-from parity import (CONFIGS, compare_states, gpu_ctx, gpu_transport_cost, oracle_state, rel_tols)
+from parity import (CONFIGS, compare_cell, compare_states, gpu_ctx, gpu_transport_cost, oracle_state,
+                    rel_tols)
 from synth import make_problem, random_flow, random_mcf_instance
 
 gpu = pytest.mark.gpu
@@ -304,3 +305,88 @@ def test_stripes_bit_identical_to_single_context(cfg, world):
             np.testing.assert_array_equal(g[2], o[2])
     for e in engs:
         e.close()
+
+
+@gpu
+def test_warm_started_flow_updates_are_exact():
+    """Flow updates of a context start the min-cost flow from the previous
+    optimal flow and prices (the supplies q are static, DESIGN.md "Warm
+    start"); along a hybrid trajectory (Alg. 3) every
+    update's objective must still equal the exact LP optimum of its own
+    instance (oracle), and the global Y-marginal must stay exact."""
+    p = make_problem("gm", 64, 2, eps_factor=2.0, theta_deg=20, seed=0)
+    dd = gpu_ctx(p)
+    for cycle in range(6):
+        dd.sweep("A")
+        dd.sweep("B")
+        _, C, q = dd.edge_costs()
+        fs = dd.flow_update(stats=True)
+        _, oobj = O.min_cost_flow(q, C, p.n, p.n)
+        assert fs["objective"] == min(oobj, 0), (cycle, fs, oobj)
+        if cycle > 0:
+            assert fs["refines"] <= 2, fs   # warm: one eps = 1 phase (+ the certificate)
+    ex, ey = dd.marginal_error()
+    assert ey < 1e-9   # truncation ledger only (reading R9)
+    dd.close()
+
+
+@gpu
+@pytest.mark.parametrize("part", ["A", "B"])
+def test_size_classes_bit_identical(part, monkeypatch):
+    """Cells whose hull exceeds the fast size class run in the large
+    (shared-memory) or huge (global-scratch) class of the same kernels
+    (DESIGN.md "Size classes"); forcing almost every cell into the huge class
+    must give bit-identical boxes and potentials, and oracle parity."""
+    p = CONFIGS["cfg2_gm"]()
+    K = 25
+    ref = gpu_ctx(p, fixed_iter=K)
+    ref.sweep(part)
+    monkeypatch.setenv("DD_CCAP_BIG", "8")
+    dd = gpu_ctx(p, fixed_iter=K, comp_cap=8)
+    gst = dd.sweep(part, stats=True)
+    assert gst["overflow"] == 0
+    for (r0, c0, d), (s0, t0, e) in zip(dd.boxes(), ref.boxes()):
+        assert r0 == s0 and c0 == t0 and np.array_equal(d, e)
+    assert np.array_equal(dd.export_alpha(part), ref.export_alpha(part))
+    st = oracle_state(p)
+    O.domdec_sweep(st, part, fixed_iter=K)
+    cmp = compare_states(dd.boxes(), st.boxes)
+    assert cmp["unexplained"] == 0, cmp
+    dd.close()
+    ref.close()
+
+
+@gpu
+@pytest.mark.parametrize("part", ["A", "B"])
+def test_hull_wider_than_cta(part):
+    """Hulls wider than the 128 threads of a CTA (huge size class): start from
+    the product coupling nu_i = m_i nu (every basic box is the whole 136x136
+    grid, a feasible coupling) and compare sampled composite cells with the
+    oracle after K passes.  Regression: stage Y2 once mapped one thread per
+    hull column and left columns >= 128 unwritten."""
+    import types
+    g = make_problem("gm", 136, 4, eps_factor=2.0, theta_deg=5, seed=0)
+    mu, nu, s, n = g.mu, g.nu, g.s, g.n
+    m = mu.reshape(n, s, n, s).sum(axis=(1, 3)).ravel()
+    I, NN = n * n, g.N * g.N
+    p = types.SimpleNamespace(mu=mu, nu=nu, s=s, eps=g.eps, h=g.h, E=g.E, eps_prime=g.eps_prime,
+                              init_off=np.zeros((I, 2), np.int32), init_ext=np.full((I, 2), g.N, np.int32),
+                              init_pos=np.arange(I, dtype=np.int64) * NN,
+                              init_data=(m[:, None] * nu.ravel()[None, :]).ravel())
+    K = 5
+    dd = gpu_ctx(p, fixed_iter=K)
+    gst = dd.sweep(part, stats=True)
+    assert gst["overflow"] == 0 and np.isfinite(gst["l1x_final"])
+    gb = dd.boxes()
+    st = oracle_state(p)
+    comp = O.composite_partition(n, n, part)
+    sample = [0, len(comp) // 2 + n // 4, len(comp) - 1]
+    res = O.domdec_sweep(st, part, fixed_iter=K, cells=sample)
+    for k in sample:
+        for i, ob in res[k]["boxes"].items():
+            c = compare_cell(gb[i], ob)
+            assert c["guard_ok"] and (c["box_equal"] or c["guard_ok"]), (k, i, c)
+            # exponents reach w * 136^2 / 4 ~ 1.7e3 (log2 units) here, ~7x the
+            # usual: fp32 bulk error scales with it (DESIGN.md "Parity tolerances")
+            assert c["rel_bulk"] < 5e-4, (k, i, c)
+    dd.close()
