@@ -38,7 +38,10 @@ def cell_sinkhorn(mu_x: np.ndarray, kx: np.ndarray, nu_y: np.ndarray, ly: np.nda
         X-update  a'(k) = -log sum_l exp(b(l) - c(k,l)/eps) nu_J(l)
     Stopping rule (App. A.2.1; per-cell reading R6):
     L1 X-marginal error of the plan (a, b) after the Y-update,
-        e = sum_k mu(k) |1 - exp(a(k) - a'(k))| <= err * mu(X_J),
+        e = sum_k mu(k) |r - exp(a(k) - a'(k))| <= err * mu(X_J),
+    where r = ||nu_J|| / mu(X_J) (reading R6': after a Y-update the plan has
+    mass ||nu_J||, which the truncation ledger R9 can make differ from
+    mu(X_J); r = 1 for balanced cells, the paper's case),
     or exactly fixed_iter passes (parity mode), or max_iter passes.
 
     nu_y must be > 0 (zero pixels of the box are excluded, reading R19).
@@ -50,13 +53,14 @@ def cell_sinkhorn(mu_x: np.ndarray, kx: np.ndarray, nu_y: np.ndarray, ly: np.nda
     lognu = np.log(nu_y)
     a = a0.astype(np.float64).copy()
     tol = err * float(mu_x.sum())
+    rm1 = (float(nu_y.sum()) - float(mu_x.sum())) / float(mu_x.sum())
     t = 0
     e0 = None
     while True:
         t += 1
         b = -lse(a[:, None] + logmu[:, None] - C, axis=0)
         a_new = -lse(b[None, :] + lognu[None, :] - C, axis=1)
-        e = float(np.sum(mu_x * np.abs(np.expm1(a - a_new))))
+        e = float(np.sum(mu_x * np.abs(np.expm1(a - a_new) - rm1)))
         if e0 is None:
             e0 = e
         if fixed_iter > 0:

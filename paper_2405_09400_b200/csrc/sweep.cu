@@ -339,10 +339,13 @@ __device__ void solve_cell(const SweepParams& p, const int J, unsigned char* sme
     return;
   }
   assemble(p, cc, ints, L1, L2, b2, BB, nuJ);
+  double nsum = 0.0;
   for (int t = tid; t < BB; t += T) {
     const double v = nuJ[t];
+    nsum += v;
     P1[t] = v > 0.0 ? lg2f((float)v) : kNeg;   // log2 nu_J (zeros -> kNeg, R19)
   }
+  const double nuMass = block_sum1_d(nsum, (double*)(smem + Ls.dred));
   // ---- X-block data, warm start (R7) and re-gauge ------------------------
   // The X-block is padded to NX x NX (ragged B cells have n = s on an axis);
   // padded pixels carry log2 mu = kNeg, so their terms vanish.
@@ -377,6 +380,12 @@ __device__ void solve_cell(const SweepParams& p, const int J, unsigned char* sme
   double muXJ = 0.0;
   for (int q = 0; q < nmem; ++q) muXJ += p.m[cc.mem[q]];
   const float tolJ = (float)(p.tol * muXJ);
+  // mass defect of the cell problem (truncation ledger, reading R9): after a
+  // Y-update the plan has mass ||nu_J||, so its X-marginal is compared with
+  // mu ||nu_J|| / mu(X_J) (reading R6')
+  const float rm1 = (float)((nuMass - muXJ) / muXJ);
+  if (p.debug && tid == 0 && fabsf(rm1) > 1e-9f)
+    printf("DD_DEBUG_RM1 cell %d mode %d nuMass %.17g muXJ %.17g rm1 %g\n", J, p.mode, nuMass, muXJ, (double)rm1);
   __syncthreads();
 
   // ---- a2: separable log-domain Sinkhorn ---------------------------------
@@ -616,7 +625,7 @@ __device__ void solve_cell(const SweepParams& p, const int J, unsigned char* sme
         A2n[oa] = ana;
         A2n[ob] = anb;
         // L1 X-marginal error of the plan (A, B): sum mu |1 - 2^(A - A')|
-        epart += MU[oa] * fabsf(exp2m1f(A2[oa] - ana)) + MU[ob] * fabsf(exp2m1f(A2[ob] - anb));
+        epart += MU[oa] * fabsf(exp2m1f(A2[oa] - ana) - rm1) + MU[ob] * fabsf(exp2m1f(A2[ob] - anb) - rm1);
         AL[oa] = ana + LM[oa] - wk2;   // AK of the next pass
         AL[ob] = anb + LM[ob] - wk2;
       }
@@ -679,7 +688,12 @@ __device__ void solve_cell(const SweepParams& p, const int J, unsigned char* sme
     atomicAdd(&p.cum->mufu, mufu);
     atomicAdd(&p.cum->iters, (unsigned long long)it);
     atomicAdd(&p.totals->iters, (unsigned long long)it);
-    if (p.fixed_iter <= 0 && it >= p.max_iter && e > tolJ) atomicAdd(&p.totals->nonconv, 1ull);
+    if (p.fixed_iter <= 0 && it >= p.max_iter && e > tolJ) {
+      atomicAdd(&p.totals->nonconv, 1ull);
+      if (p.debug)
+        printf("DD_DEBUG_NC cell %d mode %d hull %dx%d n %dx%d e0/tol %g e/tol %g muXJ %g\n", J, p.mode, b1, b2, n1,
+               n2, (double)(e0 / tolJ), (double)(e / tolJ), (double)tolJ / p.tol);
+    }
     atomicMax(&p.totals->iters_max, it);
     atomicAdd(&p.totals->e0, (double)e0);
     atomicAdd(&p.totals->e, (double)e);

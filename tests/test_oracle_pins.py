@@ -112,6 +112,27 @@ def test_cell_sinkhorn_stopping_rule():
 
 # ---------------------------------------------------------------- partitions
 
+
+def test_cell_sinkhorn_mass_defect():
+    """Reading R6': when truncation (R9) leaves ||nu_J|| != mu(X_J), the plan
+    after a Y-update has mass ||nu_J|| and the best attainable X-marginal is
+    mu ||nu_J|| / mu(X_J).  The rescaled problem has the same minimiser up to
+    that factor (the entropic plan of (mu, r nu) is r times the plan of
+    (mu, nu) in the mu (x) nu_J reference), so: the solve still meets the
+    tolerance, and its plan is exactly r times the balanced plan."""
+    rng = np.random.default_rng(5)
+    kx = np.array([(i, j) for i in range(4) for j in range(4)])
+    mu = rng.uniform(0.5, 1.5, len(kx))
+    ly = np.array([(i, j) for i in range(-1, 5) for j in range(-2, 5)])
+    nu = rng.uniform(0.5, 1.5, len(ly))
+    nu *= mu.sum() / nu.sum()
+    r = 1.0 + 3e-4                       # defect above Err: unreachable without R6'
+    _, _, p1, it1, _, e1 = O.cell_sinkhorn(mu, kx, nu, ly, 4.0, np.zeros(len(kx)), 1e-10)
+    _, _, p2, it2, _, e2 = O.cell_sinkhorn(mu, kx, r * nu, ly, 4.0, np.zeros(len(kx)), 1e-10)
+    assert it2 < 2000 and e2 <= 1e-10 * mu.sum()
+    assert np.allclose(p2, r * p1, rtol=1e-8, atol=0)
+    assert np.allclose(p2.sum(axis=1), r * mu, rtol=1e-9)
+
 @pytest.mark.parametrize("n", [2, 4, 8, 16])
 def test_partitions(n):
     """Def. partitions, Fig. PAPER.md:250: A and B each

@@ -44,7 +44,8 @@ for c in range(a.cycles):
         tf = time.time() - t1
     cost = float(dd.export_plan_cost().sum()) * p.h * p.h if c % 5 == 0 else float("nan")
     print(f"c{c:4d} t={2 * (c + 1) / p.n:6.3f} e0A={sa['l1x_entry']:.3e} e0B={sb['l1x_entry']:.3e} "
-          f"it={(sa['iters_total'] + sb['iters_total']) / (sa['cells'] + sb['cells']):5.1f} cost={cost:.6f} "
+          f"it={(sa['iters_total'] + sb['iters_total']) / (sa['cells'] + sb['cells']):5.1f} "
+          f"nc={sa['nonconverged'] + sb['nonconverged']} itmax={max(sa['iters_max'], sb['iters_max'])} cost={cost:.6f} "
           + (f"flow obj={fs['objective']} stat={fs['stationary']} cert={fs['certificate']} moved={fs['changed_cells']} "
              f"rounds={fs['rounds']} {tf:.2f}s" if fs else ""), flush=True)
     if c % 10 == 0 or c == a.cycles - 1:
