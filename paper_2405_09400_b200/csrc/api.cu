@@ -454,7 +454,6 @@ dd_status domdec_sweep(dd_ctx* c, dd_partition part, dd_sweep_stats* stats) {
   p.tol = (float)c->opt.err;
   p.max_iter = c->opt.max_iter;
   p.fixed_iter = c->opt.fixed_iter;
-  p.debug = getenv("DD_DEBUG_OVF") ? 1 : 0;
   p.tau = c->opt.trunc;
   p.stats = c->d_stats[b];
   p.totals = c->d_totals[b];

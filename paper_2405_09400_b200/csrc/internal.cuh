@@ -68,7 +68,6 @@ struct SweepParams {
   float tol;                          // Err
   int max_iter;
   int fixed_iter;
-  int debug;            // DD_DEBUG_OVF: device printf of cells left unchanged (development aid)
   double tau;
   CellStats* __restrict__ stats;
   SweepTotals* __restrict__ totals;

@@ -173,7 +173,7 @@ __host__ __device__ inline SolveLayout solve_layout(int ccap, int s) {
   L.BK = take(BB * 8);       // fp64 assembly scratch first, then BK (fp32)
   L.U = take(2 * NX * ccap * 4);
   L.V = take(2 * NX * ccap * 4);
-  L.X = take(5 * NX * NX * 4);
+  L.X = take((5 * NX * NX + 4) * 4);   // + scalars (mass defect rm1)
   L.fred = take(64 * 4);
   L.ints = take(64 * 4);
   // fp64 reduction scratch of the primal epilogue: the U/V stage buffers are
@@ -345,7 +345,15 @@ __device__ void solve_cell(const SweepParams& p, const int J, unsigned char* sme
     nsum += v;
     P1[t] = v > 0.0 ? lg2f((float)v) : kNeg;   // log2 nu_J (zeros -> kNeg, R19)
   }
-  const double nuMass = block_sum1_d(nsum, (double*)(smem + Ls.dred));
+  {
+    // mass defect of the cell problem (truncation ledger, reading R9): after
+    // a Y-update the plan has mass ||nu_J||, so its X-marginal is compared
+    // with mu ||nu_J|| / mu(X_J) (reading R6')
+    const double nuMass = block_sum1_d(nsum, (double*)(smem + Ls.dred));
+    double mX = 0.0;
+    for (int q = 0; q < nmem; ++q) mX += p.m[cc.mem[q]];
+    if (tid == 0) X[5 * NX * NX] = (float)((nuMass - mX) / mX);
+  }
   // ---- X-block data, warm start (R7) and re-gauge ------------------------
   // The X-block is padded to NX x NX (ragged B cells have n = s on an axis);
   // padded pixels carry log2 mu = kNeg, so their terms vanish.
@@ -380,12 +388,6 @@ __device__ void solve_cell(const SweepParams& p, const int J, unsigned char* sme
   double muXJ = 0.0;
   for (int q = 0; q < nmem; ++q) muXJ += p.m[cc.mem[q]];
   const float tolJ = (float)(p.tol * muXJ);
-  // mass defect of the cell problem (truncation ledger, reading R9): after a
-  // Y-update the plan has mass ||nu_J||, so its X-marginal is compared with
-  // mu ||nu_J|| / mu(X_J) (reading R6')
-  const float rm1 = (float)((nuMass - muXJ) / muXJ);
-  if (p.debug && tid == 0 && fabsf(rm1) > 1e-9f)
-    printf("DD_DEBUG_RM1 cell %d mode %d nuMass %.17g muXJ %.17g rm1 %g\n", J, p.mode, nuMass, muXJ, (double)rm1);
   __syncthreads();
 
   // ---- a2: separable log-domain Sinkhorn ---------------------------------
@@ -410,7 +412,7 @@ __device__ void solve_cell(const SweepParams& p, const int J, unsigned char* sme
   // Y2 mapping: thread -> (column l2, row group rg of RG)
   // (a hull wider than the CTA, huge class only: columns in chunks of T)
   const int RG = max(1, T / b2);
-  const int y2_col = b2 <= T ? tid % b2 : tid, y2_rg = b2 <= T ? tid / b2 : 0;
+  const int y2_col = tid % b2, y2_rg = tid / b2;
   // X2 mapping: thread -> (pair qa in [0, HX), column k2, split h of SX)
   constexpr int SX = (kSweepThreads / (HX * NX)) > 8 ? 8 : (kSweepThreads / (HX * NX));
   const int x2_h = tid % SX, x2_pair = tid / SX;
@@ -449,12 +451,12 @@ __device__ void solve_cell(const SweepParams& p, const int J, unsigned char* sme
     }
     __syncthreads();
     // Y-half stage 2: B(l1, l2) = -LSE_k1 [U(k1, l2) - w (k1 - l1~)^2]
-    for (int l2 = y2_col; y2_rg < RG && l2 < b2; l2 += T) {
+    auto y2_column = [&](const int l2, const int l1_0, const int l1_step) {
       float u[NX];
 #pragma unroll
       for (int q = 0; q < NX; ++q) u[q] = UK[q * b2 + l2];
       const float wl2 = w * (float)(l2 * l2);
-      for (int l1 = y2_rg; l1 < b1; l1 += RG) {
+      for (int l1 = l1_0; l1 < b1; l1 += l1_step) {
         const int o = l1 * b2 + l2;
         const float x = (float)l1 - fo1;
         float c;
@@ -478,6 +480,11 @@ __device__ void solve_cell(const SweepParams& p, const int J, unsigned char* sme
         P0[o] = Bv;
         BK[o] = Bv + P1[o] - wl2;
       }
+    };
+    if (b2 <= T) {
+      if (y2_rg < RG) y2_column(y2_col, y2_rg, RG);
+    } else {   // hull wider than the CTA (huge class only)
+      for (int l2 = tid; l2 < b2; l2 += T) y2_column(l2, 0, 1);
     }
     __syncthreads();
     // X-half stage 1: V(l1, k2) = LSE_l2 [B + log2 nu_J - w (k2 - l2~)^2],
@@ -625,34 +632,13 @@ __device__ void solve_cell(const SweepParams& p, const int J, unsigned char* sme
         A2n[oa] = ana;
         A2n[ob] = anb;
         // L1 X-marginal error of the plan (A, B): sum mu |1 - 2^(A - A')|
+        const float rm1 = X[5 * NXX];   // (A2/A2n swap; X itself is fixed)
         epart += MU[oa] * fabsf(exp2m1f(A2[oa] - ana) - rm1) + MU[ob] * fabsf(exp2m1f(A2[ob] - anb) - rm1);
         AL[oa] = ana + LM[oa] - wk2;   // AK of the next pass
         AL[ob] = anb + LM[ob] - wk2;
       }
     }
     const float etot = block_sum_f(epart, fred, it);
-    if (p.debug && p.mode == 2 && (b1 > 120 || b2 > 120) && (it <= 3 || it == 50) && tid == 0) {   // DD_DEBUG_OVF: stage ranges of huge cells
-      auto rng = [](const float* v, int n, const char* nm, int J, int it) {
-        float lo = 3e38f, hi = -3e38f;
-        int bad = 0, neg = 0;
-        for (int k = 0; k < n; ++k) {
-          const float x = v[k];
-          if (!(x == x) || fabsf(x) > 1e38f) { ++bad; continue; }
-          if (x <= -1e29f) { ++neg; continue; }
-          lo = fminf(lo, x);
-          hi = fmaxf(hi, x);
-        }
-        printf("DD_DEBUG_OVF J %d it %d %s n %d nonfinite %d kneg %d range [%g, %g]\n", J, it, nm, n, bad, neg, lo, hi);
-      };
-      rng(Ub, NX * b2, "U", J, it);
-      rng(P0, b1 * b2, "B", J, it);
-      rng(P1, b1 * b2, "log2nuJ", J, it);
-      rng(Vb, b1 * NX, "V", J, it);
-      rng(A2, NX * NX, "A", J, it);
-      rng(A2n, NX * NX, "A'", J, it);
-      rng(AL, NX * NX, "AL", J, it);
-      printf("DD_DEBUG_OVF J %d it %d etot %g first %d\n", J, it, etot, (int)first);
-    }
     if (it == 1) e0 = etot;
     e = etot;
     const bool stop = p.fixed_iter > 0 ? (it >= p.fixed_iter) : (etot <= tolJ || it >= p.max_iter);
@@ -688,12 +674,7 @@ __device__ void solve_cell(const SweepParams& p, const int J, unsigned char* sme
     atomicAdd(&p.cum->mufu, mufu);
     atomicAdd(&p.cum->iters, (unsigned long long)it);
     atomicAdd(&p.totals->iters, (unsigned long long)it);
-    if (p.fixed_iter <= 0 && it >= p.max_iter && e > tolJ) {
-      atomicAdd(&p.totals->nonconv, 1ull);
-      if (p.debug)
-        printf("DD_DEBUG_NC cell %d mode %d hull %dx%d n %dx%d e0/tol %g e/tol %g muXJ %g\n", J, p.mode, b1, b2, n1,
-               n2, (double)(e0 / tolJ), (double)(e / tolJ), (double)tolJ / p.tol);
-    }
+    if (p.fixed_iter <= 0 && it >= p.max_iter && e > tolJ) atomicAdd(&p.totals->nonconv, 1ull);
     atomicMax(&p.totals->iters_max, it);
     atomicAdd(&p.totals->e0, (double)e0);
     atomicAdd(&p.totals->e, (double)e);
@@ -816,16 +797,6 @@ __device__ void split_cell(const SweepParams& p, const int J, unsigned char* sme
         p.ext_out[2 * i + 1] = ints[12 + k];
       }
       at += len;
-    }
-    if (tid == 0 && p.debug) {
-      printf("DD_DEBUG_OVF cell %d reason %d mode %d hull (%d,%d)+(%d,%d) nmem %d iters %d e0 %g e %g\n", J, reason,
-             p.mode, L1, L2, b1, b2, nmem, p.stats[J].iters, (double)p.stats[J].e0, (double)p.stats[J].e);
-      for (int k = 0; k < nmem; ++k) {
-        const int i = cc.mem[k];
-        printf("DD_DEBUG_OVF   member %d box (%d,%d)+(%d,%d) new min/max (%d..%d, %d..%d)\n", i, ints[k], ints[4 + k],
-               ints[8 + k], ints[12 + k], ints[16 + 4 * k], ints[16 + 4 * k + 1], ints[16 + 4 * k + 2],
-               ints[16 + 4 * k + 3]);
-      }
     }
     if (tid == 0) {
       p.stats[J].overflow = reason;
