@@ -74,9 +74,10 @@ def lib():
     """Load libdomdec.so (built in-tree by __graft_entry__.build())."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise ImportError(f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
-        L = C.CDLL(LIB_PATH)
+        path = os.environ.get("DD_LIB_PATH", LIB_PATH)   # development A/B builds
+        if not os.path.exists(path):
+            raise ImportError(f"{path} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(path)
         vp = C.c_void_p
         L.domdec_init.argtypes = [C.POINTER(_Problem), C.POINTER(_Options), C.POINTER(vp)]
         L.domdec_sweep.argtypes = [vp, C.c_int, C.POINTER(SweepStats)]
