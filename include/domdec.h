@@ -141,7 +141,13 @@ dd_status domdec_init(const dd_problem *problem, const dd_options *options, dd_c
 
 /* One DomDecIter on partition A or B (Alg. 1 / Alg. 4).  Warm start: the X
  * potential of the previous sweep on the same partition (zero on the first,
- * reading R7).  stats may be NULL (asynchronous). */
+ * reading R7).  Per-cell stopping rule (readings R6/R6'):
+ * sum_x mu |r - 2^(A - A')| <= err mu(X_J) after the Y-update, with
+ * r = ||nu_J|| / mu(X_J) (1 unless truncation removed mass).  Cells that hit
+ * max_iter are counted in stats->nonconverged, not an error.  Cells that
+ * cannot be written (pool exhausted, annihilated box) keep their previous
+ * marginals and make a stats call return DD_ERR_NUMERIC.  stats may be NULL
+ * (asynchronous). */
 dd_status domdec_sweep(dd_ctx *ctx, dd_partition part, dd_sweep_stats *stats);
 
 /* One flow update (Def. flow-update) using the plan costs of
@@ -149,7 +155,11 @@ dd_status domdec_sweep(dd_ctx *ctx, dd_partition part, dd_sweep_stats *stats);
  * (C_ij = rint(c_bar_ij[px^2] * 1024), q_i = rint(m_i 2^E)), negative-cycle
  * certificate, exact min-cost flow (GPU cost scaling) if needed, apply flow
  * iff the optimal objective is < 0.  Requires a previous sweep
- * (DD_ERR_PRECOND otherwise).  stats may be NULL (asynchronous). */
+ * (DD_ERR_PRECOND otherwise).  The context keeps the last optimal flow and
+ * its prices on the device and starts the next solve from them (the supplies
+ * q are static, so that flow stays feasible); the result is still an exactly
+ * optimal flow, possibly a different one of several optima.
+ * stats may be NULL (asynchronous). */
 dd_status flow_update(dd_ctx *ctx, dd_flow_stats *stats);
 
 /* L1 marginal errors (Table rows), fp64:
