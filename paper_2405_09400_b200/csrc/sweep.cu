@@ -160,14 +160,16 @@ __device__ __forceinline__ float block_sum_f(float v, float* scratch, int parity
 
 // ---------------------------------------------------------------------------
 // Shared-memory layouts.  BB = ccap^2 box entries, NX = 2 s.
+// Byte offsets are 32-bit (the global-scratch class at ccap 1024 needs ~10 MB):
+// cheaper to rematerialise than 64-bit offsets in the register-bound loops.
 struct SolveLayout {
-  size_t B, LN, BK, U, V, X, fred, ints, dred, total;   // X: A2, A2n, LM, MU, AL
+  unsigned B, LN, BK, U, V, X, fred, ints, dred, total;   // X: A2, A2n, LM, MU, AL
 };
 __host__ __device__ inline SolveLayout solve_layout(int ccap, int s) {
   SolveLayout L;
-  const size_t BB = (size_t)ccap * ccap, NX = 2 * (size_t)s;
-  size_t o = 0;
-  auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 15) & ~size_t(15); return r; };
+  const unsigned BB = (unsigned)ccap * (unsigned)ccap, NX = 2u * (unsigned)s;
+  unsigned o = 0;
+  auto take = [&](unsigned bytes) { unsigned r = o; o += (bytes + 15u) & ~15u; return r; };
   L.B = take(BB * 4);
   L.LN = take(BB * 4);
   L.BK = take(BB * 8);       // fp64 assembly scratch first, then BK (fp32)
@@ -183,13 +185,13 @@ __host__ __device__ inline SolveLayout solve_layout(int ccap, int s) {
   return L;
 }
 struct SplitLayout {
-  size_t nuJ, red, P0, P1, P2, P3, U, R, AL, ints, total;
+  unsigned nuJ, red, P0, P1, P2, P3, U, R, AL, ints, total;
 };
 __host__ __device__ inline SplitLayout split_layout(int ccap, int s) {
   SplitLayout L;
-  const size_t BB = (size_t)ccap * ccap, NX = 2 * (size_t)s;
-  size_t o = 0;
-  auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 15) & ~size_t(15); return r; };
+  const unsigned BB = (unsigned)ccap * (unsigned)ccap, NX = 2u * (unsigned)s;
+  unsigned o = 0;
+  auto take = [&](unsigned bytes) { unsigned r = o; o += (bytes + 15u) & ~15u; return r; };
   L.nuJ = take(BB * 8);
   L.red = take(288 * 8);
   L.P0 = take(BB * 4);

@@ -469,3 +469,27 @@ def test_time_to_convergence_cycle_matches_oracle():
     _lockstep_hybrid(p, 200, record, err=1e-4)
     assert "o" in first and "g" in first, first
     assert abs(first["o"] - first["g"]) <= 1, (first["o"], first["g"])
+
+
+@gpu
+def test_long_hybrid_trajectory_is_healthy():
+    """Regression guard for long runs (the bugs of round 1 showed up only
+    after tens of hybrid cycles): 120 cycles of Alg. 3 in tolerance mode on a
+    256^2 problem - no cell left unchanged, no cell at the iteration cap, the
+    sweep-entry error decreasing overall, the Y-marginal exact up to the
+    truncation ledger (R9) and the X-marginal error at the stopping level."""
+    p = make_problem("gm", 256, 4, eps_factor=2.0, theta_deg=20, seed=3)
+    dd = gpu_ctx(p)
+    first = last = None
+    for cyc in range(120):
+        for part in ("A", "B"):
+            st = dd.sweep(part, stats=True)
+            assert st["overflow"] == 0 and st["nonconverged"] == 0, (cyc, part, st)
+            assert np.isfinite(st["l1x_entry"]) and np.isfinite(st["l1x_final"]), (cyc, part, st)
+        dd.flow_update()
+        first = st["l1x_entry"] if first is None else first
+        last = st["l1x_entry"]
+    assert last < 0.1 * first, (first, last)
+    ex, ey = dd.marginal_error()
+    assert ex < 2e-4 and ey < 1e-6, (ex, ey)
+    dd.close()
