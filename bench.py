@@ -391,6 +391,10 @@ def run_ours(a):
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "time_to_l1_1e-4": ttc,
+            # sweeps/s with A and B separately, flow-update time, cycles/s
+            "per_partition": {"sweep_ms_A": float(np.mean(sweep_ms[0::2])), "sweep_ms_B": float(np.mean(sweep_ms[1::2])),
+                              "flow_ms": (sum(step_ms) - sum(sweep_ms)) / a.steps,
+                              "cycles_per_s": a.steps * world / total_s},
             "state": {"l1_x": ex, "l1_y": ey, "iters_per_cell": cnt["iters"] / max(1, cnt["cells"]),
                       "flow_ms_per_step": (sum(step_ms) - sum(sweep_ms)) / a.steps},
             "step_breakdown": {
