@@ -304,7 +304,11 @@ __device__ __forceinline__ void primal_terms(const SweepParams& p, const CompCel
 
 // ===========================================================================
 // solve_kernel: a1 (log2 nu_J) + a2 (Sinkhorn), one CTA per composite cell.
-template <int NX, bool PR>
+// GS: the cell's work arrays live in global scratch (huge size class); a
+// separate instantiation so that the shared-memory classes see a pointer
+// derived from the __shared__ array and compile to LDS/STS with 32-bit
+// addresses instead of generic 64-bit loads.
+template <int NX, bool PR, bool GS>
 __device__ void solve_cell(const SweepParams& p, const int J, unsigned char* smem) {
   const int tid = threadIdx.x, T = blockDim.x;
   const SolveLayout Ls = solve_layout(p.ccap, p.s);
@@ -426,6 +430,7 @@ __device__ void solve_cell(const SweepParams& p, const int J, unsigned char* sme
     for (int o = tid, k1 = tid / b2, l2 = tid % b2; o < NX * b2;
          o += T, k1 += T / b2, l2 += T % b2, (l2 >= b2 ? (l2 -= b2, ++k1) : 0)) {
       const float x = (float)l2 - fo2;
+      const float wx = w2 * x;   // term q: fma(q, w2 x, a_q) (immediate q, no per-q constants live)
       const float* ar = AL + k1 * NX;
       float a[NX];
 #pragma unroll
@@ -434,18 +439,18 @@ __device__ void solve_cell(const SweepParams& p, const int J, unsigned char* sme
       if (first) {
         c = kNeg;
 #pragma unroll
-        for (int q = 0; q < NX; ++q) c = fmaxf(c, fmaf(w2 * (float)q, x, a[q]));
+        for (int q = 0; q < NX; ++q) c = fmaxf(c, fmaf((float)q, wx, a[q]));
       } else {
         c = Ub[o] + w * x * x;
       }
       float sum = 0.f;
 #pragma unroll
-      for (int q = 0; q < NX; ++q) sum += ex2f(fmaf(w2 * (float)q, x, a[q]) - c);
+      for (int q = 0; q < NX; ++q) sum += ex2f(fmaf((float)q, wx, a[q]) - c);
       if (!(sum > 0x1p-60f && sum < 0x1p60f)) {
         c = kNeg;
-        for (int q = 0; q < NX; ++q) c = fmaxf(c, fmaf(w2 * (float)q, x, a[q]));
+        for (int q = 0; q < NX; ++q) c = fmaxf(c, fmaf((float)q, wx, a[q]));
         sum = 0.f;
-        for (int q = 0; q < NX; ++q) sum += ex2f(fmaf(w2 * (float)q, x, a[q]) - c);
+        for (int q = 0; q < NX; ++q) sum += ex2f(fmaf((float)q, wx, a[q]) - c);
       }
       const float U = c + lg2f(sum) - w * x * x;
       Ub[o] = U;
@@ -461,22 +466,23 @@ __device__ void solve_cell(const SweepParams& p, const int J, unsigned char* sme
       for (int l1 = l1_0; l1 < b1; l1 += l1_step) {
         const int o = l1 * b2 + l2;
         const float x = (float)l1 - fo1;
+        const float wx = w2 * x;
         float c;
         if (first) {
           c = kNeg;
 #pragma unroll
-          for (int q = 0; q < NX; ++q) c = fmaxf(c, fmaf(w2 * (float)q, x, u[q]));
+          for (int q = 0; q < NX; ++q) c = fmaxf(c, fmaf((float)q, wx, u[q]));
         } else {
           c = -P0[o] + w * x * x;
         }
         float sum = 0.f;
 #pragma unroll
-        for (int q = 0; q < NX; ++q) sum += ex2f(fmaf(w2 * (float)q, x, u[q]) - c);
+        for (int q = 0; q < NX; ++q) sum += ex2f(fmaf((float)q, wx, u[q]) - c);
         if (!(sum > 0x1p-60f && sum < 0x1p60f)) {
           c = kNeg;
-          for (int q = 0; q < NX; ++q) c = fmaxf(c, fmaf(w2 * (float)q, x, u[q]));
+          for (int q = 0; q < NX; ++q) c = fmaxf(c, fmaf((float)q, wx, u[q]));
           sum = 0.f;
-          for (int q = 0; q < NX; ++q) sum += ex2f(fmaf(w2 * (float)q, x, u[q]) - c);
+          for (int q = 0; q < NX; ++q) sum += ex2f(fmaf((float)q, wx, u[q]) - c);
         }
         const float Bv = -(c + lg2f(sum) - w * x * x);
         P0[o] = Bv;
@@ -688,12 +694,20 @@ __global__ void __launch_bounds__(kSweepThreads, DD_SOLVE_MINB) solve_kernel(Swe
   extern __shared__ __align__(16) unsigned char smem[];
   // one call site, so the cell routine is inlined (two call sites made the
   // compiler emit it as a real call: ABI stack frame and spills, 3% slower)
+  // (each instantiation has one call site, so it is inlined)
   const int n = p.mode == 0 ? p.ncells : (p.mode == 1 ? *p.ovf_count : *p.ovf2_count);
   const int* list = p.mode == 1 ? p.ovf_list : p.ovf2_list;
-  unsigned char* base = p.mode == 2 ? p.scratch + (size_t)blockIdx.x * p.scratch_stride : smem;
-  for (int k = blockIdx.x; k < n; k += gridDim.x) {
-    solve_cell<NX, PR>(p, p.mode == 0 ? k : list[k], base);
-    __syncthreads();
+  if (p.mode == 2) {
+    unsigned char* base = p.scratch + (size_t)blockIdx.x * p.scratch_stride;
+    for (int k = blockIdx.x; k < n; k += gridDim.x) {
+      solve_cell<NX, PR, true>(p, list[k], base);
+      __syncthreads();
+    }
+  } else {
+    for (int k = blockIdx.x; k < n; k += gridDim.x) {
+      solve_cell<NX, PR, false>(p, p.mode == 0 ? k : list[k], smem);
+      __syncthreads();
+    }
   }
 }
 
@@ -749,7 +763,7 @@ __device__ __forceinline__ int pair_id(int a, int b) {   // a < b, 4 members -> 
   return a == 0 ? b - 1 : (a == 1 ? b + 1 : 5);
 }
 
-template <int NX>
+template <int NX, bool GS>
 __device__ void split_cell(const SweepParams& p, const int J, unsigned char* smem) {
   const int tid = threadIdx.x, T = blockDim.x;
   const SplitLayout Ls = split_layout(p.ccap, p.s);
@@ -1164,12 +1178,20 @@ __global__ void __launch_bounds__(kSweepThreads, DD_SPLIT_MINB) split_kernel(Swe
   extern __shared__ __align__(16) unsigned char smem[];
   // one call site, so the cell routine is inlined (two call sites made the
   // compiler emit it as a real call: ABI stack frame and spills, 3% slower)
+  // (each instantiation has one call site, so it is inlined)
   const int n = p.mode == 0 ? p.ncells : (p.mode == 1 ? *p.ovf_count : *p.ovf2_count);
   const int* list = p.mode == 1 ? p.ovf_list : p.ovf2_list;
-  unsigned char* base = p.mode == 2 ? p.scratch + (size_t)blockIdx.x * p.scratch_stride : smem;
-  for (int k = blockIdx.x; k < n; k += gridDim.x) {
-    split_cell<NX>(p, p.mode == 0 ? k : list[k], base);
-    __syncthreads();
+  if (p.mode == 2) {
+    unsigned char* base = p.scratch + (size_t)blockIdx.x * p.scratch_stride;
+    for (int k = blockIdx.x; k < n; k += gridDim.x) {
+      split_cell<NX, true>(p, list[k], base);
+      __syncthreads();
+    }
+  } else {
+    for (int k = blockIdx.x; k < n; k += gridDim.x) {
+      split_cell<NX, false>(p, p.mode == 0 ? k : list[k], smem);
+      __syncthreads();
+    }
   }
 }
 
