@@ -724,9 +724,10 @@ __global__ void __launch_bounds__(kSweepThreads, DD_SOLVE_MINB) solve_kernel(Swe
 __device__ __forceinline__ void member_values(double nuj, const float (&p)[4], int nmem, const double* bc,
                                               double (&out)[4]) {
   int am = 0;
+  float pbest = p[0];   // running maximum: no dynamic index (keeps p in registers)
 #pragma unroll
   for (int k = 1; k < 4; ++k)
-    if (k < nmem && p[k] > p[am]) am = k;
+    if (k < nmem && p[k] > pbest) { am = k; pbest = p[k]; }
   double parts[4];
   double rest = 0.0;
 #pragma unroll
@@ -934,9 +935,10 @@ __device__ void split_cell(const SweepParams& p, const int J, unsigned char* sme
       // identity split (the largest share takes the remainder: exact sum)
       double v[4];
       int am = 0;
+      float pbest = pk[0];
 #pragma unroll
       for (int q = 1; q < 4; ++q)
-        if (q < nmem && pk[q] > pk[am]) am = q;
+        if (q < nmem && pk[q] > pbest) { am = q; pbest = pk[q]; }
       double rest = 0.0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -1058,20 +1060,40 @@ __device__ void split_cell(const SweepParams& p, const int J, unsigned char* sme
   __syncthreads();
   double drop[1] = {0.0};
   double dloc = 0.0;
+  // per-thread bounds in registers (static member indices), one warp
+  // reduction and one shared atomic per warp and bound at the end
+  int bmn1[4], bmx1[4], bmn2[4], bmx2[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) { bmn1[k] = 1 << 30; bmx1[k] = -1; bmn2[k] = 1 << 30; bmx2[k] = -1; }
   for (int o = tid; o < BB; o += T) {
     const int l1 = o / b2, l2 = o - l1 * b2;
     const float pk[4] = {P0[o], P1[o], P2[o], P3[o]};
     double v[4];
     member_values(nuJ[o], pk, nmem, bc, v);
-    for (int k = 0; k < nmem; ++k) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k >= nmem) continue;
       if (v[k] >= p.tau) {
-        atomicMin(&ints[16 + 4 * k + 0], l1);
-        atomicMax(&ints[16 + 4 * k + 1], l1);
-        atomicMin(&ints[16 + 4 * k + 2], l2);
-        atomicMax(&ints[16 + 4 * k + 3], l2);
+        bmn1[k] = min(bmn1[k], l1);
+        bmx1[k] = max(bmx1[k], l1);
+        bmn2[k] = min(bmn2[k], l2);
+        bmx2[k] = max(bmx2[k], l2);
       } else if (v[k] > 0.0) {
         dloc += v[k];
       }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int a = __reduce_min_sync(0xffffffffu, bmn1[k]);
+    const int b = __reduce_max_sync(0xffffffffu, bmx1[k]);
+    const int c = __reduce_min_sync(0xffffffffu, bmn2[k]);
+    const int d = __reduce_max_sync(0xffffffffu, bmx2[k]);
+    if ((tid & 31) == 0 && k < nmem && b >= 0) {
+      atomicMin(&ints[16 + 4 * k + 0], a);
+      atomicMax(&ints[16 + 4 * k + 1], b);
+      atomicMin(&ints[16 + 4 * k + 2], c);
+      atomicMax(&ints[16 + 4 * k + 3], d);
     }
   }
   drop[0] = block_sum1_d(dloc, red);
@@ -1105,7 +1127,9 @@ __device__ void split_cell(const SweepParams& p, const int J, unsigned char* sme
   long long* pbase = (long long*)(ints + 48);
   if (tid == 0) {
     long long tot = 0;
-    for (int q = 0; q < nmem; ++q) tot += (long long)(bx[q][1] - bx[q][0] + 1) * (bx[q][3] - bx[q][2] + 1);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)   // static indices keep bx / mbase in registers
+      if (q < nmem) tot += (long long)(bx[q][1] - bx[q][0] + 1) * (bx[q][3] - bx[q][2] + 1);
     long long b0 = (long long)atomicAdd(p.pool_ctr, (unsigned long long)tot);
     if (b0 + tot > p.pool_cap) { b0 = -1; atomicAdd(&p.totals->overflow, 1ull); }
     pbase[0] = b0;
@@ -1138,13 +1162,16 @@ __device__ void split_cell(const SweepParams& p, const int J, unsigned char* sme
       }
     }
   }
-  if (tid < nmem) {
-    const int q = tid, i = cc.mem[q];
-    p.pos_out[i] = mbase[q];
-    p.off_out[2 * i] = L1 + bx[q][0];
-    p.off_out[2 * i + 1] = L2 + bx[q][2];
-    p.ext_out[2 * i] = bx[q][1] - bx[q][0] + 1;
-    p.ext_out[2 * i + 1] = bx[q][3] - bx[q][2] + 1;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (tid == q && q < nmem) {
+      const int i = cc.mem[q];
+      p.pos_out[i] = mbase[q];
+      p.off_out[2 * i] = L1 + bx[q][0];
+      p.off_out[2 * i + 1] = L2 + bx[q][2];
+      p.ext_out[2 * i] = bx[q][1] - bx[q][0] + 1;
+      p.ext_out[2 * i + 1] = bx[q][3] - bx[q][2] + 1;
+    }
   }
   if (tid == 0) {
     for (int q = 0; q < nmem; ++q)
