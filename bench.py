@@ -134,6 +134,15 @@ def cpu_baseline(p, seconds):
                       f"(fp64 dense log-domain Sinkhorn, Err=1e-4), {dt:.1f} s, extrapolated to one sweep"}
 
 
+def bench_config(a, world):
+    """The workload both arms report (the reference arm adds its sample)."""
+    return {"workload": f"GM(rank) {a.N}x{a.N} -> {a.N}x{a.N}, s={a.s}, eps=(2h)^2, theta=20deg; "
+                        "step = hybrid cycle (sweep A, sweep B, flow update)",
+            "grid": a.N, "cell_size": a.s, "eps": "(2h)^2", "parallelism": f"independent problems x{world}",
+            "l2": "flushed between timed steps (256 MB write)",
+            "precision": "log-domain fp32 (local gauge), marginals fp64"}
+
+
 def run_reference(a):
     world, rank, local = dist_env()
     if rank != 0:
@@ -151,8 +160,8 @@ def run_reference(a):
     out = {"metric": METRIC, "value": v, "unit": "sweeps/s", "n_gpus": a.gpus, "steps": a.steps,
            "warmup": a.warmup, "ms_per_step": dt * 1e3 / a.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"GM(0) {a.N}x{a.N}, s={a.s}, eps=(2h)^2, theta=20deg, hybrid A/B/flow",
-                      "sample": vals[-1]["sample"]},
+           "config": dict(bench_config(a, a.gpus), sample=vals[-1]["sample"],
+                                precision="fp64 oracle (log-domain Sinkhorn)"),
            "impl": "reference",
            "cpu_baseline": {"value": v, "unit": "sweeps/s", "cores": 1, "kind": "oracle",
                             "sample": vals[-1]["sample"]},
@@ -360,11 +369,7 @@ def run_ours(a):
             "metric": METRIC, "value": value, "unit": "sweeps/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": total_s * 1e3 / a.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"GM(rank) {a.N}x{a.N} -> {a.N}x{a.N}, s={a.s}, eps=(2h)^2, theta=20deg; "
-                                   "step = hybrid cycle (sweep A, sweep B, flow update)",
-                       "grid": a.N, "cell_size": a.s, "eps": "(2h)^2", "parallelism": f"independent problems x{world}",
-                       "l2": "flushed between timed steps (256 MB write)",
-                       "precision": "log-domain fp32 (local gauge), marginals fp64"},
+            "config": bench_config(a, world),
             "e2e": {"value": 2 * e2e_steps * world / e2e_s, "unit": "sweeps/s",
                     "h2d_bytes_per_step": int(h2d / e2e_steps), "d2h_bytes_per_step": int(16 / e2e_steps),
                     "steps": e2e_steps,
