@@ -381,9 +381,9 @@ def run_ours(a):
                          "unit": "TOP/s (MUFU ex2+lg2)", "frac": achieved / peak_nominal,
                          # dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full
                          # capture of each sweep kernel (profiles/r01_ncu_summary.txt: solve
-                         # 199.3 + 6.3 MB, split 195.9 + 167.4 MB, small size class, one sweep)
-                         "traffic": 5.69e8, "traffic_unit": "bytes per sweep (solve + split launch)",
-                         "traffic_vs_algorithmic": 5.69e8 / max(1.0, cnt["bytes"] / max(1, cnt["sweeps"])),
+                         # 199.3 + 9.3 MB, split 195.3 + 154.8 MB, small size class, one sweep)
+                         "traffic": 5.59e8, "traffic_unit": "bytes per sweep (solve + split launch)",
+                         "traffic_vs_algorithmic": 5.59e8 / max(1.0, cnt["bytes"] / max(1, cnt["sweeps"])),
                          "kernel": "sweep = solve_kernel + split_kernel (a1-a6)",
                          "peak_source": f"148 SM x 16 MUFU/clk x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
                          "measured_mufu_peak": measured_mufu / 1e12,
