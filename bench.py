@@ -358,6 +358,18 @@ def run_ours(a):
             dd3.close()
             return res
 
+        sg = None
+        if rank == 0 and not a.no_ttc:
+            # SinkhornGPU comparator: global separable
+            # Sinkhorn on the cfg3 pair (256^2, theta=5), cold start at eps=(2h)^2, to Err=1e-4.
+            from paper_2405_09400_b200 import sinkhorn_global
+            from synth import make_problem as _mp
+            q = _mp("gm", 256, 4, theta_deg=5.0, seed=0)
+            _, _, it_sg, e_sg, ms_sg = sinkhorn_global(q.mu, q.nu, q.eps_prime, err=1e-4, max_iter=20000,
+                                                       check_every=10)
+            sg = {"workload": "GM(0) 256^2 theta=5deg, eps=(2h)^2, cold start, Err=1e-4 (PAPER.md:1264)",
+                  "seconds": ms_sg / 1e3, "iterations": it_sg, "l1_x": e_sg, "ms_per_iteration": ms_sg / it_sg,
+                  "note": "device time (CUDA events), host copies excluded; fp64 potentials"}
         ttc = None
         if not a.no_ttc:
             ttc = {"cfg3_256": ttc_run(256, 4, 5.0, a.ttc_seconds, a.ttc_cycles),
@@ -396,6 +408,7 @@ def run_ours(a):
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "time_to_l1_1e-4": ttc,
+            "sinkhorn_global_cfg3": sg,
             # sweeps/s with A and B separately, flow-update time, cycles/s
             "per_partition": {"sweep_ms_A": float(np.mean(sweep_ms[0::2])), "sweep_ms_B": float(np.mean(sweep_ms[1::2])),
                               "flow_ms": (sum(step_ms) - sum(sweep_ms)) / a.steps,

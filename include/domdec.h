@@ -215,6 +215,31 @@ dd_status dd_mincost_flow(int32_t n1, int32_t n2, const int64_t *q, const int64_
                           int64_t *w, int64_t *objective, dd_flow_stats *stats,
                           int32_t device, void *stream);
 
+/* Global separable log-domain Sinkhorn on the whole N1 x N2 grid, no domain
+ * decomposition: the SinkhornGPU comparator of the paper's benchmark
+ * (Table).
+ * Potentials in units of eps: a = alpha/eps on X, b = beta/eps on Y; cost in
+ * pixel units, eps_p = eps/h^2 (eps' of SURVEY 8).  Iterates the Y-update
+ * b(l) = -LSE_k[a(k) + log mu(k) - |k-l|^2/eps_p] and the X-update
+ * a(k) = -LSE_l[b(l) + log nu(l) - |k-l|^2/eps_p] (Eq. entropic-transport
+ * PAPER.md:196-202, separable stages PAPER.md:1145) until the L1 X-marginal
+ * error after the Y-update, sum_k mu(k)|1 - exp(a(k) - a'(k))|, is
+ * <= err * ||mu||, checked every check_every iterations, or
+ * max_iter iterations ran (err = 0 with check_every = max_iter: exactly
+ * max_iter iterations, parity mode).  Then one final Y-update.
+ * mu, nu: host [N1*N2] row-major, >= 0, equal total mass (else
+ * DD_ERR_PRECOND).  alpha: host [N1*N2], in = initial a (zeros for a cold
+ * start), out = final a on supp(mu) (0 elsewhere); beta: host [N1*N2] out,
+ * final b on supp(nu) (0 elsewhere).  iters, l1_x (last checked error),
+ * solve_ms (CUDA-event time of the device iterations, host copies excluded)
+ * may be NULL.  stream may be NULL.  Errors: DD_ERR_ARG (bad sizes/values),
+ * DD_ERR_OOM, DD_ERR_CUDA, DD_ERR_NUMERIC (non-finite error); message via
+ * dd_last_error(NULL).  fp64 potentials and terms, fp32 exp2 of shifted terms. */
+dd_status dd_sinkhorn_global(int32_t N1, int32_t N2, const double *mu, const double *nu, double eps_p,
+                             double err, int32_t max_iter, int32_t check_every, int32_t device,
+                             void *stream, double *alpha, double *beta, int32_t *iters, double *l1_x,
+                             double *solve_ms);
+
 /* Cumulative work counters since domdec_init / domdec_reset_counters (for
  * roofline accounting without per-call synchronisation).  Synchronises. */
 typedef struct {

@@ -93,6 +93,9 @@ def lib():
         L.dd_mincost_flow.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                       C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(FlowStats),
                                       C.c_int32, vp]
+        pd = C.POINTER(C.c_double)
+        L.dd_sinkhorn_global.argtypes = [C.c_int32, C.c_int32, pd, pd, C.c_double, C.c_double, C.c_int32, C.c_int32,
+                                         C.c_int32, vp, pd, pd, C.POINTER(C.c_int32), pd, pd]
         L.domdec_halo_pack.argtypes = [vp, C.c_int32, vp, C.c_int64, C.POINTER(C.c_int64)]
         L.domdec_halo_unpack.argtypes = [vp, C.c_int32, vp, C.c_int64]
         L.domdec_destroy.argtypes = [vp]
@@ -105,7 +108,8 @@ def lib():
         for fn in ("domdec_init", "domdec_sweep", "flow_update", "marginal_error", "primal_dual_gap",
                    "domdec_export_cells", "domdec_export_alpha", "domdec_export_plan_cost",
                    "flow_edge_costs", "flow_apply", "dd_mincost_flow", "domdec_destroy", "domdec_counters",
-                   "domdec_reset_counters", "dd_mufu_peak", "domdec_halo_pack", "domdec_halo_unpack"):
+                   "domdec_reset_counters", "dd_mufu_peak", "domdec_halo_pack", "domdec_halo_unpack",
+                   "dd_sinkhorn_global"):
             getattr(L, fn).restype = C.c_int
         _lib = L
     return _lib
@@ -114,7 +118,8 @@ def lib():
 EXPORTED = ("domdec_init", "domdec_sweep", "flow_update", "marginal_error", "primal_dual_gap",
             "domdec_export_cells", "domdec_export_alpha", "domdec_export_plan_cost", "flow_edge_costs",
             "flow_apply", "dd_mincost_flow", "domdec_destroy", "dd_last_error", "dd_version", "domdec_counters",
-            "domdec_reset_counters", "dd_mufu_peak", "domdec_halo_pack", "domdec_halo_unpack")
+            "domdec_reset_counters", "dd_mufu_peak", "domdec_halo_pack", "domdec_halo_unpack",
+            "dd_sinkhorn_global")
 
 
 def _ptr(a, ctype):
@@ -281,3 +286,21 @@ def mincost_flow(n1, n2, q, Cc, device=0, stream=None):
                                  C.byref(obj), C.byref(st), int(device), C.c_void_p(stream) if stream else None),
            None)
     return w, obj.value, st.as_dict()
+
+
+def sinkhorn_global(mu, nu, eps_p, err=1e-4, max_iter=100000, check_every=1, alpha0=None, device=0, stream=None):
+    """Global separable log-domain Sinkhorn on the GPU (dd_sinkhorn_global,
+    the SinkhornGPU comparator).  mu, nu: (N1, N2) float64.  Returns
+    (a, b, iters, l1_x, solve_ms) with a, b (N1, N2) float64 in units of eps."""
+    mu = np.ascontiguousarray(mu, np.float64)
+    nu = np.ascontiguousarray(nu, np.float64)
+    N1, N2 = mu.shape
+    a = np.zeros((N1, N2)) if alpha0 is None else np.array(alpha0, np.float64, order="C", copy=True)
+    b = np.zeros((N1, N2))
+    it, e, ms = C.c_int32(), C.c_double(), C.c_double()
+    pd = C.c_double
+    _check(lib().dd_sinkhorn_global(int(N1), int(N2), _ptr(mu, pd), _ptr(nu, pd), float(eps_p), float(err),
+                                    int(max_iter), int(check_every), int(device),
+                                    C.c_void_p(stream) if stream else None, _ptr(a, pd), _ptr(b, pd),
+                                    C.byref(it), C.byref(e), C.byref(ms)), None)
+    return a, b, it.value, e.value, ms.value

@@ -5,7 +5,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SOURCES = ["csrc/api.cu", "csrc/sweep.cu", "csrc/flow.cu", "csrc/mcf.cu", "csrc/pdgap.cu"]
+SOURCES = ["csrc/api.cu", "csrc/sweep.cu", "csrc/flow.cu", "csrc/mcf.cu", "csrc/pdgap.cu", "csrc/sinkhorn_global.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
 

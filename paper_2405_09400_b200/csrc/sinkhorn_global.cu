@@ -1,0 +1,211 @@
+// sinkhorn_global.cu — global separable log-domain Sinkhorn on the whole
+// N1 x N2 grid (the SinkhornGPU comparator of the paper's benchmark,
+// PAPER.md:1249-1250, Table).
+//
+// Potentials in units of eps (a = alpha/eps, b = beta/eps), pixel units for
+// the cost, eps' = eps/h^2 (SURVEY 8 symbols):
+//   b(l) = -LSE_k [ a(k) + log mu(k) - |k - l|^2 / eps' ]      (Y-update)
+//   a(k) = -LSE_l [ b(l) + log nu(l) - |k - l|^2 / eps' ]      (X-update)
+// each half split into two 1-D LSE stages along the axes (separable kernel,
+// PAPER.md:1145).  Stop when the L1 X-marginal error after the Y-update,
+// sum_k mu(k) |1 - exp(a(k) - a'(k))| (a' = the next X-update), is
+// <= ||mu|| Err.
+//
+// Precision: the global gauge has exponents of magnitude O(N^2/eps'), which
+// the paper reports as the fp32 stall, so potentials and
+// terms are fp64 here; only exp2 of (term - row max) <= 0 and its sum are
+// fp32.  One CTA per output row of a stage; the input row is staged in shared
+// memory and every thread computes whole output entries.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "ctx.cuh"
+
+namespace dd {
+namespace {
+
+constexpr double kLog2eG = 1.4426950408889634;
+
+// in[i] = w[i] > 0 ? p[i] + log w[i] : -inf
+__global__ void k_sg_prep(const double* __restrict__ p, const double* __restrict__ w, double* __restrict__ in,
+                          long long NN) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < NN; i += (long long)gridDim.x * blockDim.x)
+    in[i] = w[i] > 0.0 ? p[i] + log(w[i]) : -INFINITY;
+}
+
+// out[y * R + x] = LSE_z [ in[x * M + z] - (z - y)^2 * inv_eps ], x < R, y, z < M
+// (transposed so the next stage reads rows).  Max pass then sum pass.
+__global__ void k_sg_stage(const double* __restrict__ in, double* __restrict__ out, int R, int M, double inv_eps) {
+  extern __shared__ double srow[];
+  const int x = blockIdx.x;
+  for (int z = threadIdx.x; z < M; z += blockDim.x) srow[z] = in[(long long)x * M + z];
+  __syncthreads();
+  for (int y = threadIdx.x; y < M; y += blockDim.x) {
+    double m = -INFINITY;
+    for (int z = 0; z < M; ++z) {
+      const double d = (double)(z - y);
+      m = fmax(m, fma(-d * d, inv_eps, srow[z]));
+    }
+    double res = -INFINITY;
+    if (m > -INFINITY) {
+      float sum = 0.f;
+      for (int z = 0; z < M; ++z) {
+        const double d = (double)(z - y);
+        sum += exp2f((float)((fma(-d * d, inv_eps, srow[z]) - m) * kLog2eG));
+      }
+      res = m + log((double)sum);
+    }
+    out[(long long)y * R + x] = res;
+  }
+}
+
+// dst[i] = w[i] > 0 ? -lse[i] : 0   (potential defined on the support only)
+__global__ void k_sg_neg(const double* __restrict__ lse, const double* __restrict__ w, double* __restrict__ dst,
+                         long long NN) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < NN; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = w[i] > 0.0 ? -lse[i] : 0.0;
+}
+
+// per-block partial sums of mu |expm1(a_old - a_new)| (fixed grid, fixed order)
+__global__ void k_sg_err(const double* __restrict__ a_old, const double* __restrict__ a_new,
+                         const double* __restrict__ mu, long long NN, double* __restrict__ part) {
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < NN; i += (long long)gridDim.x * blockDim.x)
+    if (mu[i] > 0.0) s += mu[i] * fabs(expm1(a_old[i] - a_new[i]));
+  __shared__ double sh[32];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void k_sg_err_final(const double* __restrict__ part, int n, double* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < n; ++i) t += part[i];
+    *out = t;
+  }
+}
+
+constexpr int kSgThreads = 256;
+constexpr int kSgErrBlocks = 296;   // 2 x 148 SMs
+
+struct SgBuffers {
+  double *mu = nullptr, *nu = nullptr, *a = nullptr, *a2 = nullptr, *b = nullptr, *in = nullptr, *t = nullptr,
+         *out = nullptr, *part = nullptr, *err = nullptr;
+  ~SgBuffers() {
+    for (double* p : {mu, nu, a, a2, b, in, t, out, part, err})
+      if (p) cudaFree(p);
+  }
+};
+
+// One half-iteration: dst = -LSE over the source grid of (src + log w_src - c/eps'), masked by w_dst.
+void sg_half(const SgBuffers& B, const double* src, const double* wsrc, const double* wdst, double* dst, int N1,
+             int N2, double inv_eps, int grid_ew, cudaStream_t st) {
+  const long long NN = (long long)N1 * N2;
+  k_sg_prep<<<grid_ew, kSgThreads, 0, st>>>(src, wsrc, B.in, NN);
+  k_sg_stage<<<N1, kSgThreads, N2 * sizeof(double), st>>>(B.in, B.t, N1, N2, inv_eps);
+  k_sg_stage<<<N2, kSgThreads, N1 * sizeof(double), st>>>(B.t, B.out, N2, N1, inv_eps);
+  k_sg_neg<<<grid_ew, kSgThreads, 0, st>>>(B.out, wdst, dst, NN);
+}
+
+}  // namespace
+}  // namespace dd
+
+using namespace dd;
+
+extern "C" {
+
+dd_status dd_sinkhorn_global(int32_t N1, int32_t N2, const double* mu, const double* nu, double eps_p, double err,
+                             int32_t max_iter, int32_t check_every, int32_t device, void* stream, double* alpha,
+                             double* beta, int32_t* iters, double* l1_x, double* solve_ms) {
+  if (N1 <= 0 || N2 <= 0 || N1 > 8192 || N2 > 8192 || !mu || !nu || !alpha || !beta || !(eps_p > 0.0) ||
+      max_iter <= 0 || check_every <= 0) {
+    set_global_error("dd_sinkhorn_global: bad argument");
+    return DD_ERR_ARG;
+  }
+  const long long NN = (long long)N1 * N2;
+  double mass_mu = 0.0, mass_nu = 0.0;
+  for (long long i = 0; i < NN; ++i) {
+    if (!(mu[i] >= 0.0) || !(nu[i] >= 0.0)) {
+      set_global_error("dd_sinkhorn_global: negative or NaN mass");
+      return DD_ERR_ARG;
+    }
+    mass_mu += mu[i];
+    mass_nu += nu[i];
+  }
+  if (!(mass_mu > 0.0) || std::fabs(mass_mu - mass_nu) > 1e-9 * mass_mu) {
+    set_global_error("dd_sinkhorn_global: marginals must have equal positive mass");
+    return DD_ERR_PRECOND;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) return DD_ERR_CUDA;
+  cudaStream_t st = (cudaStream_t)stream;
+  SgBuffers B;
+  const size_t bytes = NN * sizeof(double);
+  if (cudaMalloc(&B.mu, bytes) || cudaMalloc(&B.nu, bytes) || cudaMalloc(&B.a, bytes) || cudaMalloc(&B.a2, bytes) ||
+      cudaMalloc(&B.b, bytes) || cudaMalloc(&B.in, bytes) || cudaMalloc(&B.t, bytes) || cudaMalloc(&B.out, bytes) ||
+      cudaMalloc(&B.part, kSgErrBlocks * sizeof(double)) || cudaMalloc(&B.err, sizeof(double))) {
+    set_global_error("dd_sinkhorn_global: cudaMalloc failed");
+    return DD_ERR_OOM;
+  }
+  const int smem = (N1 > N2 ? N1 : N2) * (int)sizeof(double);
+  if (smem > 48 * 1024 && cudaFuncSetAttribute(k_sg_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))
+    return DD_ERR_CUDA;
+  cudaMemcpyAsync(B.mu, mu, bytes, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(B.nu, nu, bytes, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(B.a, alpha, bytes, cudaMemcpyHostToDevice, st);
+  const double inv_eps = 1.0 / eps_p;
+  const int grid_ew = (int)std::min<long long>((NN + kSgThreads - 1) / kSgThreads, 148 * 16);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, st);
+  int it = 0;
+  double e = INFINITY;
+  double *a = B.a, *a2 = B.a2;
+  while (it < max_iter) {
+    sg_half(B, a, B.mu, B.nu, B.b, N1, N2, inv_eps, grid_ew, st);    // Y-update
+    sg_half(B, B.b, B.nu, B.mu, a2, N1, N2, inv_eps, grid_ew, st);   // X-update
+    ++it;
+    const bool check = (it % check_every == 0) || it == max_iter;
+    if (check) {
+      k_sg_err<<<kSgErrBlocks, kSgThreads, 0, st>>>(a, a2, B.mu, NN, B.part);
+      k_sg_err_final<<<1, 32, 0, st>>>(B.part, kSgErrBlocks, B.err);
+      cudaMemcpyAsync(&e, B.err, sizeof(double), cudaMemcpyDeviceToHost, st);
+      if (cudaStreamSynchronize(st) != cudaSuccess) break;
+    }
+    std::swap(a, a2);
+    if (check && e <= err * mass_mu) break;
+  }
+  sg_half(B, a, B.mu, B.nu, B.b, N1, N2, inv_eps, grid_ew, st);      // final Y-update: beta matches alpha
+  cudaEventRecord(e1, st);
+  cudaMemcpyAsync(alpha, a, bytes, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(beta, B.b, bytes, cudaMemcpyDeviceToHost, st);
+  const cudaError_t ce = cudaStreamSynchronize(st);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (ce != cudaSuccess || cudaGetLastError() != cudaSuccess) {
+    set_global_error(std::string("dd_sinkhorn_global: CUDA: ") + cudaGetErrorString(ce));
+    return DD_ERR_CUDA;
+  }
+  if (iters) *iters = it;
+  if (l1_x) *l1_x = e;
+  if (solve_ms) *solve_ms = ms;
+  if (!std::isfinite(e)) {
+    set_global_error("dd_sinkhorn_global: non-finite marginal error");
+    return DD_ERR_NUMERIC;
+  }
+  return DD_OK;
+}
+
+}  // extern "C"
