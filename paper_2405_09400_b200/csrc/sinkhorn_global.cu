@@ -38,26 +38,48 @@ __global__ void k_sg_prep(const double* __restrict__ p, const double* __restrict
 }
 
 // out[y * R + x] = LSE_z [ in[x * M + z] - (z - y)^2 * inv_eps ], x < R, y, z < M
-// (transposed so the next stage reads rows).  Max pass then sum pass.
-__global__ void k_sg_stage(const double* __restrict__ in, double* __restrict__ out, int R, int M, double inv_eps) {
+// (transposed so the next stage reads rows).  The shift m of each output is
+// the previous iteration's value of the same output when `shift` is given
+// (one pass; the fixed point makes it the LSE itself), else the
+// true maximum (a max pass).  A shifted sum outside [2^-60, 2^60] (or a
+// non-finite shift) falls back to the true maximum for that output.
+__global__ void k_sg_stage(const double* __restrict__ in, double* __restrict__ out, int R, int M, double inv_eps,
+                           const double* __restrict__ shift) {
   extern __shared__ double srow[];
   const int x = blockIdx.x;
   for (int z = threadIdx.x; z < M; z += blockDim.x) srow[z] = in[(long long)x * M + z];
   __syncthreads();
   for (int y = threadIdx.x; y < M; y += blockDim.x) {
-    double m = -INFINITY;
-    for (int z = 0; z < M; ++z) {
-      const double d = (double)(z - y);
-      m = fmax(m, fma(-d * d, inv_eps, srow[z]));
-    }
     double res = -INFINITY;
-    if (m > -INFINITY) {
-      float sum = 0.f;
+    bool done = false;
+    if (shift) {
+      const double m = shift[(long long)y * R + x];
+      if (m > -INFINITY && m < INFINITY) {
+        float sum = 0.f;
+        for (int z = 0; z < M; ++z) {
+          const double d = (double)(z - y);
+          sum += exp2f((float)((fma(-d * d, inv_eps, srow[z]) - m) * kLog2eG));
+        }
+        if (sum > 8.67361738e-19f && sum < 1.15292150e18f) {   // 2^-60 .. 2^60
+          res = m + log((double)sum);
+          done = true;
+        }
+      }
+    }
+    if (!done) {
+      double m = -INFINITY;
       for (int z = 0; z < M; ++z) {
         const double d = (double)(z - y);
-        sum += exp2f((float)((fma(-d * d, inv_eps, srow[z]) - m) * kLog2eG));
+        m = fmax(m, fma(-d * d, inv_eps, srow[z]));
       }
-      res = m + log((double)sum);
+      if (m > -INFINITY) {
+        float sum = 0.f;
+        for (int z = 0; z < M; ++z) {
+          const double d = (double)(z - y);
+          sum += exp2f((float)((fma(-d * d, inv_eps, srow[z]) - m) * kLog2eG));
+        }
+        res = m + log((double)sum);
+      }
     }
     out[(long long)y * R + x] = res;
   }
@@ -99,22 +121,26 @@ constexpr int kSgThreads = 256;
 constexpr int kSgErrBlocks = 296;   // 2 x 148 SMs
 
 struct SgBuffers {
-  double *mu = nullptr, *nu = nullptr, *a = nullptr, *a2 = nullptr, *b = nullptr, *in = nullptr, *t = nullptr,
-         *out = nullptr, *part = nullptr, *err = nullptr;
+  double *mu = nullptr, *nu = nullptr, *a = nullptr, *a2 = nullptr, *b = nullptr, *in = nullptr, *part = nullptr,
+         *err = nullptr;
+  double *t[2] = {nullptr, nullptr}, *out[2] = {nullptr, nullptr};   // per half: stage outputs (next shifts)
   ~SgBuffers() {
-    for (double* p : {mu, nu, a, a2, b, in, t, out, part, err})
+    for (double* p : {mu, nu, a, a2, b, in, t[0], t[1], out[0], out[1], part, err})
       if (p) cudaFree(p);
   }
 };
 
-// One half-iteration: dst = -LSE over the source grid of (src + log w_src - c/eps'), masked by w_dst.
-void sg_half(const SgBuffers& B, const double* src, const double* wsrc, const double* wdst, double* dst, int N1,
-             int N2, double inv_eps, int grid_ew, cudaStream_t st) {
+// One half-iteration h (0 = Y-update, 1 = X-update): dst = -LSE over the
+// source grid of (src + log w_src - c/eps'), masked by w_dst.  warm: the
+// half's stage outputs from the previous iteration serve as shifts.
+void sg_half(const SgBuffers& B, int h, bool warm, const double* src, const double* wsrc, const double* wdst,
+             double* dst, int N1, int N2, double inv_eps, int grid_ew, cudaStream_t st) {
   const long long NN = (long long)N1 * N2;
   k_sg_prep<<<grid_ew, kSgThreads, 0, st>>>(src, wsrc, B.in, NN);
-  k_sg_stage<<<N1, kSgThreads, N2 * sizeof(double), st>>>(B.in, B.t, N1, N2, inv_eps);
-  k_sg_stage<<<N2, kSgThreads, N1 * sizeof(double), st>>>(B.t, B.out, N2, N1, inv_eps);
-  k_sg_neg<<<grid_ew, kSgThreads, 0, st>>>(B.out, wdst, dst, NN);
+  k_sg_stage<<<N1, kSgThreads, N2 * sizeof(double), st>>>(B.in, B.t[h], N1, N2, inv_eps, warm ? B.t[h] : nullptr);
+  k_sg_stage<<<N2, kSgThreads, N1 * sizeof(double), st>>>(B.t[h], B.out[h], N2, N1, inv_eps,
+                                                           warm ? B.out[h] : nullptr);
+  k_sg_neg<<<grid_ew, kSgThreads, 0, st>>>(B.out[h], wdst, dst, NN);
 }
 
 }  // namespace
@@ -151,7 +177,8 @@ dd_status dd_sinkhorn_global(int32_t N1, int32_t N2, const double* mu, const dou
   SgBuffers B;
   const size_t bytes = NN * sizeof(double);
   if (cudaMalloc(&B.mu, bytes) || cudaMalloc(&B.nu, bytes) || cudaMalloc(&B.a, bytes) || cudaMalloc(&B.a2, bytes) ||
-      cudaMalloc(&B.b, bytes) || cudaMalloc(&B.in, bytes) || cudaMalloc(&B.t, bytes) || cudaMalloc(&B.out, bytes) ||
+      cudaMalloc(&B.b, bytes) || cudaMalloc(&B.in, bytes) || cudaMalloc(&B.t[0], bytes) || cudaMalloc(&B.t[1], bytes) ||
+      cudaMalloc(&B.out[0], bytes) || cudaMalloc(&B.out[1], bytes) ||
       cudaMalloc(&B.part, kSgErrBlocks * sizeof(double)) || cudaMalloc(&B.err, sizeof(double))) {
     set_global_error("dd_sinkhorn_global: cudaMalloc failed");
     return DD_ERR_OOM;
@@ -172,8 +199,8 @@ dd_status dd_sinkhorn_global(int32_t N1, int32_t N2, const double* mu, const dou
   double e = INFINITY;
   double *a = B.a, *a2 = B.a2;
   while (it < max_iter) {
-    sg_half(B, a, B.mu, B.nu, B.b, N1, N2, inv_eps, grid_ew, st);    // Y-update
-    sg_half(B, B.b, B.nu, B.mu, a2, N1, N2, inv_eps, grid_ew, st);   // X-update
+    sg_half(B, 0, it > 0, a, B.mu, B.nu, B.b, N1, N2, inv_eps, grid_ew, st);    // Y-update
+    sg_half(B, 1, it > 0, B.b, B.nu, B.mu, a2, N1, N2, inv_eps, grid_ew, st);   // X-update
     ++it;
     const bool check = (it % check_every == 0) || it == max_iter;
     if (check) {
@@ -185,7 +212,7 @@ dd_status dd_sinkhorn_global(int32_t N1, int32_t N2, const double* mu, const dou
     std::swap(a, a2);
     if (check && e <= err * mass_mu) break;
   }
-  sg_half(B, a, B.mu, B.nu, B.b, N1, N2, inv_eps, grid_ew, st);      // final Y-update: beta matches alpha
+  sg_half(B, 0, it > 0, a, B.mu, B.nu, B.b, N1, N2, inv_eps, grid_ew, st);   // final Y-update: beta matches alpha
   cudaEventRecord(e1, st);
   cudaMemcpyAsync(alpha, a, bytes, cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(beta, B.b, bytes, cudaMemcpyDeviceToHost, st);
