@@ -37,49 +37,73 @@ __global__ void k_sg_prep(const double* __restrict__ p, const double* __restrict
     in[i] = w[i] > 0.0 ? p[i] + log(w[i]) : -INFINITY;
 }
 
+// float(v) without F2F (which runs on the XU pipe next to MUFU.EX2): the
+// fp64 word's low 9 exponent bits and top 23 mantissa bits are funnel-shifted
+// into place and the exponent rebased (E_f = E_d - 896 == low9 + 128 mod 512);
+// mantissa truncated (<= 1 float ulp); sign copied.  |v| < 2^-126 gives 0
+// (2^v = 1 to fp32 precision); |v| >= 256 gives -256 (2^v = 0 for v < 0; a
+// positive v that large overflows the shifted sum, which then falls back to
+// the max pass).  Integer ops only.
+__device__ __forceinline__ float sg_d2f(double v) {
+  const unsigned hi = (unsigned)__double2hiint(v), lo = (unsigned)__double2loint(v);
+  const unsigned e = hi & 0x7ff00000u;
+  const unsigned bits = (__funnelshift_l(lo, hi, 3) + (128u << 23)) | (hi & 0x80000000u);
+  const float f = e < (897u << 20) ? 0.f : __uint_as_float(bits);
+  return e >= (1031u << 20) ? -256.f : f;
+}
+
+__device__ __forceinline__ float sg_ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// sum_z 2^(t(z) - m2) with t(z) = srow2[z] - ie2 (z - y)^2
+//   = s2[z] + z (2 ie2 y) - ie2 y^2,   s2[z] = srow2[z] - ie2 z^2 (shared).
+__device__ __forceinline__ float sg_sum(const double* s2, int M, int y, double ie2, double m2) {
+  const double g = 2.0 * ie2 * (double)y, c = fma(ie2 * (double)y, (double)y, m2);
+  float sum = 0.f;
+  double zd = 0.0;
+  for (int z = 0; z < M; ++z, zd += 1.0) sum += sg_ex2(sg_d2f(fma(zd, g, s2[z]) - c));
+  return sum;
+}
+
 // out[y * R + x] = LSE_z [ in[x * M + z] - (z - y)^2 * inv_eps ], x < R, y, z < M
-// (transposed so the next stage reads rows).  The shift m of each output is
-// the previous iteration's value of the same output when `shift` is given
-// (one pass; the fixed point makes it the LSE itself), else the
-// true maximum (a max pass).  A shifted sum outside [2^-60, 2^60] (or a
-// non-finite shift) falls back to the true maximum for that output.
+// (transposed so the next stage reads rows), computed in log2 units.  The
+// shift m of each output is the previous iteration's value of the same output
+// when `shift` is given (one pass; the fixed point makes it the
+// LSE itself), else the true maximum (a max pass).  A shifted sum outside
+// [2^-60, 2^60] (or a non-finite shift) falls back to the true maximum for
+// that output.
 __global__ void k_sg_stage(const double* __restrict__ in, double* __restrict__ out, int R, int M, double inv_eps,
                            const double* __restrict__ shift) {
-  extern __shared__ double srow[];
+  extern __shared__ double srow2[];
   const int x = blockIdx.x;
-  for (int z = threadIdx.x; z < M; z += blockDim.x) srow[z] = in[(long long)x * M + z];
+  const double ie2 = inv_eps * kLog2eG;
+  for (int z = threadIdx.x; z < M; z += blockDim.x)
+    srow2[z] = fma(-ie2 * (double)z, (double)z, in[(long long)x * M + z] * kLog2eG);   // s2[z]
   __syncthreads();
+  constexpr double kLn2 = 0.6931471805599453;
   for (int y = threadIdx.x; y < M; y += blockDim.x) {
     double res = -INFINITY;
     bool done = false;
     if (shift) {
       const double m = shift[(long long)y * R + x];
       if (m > -INFINITY && m < INFINITY) {
-        float sum = 0.f;
-        for (int z = 0; z < M; ++z) {
-          const double d = (double)(z - y);
-          sum += exp2f((float)((fma(-d * d, inv_eps, srow[z]) - m) * kLog2eG));
-        }
+        const double m2 = m * kLog2eG;
+        const float sum = sg_sum(srow2, M, y, ie2, m2);
         if (sum > 8.67361738e-19f && sum < 1.15292150e18f) {   // 2^-60 .. 2^60
-          res = m + log((double)sum);
+          res = (m2 + log2((double)sum)) * kLn2;
           done = true;
         }
       }
     }
     if (!done) {
-      double m = -INFINITY;
-      for (int z = 0; z < M; ++z) {
-        const double d = (double)(z - y);
-        m = fmax(m, fma(-d * d, inv_eps, srow[z]));
-      }
-      if (m > -INFINITY) {
-        float sum = 0.f;
-        for (int z = 0; z < M; ++z) {
-          const double d = (double)(z - y);
-          sum += exp2f((float)((fma(-d * d, inv_eps, srow[z]) - m) * kLog2eG));
-        }
-        res = m + log((double)sum);
-      }
+      double m2 = -INFINITY;
+      const double g = 2.0 * ie2 * (double)y, c = ie2 * (double)y * (double)y;
+      double zd = 0.0;
+      for (int z = 0; z < M; ++z, zd += 1.0) m2 = fmax(m2, fma(zd, g, srow2[z]) - c);
+      if (m2 > -INFINITY) res = (m2 + log2((double)sg_sum(srow2, M, y, ie2, m2))) * kLn2;
     }
     out[(long long)y * R + x] = res;
   }
