@@ -50,3 +50,20 @@ def test_no_cpu_fallback_without_device():
     with pytest.raises(DomDecError) as ei:
         DomDec.from_problem(p)
     assert ei.value.status == 4
+
+
+def test_global_sinkhorn_no_cpu_fallback_without_device():
+    """dd_sinkhorn_global validates its arguments on the host, then needs the
+    GPU: without one it returns DD_ERR_CUDA (no CPU path)."""
+    import numpy as np
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2405_09400_b200 import DomDecError, sinkhorn_global
+    mu = np.full((4, 4), 1 / 16)
+    with pytest.raises(DomDecError) as ei:
+        sinkhorn_global(mu, mu, 4.0)
+    assert ei.value.status == 4
+    with pytest.raises(DomDecError) as ei:   # argument check precedes the device
+        sinkhorn_global(mu, 2 * mu, 4.0)
+    assert ei.value.status == 2
