@@ -19,7 +19,7 @@ DESIGN.md "Oracle pins"; functions with no independent pin say
 "parity unpinned" in their docstring.
 """
 from .partitions import basic_partition, composite_partition, partition_graph_connected  # noqa: F401
-from .sinkhorn import cell_sinkhorn, dense_sinkhorn, lse  # noqa: F401
+from .sinkhorn import cell_sinkhorn, dense_sinkhorn, lse, y_update_at  # noqa: F401
 from .domdec import OracleState, init_state, domdec_sweep, basic_to_composite, balance, truncate_box  # noqa: F401
 from .flow import (edge_costs, integer_instance, min_cost_flow, mcf_bruteforce,  # noqa: F401
                    apply_flow, flow_update, flow_objective)

@@ -101,3 +101,21 @@ def dense_sinkhorn(mu: np.ndarray, nu: np.ndarray, eps_p: float, tol: float = 1e
     b = -lse(a[:, None] + logmu[:, None] - C, axis=0)
     plan = np.exp(a[:, None] + b[None, :] - C) * mux[:, None] * nuy[None, :]
     return plan, a, b, xs, ys
+
+
+def y_update_at(a: np.ndarray, mu: np.ndarray, eps_p: float, ls) -> np.ndarray:
+    """Y-half of the Sinkhorn iteration at selected target pixels only:
+    b(l) = -LSE_k [a(k) + log mu(k) - |k - l|^2 / eps'] over supp(mu)
+    (the beta-update of Eq. entropic-transport's dual, the
+    same formula as the first line of dense_sinkhorn's loop).  a, mu: (N1, N2)
+    grids; ls: (m, 2) integer pixel coordinates.  O(N1 N2) per target, so it
+    serves sampled checks at full size."""
+    N1, N2 = mu.shape
+    xs = np.flatnonzero(mu.ravel() > 0)
+    kx = np.stack([xs // N2, xs % N2], axis=1)
+    base = a.ravel()[xs] + np.log(mu.ravel()[xs])
+    ls = np.asarray(ls, dtype=np.int64).reshape(-1, 2)
+    out = np.empty(len(ls))
+    for j, l in enumerate(ls):
+        out[j] = -lse(base - sqdist(kx, l[None, :])[:, 0] / eps_p, axis=0)
+    return out

@@ -503,3 +503,32 @@ def test_hybrid_flow_decreases_objective_and_stops():
             assert dc < 0
     assert not hist[0]           # the T0 rotation has curl: the first flow moves mass
     assert all(hist[-3:])        # ... and the flows stop near the optimum
+
+
+def test_y_update_at_dirac_closed_form():
+    """mu = Dirac at k0: b(l) = |k0 - l|^2/eps' - a(k0) - log mu(k0) exactly."""
+    mu = np.zeros((5, 7))
+    mu[2, 3] = 0.5
+    a = np.full((5, 7), 0.3)
+    ls = [(0, 0), (2, 3), (4, 6), (1, 5)]
+    b = O.y_update_at(a, mu, 2.0, ls)
+    want = [((2 - r) ** 2 + (3 - c) ** 2) / 2.0 - 0.3 - np.log(0.5) for r, c in ls]
+    assert np.allclose(b, want, rtol=0, atol=1e-14)
+
+
+def test_y_update_at_brute_force_linear_domain():
+    """Brute force in the linear domain on a 3x4 grid (plain loops, no LSE):
+    exp(-b(l)) = sum_k mu(k) e^{a(k)} e^{-|k-l|^2/eps'}."""
+    rng = np.random.default_rng(7)
+    mu = rng.random((3, 4))
+    mu[1, 2] = 0.0
+    a = rng.normal(size=(3, 4))
+    eps_p = 1.5
+    ls = [(r, c) for r in range(3) for c in range(4)]
+    b = O.y_update_at(a, mu, eps_p, ls)
+    for j, (r, c) in enumerate(ls):
+        s = 0.0
+        for k1 in range(3):
+            for k2 in range(4):
+                s += mu[k1, k2] * np.exp(a[k1, k2]) * np.exp(-((k1 - r) ** 2 + (k2 - c) ** 2) / eps_p)
+        assert abs(b[j] - (-np.log(s))) <= 1e-13
