@@ -108,4 +108,5 @@ def test_global_sinkhorn_full_size_sampled(N, K):
     ls = np.stack([pick // N, pick % N], axis=1)
     want = O.y_update_at(a, p.mu, p.eps_prime, ls)
     got = b.ravel()[pick]
-    assert np.all(np.abs(got - want) <= 4 * N * 2.0 ** -24 * (1.0 + np.abs(want))), np.max(np.abs(got - want))
+    # log-domain error is absolute (log of a relatively perturbed sum); fp64 rounding of |b| adds 1e-12 |b|
+    assert np.all(np.abs(got - want) <= 4 * N * 2.0 ** -24 + 1e-12 * np.abs(want)), np.max(np.abs(got - want))
