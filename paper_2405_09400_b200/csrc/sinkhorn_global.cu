@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -222,7 +223,48 @@ dd_status dd_sinkhorn_global(int32_t N1, int32_t N2, const double* mu, const dou
   int it = 0;
   double e = INFINITY;
   double *a = B.a, *a2 = B.a2;
+  // Launch-bound at small N (8 launches per iteration): after the first
+  // check_every iterations (cold first iteration), whole chunks of
+  // check_every iterations + the error reduction run as one CUDA graph.  An
+  // even chunk returns a/a2 to their roles, so one graph serves every chunk;
+  // same kernels in the same order as the eager loop (bit-identical).
+  const bool use_graph = check_every >= 2 && check_every % 2 == 0 && !getenv("DD_SG_NO_GRAPH");
+  cudaGraphExec_t gexec = nullptr;
+  cudaStream_t cs = nullptr;
+  dd_status gs = DD_OK;
   while (it < max_iter) {
+    if (use_graph && it > 0 && it % check_every == 0 && max_iter - it > check_every) {
+      if (!gexec) {
+        cudaGraph_t g = nullptr;
+        if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+          gs = DD_ERR_CUDA;
+          break;
+        }
+        double *ga = a, *ga2 = a2;
+        for (int j = 0; j < check_every; ++j) {
+          sg_half(B, 0, true, ga, B.mu, B.nu, B.b, N1, N2, inv_eps, grid_ew, cs);
+          sg_half(B, 1, true, B.b, B.nu, B.mu, ga2, N1, N2, inv_eps, grid_ew, cs);
+          if (j == check_every - 1) {
+            k_sg_err<<<kSgErrBlocks, kSgThreads, 0, cs>>>(ga, ga2, B.mu, NN, B.part);
+            k_sg_err_final<<<1, 32, 0, cs>>>(B.part, kSgErrBlocks, B.err);
+          }
+          std::swap(ga, ga2);
+        }
+        if (cudaStreamEndCapture(cs, &g) != cudaSuccess || cudaGraphInstantiate(&gexec, g, 0) != cudaSuccess) {
+          if (g) cudaGraphDestroy(g);
+          gs = DD_ERR_CUDA;
+          break;
+        }
+        cudaGraphDestroy(g);
+      }
+      cudaGraphLaunch(gexec, st);
+      it += check_every;
+      cudaMemcpyAsync(&e, B.err, sizeof(double), cudaMemcpyDeviceToHost, st);
+      if (cudaStreamSynchronize(st) != cudaSuccess) break;
+      if (e <= err * mass_mu) break;
+      continue;
+    }
     sg_half(B, 0, it > 0, a, B.mu, B.nu, B.b, N1, N2, inv_eps, grid_ew, st);    // Y-update
     sg_half(B, 1, it > 0, B.b, B.nu, B.mu, a2, N1, N2, inv_eps, grid_ew, st);   // X-update
     ++it;
@@ -235,6 +277,14 @@ dd_status dd_sinkhorn_global(int32_t N1, int32_t N2, const double* mu, const dou
     }
     std::swap(a, a2);
     if (check && e <= err * mass_mu) break;
+  }
+  if (gexec) cudaGraphExecDestroy(gexec);
+  if (cs) cudaStreamDestroy(cs);
+  if (gs != DD_OK) {
+    set_global_error(std::string("dd_sinkhorn_global: graph capture: ") + cudaGetErrorString(cudaGetLastError()));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return gs;
   }
   sg_half(B, 0, it > 0, a, B.mu, B.nu, B.b, N1, N2, inv_eps, grid_ew, st);   // final Y-update: beta matches alpha
   cudaEventRecord(e1, st);

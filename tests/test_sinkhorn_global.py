@@ -110,3 +110,22 @@ def test_global_sinkhorn_full_size_sampled(N, K):
     got = b.ravel()[pick]
     # log-domain error is absolute (log of a relatively perturbed sum); fp64 rounding of |b| adds 1e-12 |b|
     assert np.all(np.abs(got - want) <= 4 * N * 2.0 ** -24 + 1e-12 * np.abs(want)), np.max(np.abs(got - want))
+
+
+@gpu
+def test_global_sinkhorn_graph_chunks_bit_identical(monkeypatch):
+    """Chunks of check_every iterations replayed as one CUDA graph run the
+    same kernels in the same order as the eager loop: bit-identical a, b,
+    iteration count and error, at fixed K and under the stopping rule."""
+    from paper_2405_09400_b200 import sinkhorn_global
+    p = make_problem("gm", 64, 2, theta_deg=20.0, seed=4)
+    runs = {}
+    for mode in ("graph", "eager"):
+        if mode == "eager":
+            monkeypatch.setenv("DD_SG_NO_GRAPH", "1")
+        runs[mode] = (sinkhorn_global(p.mu, p.nu, p.eps_prime, err=0.0, max_iter=42, check_every=4),
+                      sinkhorn_global(p.mu, p.nu, p.eps_prime, err=1e-4, max_iter=100000, check_every=10))
+    for (ag, bg, ig, eg, _), (ae, be, ie, ee, _) in zip(runs["graph"], runs["eager"]):
+        assert ig == ie and eg == ee
+        assert np.array_equal(ag, ae) and np.array_equal(bg, be)
+    assert runs["graph"][0][2] == 42
