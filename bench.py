@@ -336,10 +336,15 @@ def run_ours(a):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             res, conv, flows = None, float("nan"), 0
+            t_sw = t_fl = 0.0   # host time per phase (each stats call synchronises)
             for c in range(cap_cycles):
+                t1 = time.perf_counter()
                 sa = dd3.sweep("A", stats=True)
                 sb = dd3.sweep("B", stats=True)
+                t2 = time.perf_counter()
                 fs = dd3.flow_update(stats=True)
+                t_sw += t2 - t1
+                t_fl += time.perf_counter() - t2
                 flows += int(fs["stationary"] == 0)
                 conv = allmax(max(sa["l1x_entry"], sb["l1x_entry"]))
                 if conv <= 1e-4:
@@ -355,6 +360,7 @@ def run_ours(a):
                 res = {"seconds": None, "reached": False, "cycles_run": cap_cycles, "last_entry_error": conv,
                        "nonstationary_flows": flows}
             res["workload"] = f"GM(rank) {N}^2 s={s} eps=(2h)^2 theta={theta:g}deg, hybrid A/B/flow"
+            res["phase_seconds"] = {"sweeps": t_sw, "flow_updates": t_fl}
             dd3.close()
             return res
 
