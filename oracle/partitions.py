@@ -49,11 +49,13 @@ def composite_partition(n1: int, n2: int, kind: str):
     return cells
 
 
-def partition_graph_connected(n1: int, n2: int) -> bool:
+def partition_graph_connected(n1: int, n2: int, A=None, B=None) -> bool:
     """Def. PartitionGraph: vertices = A and B composite
-    cells, edge iff they share a basic cell.  BFS connectivity."""
-    A = composite_partition(n1, n2, "A")
-    B = composite_partition(n1, n2, "B")
+    cells, edge iff they share a basic cell.  BFS connectivity.  A and B
+    default to the staggered grid partitions; explicit partitions (lists of
+    basic-cell index lists) may be given."""
+    A = composite_partition(n1, n2, "A") if A is None else A
+    B = composite_partition(n1, n2, "B") if B is None else B
     verts = [("A", k) for k in range(len(A))] + [("B", k) for k in range(len(B))]
     owner = {}
     for k, J in enumerate(A):

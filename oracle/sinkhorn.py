@@ -75,7 +75,7 @@ def cell_sinkhorn(mu_x: np.ndarray, kx: np.ndarray, nu_y: np.ndarray, ly: np.nda
 
 
 def dense_sinkhorn(mu: np.ndarray, nu: np.ndarray, eps_p: float, tol: float = 1e-13,
-                   max_iter: int = 200000):
+                   max_iter: int = 200000, a0=None):
     """Global dense log-domain Sinkhorn on the whole grid problem
     (Eq. entropic-transport) — the brute-force reference
     (O6).  Runs until the L1 X-marginal error after the Y-update is
@@ -90,7 +90,7 @@ def dense_sinkhorn(mu: np.ndarray, nu: np.ndarray, eps_p: float, tol: float = 1e
     nuy = nu.ravel()[ys]
     C = sqdist(kx, ly) / eps_p
     logmu, lognu = np.log(mux), np.log(nuy)
-    a = np.zeros(len(xs))
+    a = np.zeros(len(xs)) if a0 is None else np.asarray(a0, np.float64).ravel()[xs].copy()
     for _ in range(max_iter):
         b = -lse(a[:, None] + logmu[:, None] - C, axis=0)
         a_new = -lse(b[None, :] + lognu[None, :] - C, axis=1)

@@ -148,6 +148,37 @@ def test_partitions(n):
     assert O.partition_graph_connected(n, n)
 
 
+def test_partition_graph_hand_cases():
+    """Def. PartitionGraph on hand-made partitions of 2x2
+    basic cells (n1 = n2 = 2): if B = A, each A-cell only meets its own copy
+    (two components per cell pair: disconnected whenever there are >= 2
+    cells); a B that straddles the A-cells joins them (connected).  Also a
+    1 x 3 strip where B = {0}, {1, 2} and A = {0, 1}, {2}: path A0-B0,
+    A0-B1, B1-A1 (connected); with B = {0, 1}, {2} = A it is disconnected."""
+    A = [[0, 1], [2, 3]]
+    assert not O.partition_graph_connected(2, 2, A=A, B=[[0, 1], [2, 3]])
+    assert O.partition_graph_connected(2, 2, A=A, B=[[0], [1, 2], [3]])
+    assert not O.partition_graph_connected(2, 2, A=[[0], [1], [2], [3]], B=[[0], [1], [2], [3]])
+    assert O.partition_graph_connected(1, 3, A=[[0, 1], [2]], B=[[0], [1, 2]])
+    assert not O.partition_graph_connected(1, 3, A=[[0, 1], [2]], B=[[0, 1], [2]])
+
+
+def test_integer_instance_half_even_hand_case():
+    """Reading R11: C_ij = round_half_even(c_bar_ij * 2^10), 0 on the self arc
+    and on arcs leaving the grid (NaN); q exact.  Hand values on the exact
+    half-integers of the cost quantum: 0.5 -> 0, 1.5 -> 2, 2.5 -> 2,
+    -0.5 -> 0, -1.5 -> -2, 3.25 -> 3, -2.75 -> -3 (floor or ceil or round
+    half away from zero each fail one of them)."""
+    u = 1.0 / 1024.0
+    cbar = np.array([[0.0, 0.5 * u, 1.5 * u, 2.5 * u, np.nan],
+                     [7.0, -0.5 * u, -1.5 * u, 3.25 * u, -2.75 * u]])
+    q = np.array([5, 9], dtype=np.int64)
+    C, qq = O.integer_instance(cbar, q)
+    assert C.dtype == np.int64 and qq.dtype == np.int64
+    assert C.tolist() == [[0, 0, 2, 2, 0], [0, 0, -2, 3, -3]]
+    assert qq.tolist() == [5, 9]
+
+
 def test_zero_mass_cell_rejected():
     """m_i > 0 is required (PAPER.md:233)."""
     mu = np.ones((4, 4))
