@@ -195,6 +195,15 @@ dd_status domdec_export_alpha(dd_ctx *ctx, dd_partition part, double *alpha);
  * units (reading R13), host [I].  Synchronises. */
 dd_status domdec_export_plan_cost(dd_ctx *ctx, double *Qm);
 
+/* Per composite cell statistics of the last sweep on a partition, in the
+ * partition's cell order (row-major over the composite-cell grid; stripe
+ * mode: the cells this context solves): Sinkhorn passes iters [ncells], the
+ * X-error after the first pass e0 and of the returned plan e (reading R14),
+ * host arrays, any may be NULL.  *ncells receives the count (ncells may be
+ * NULL).  DD_ERR_PRECOND if the partition was never swept.  Synchronises. */
+dd_status domdec_export_cell_stats(dd_ctx *ctx, dd_partition part, int32_t *iters, double *e0, double *e,
+                                   int32_t *ncells);
+
 /* Step 1 of the flow update alone: edge costs of the current state.
  * cbar [I][5] fp64 pixel^2 units (NaN on arcs leaving the grid, 0 on self),
  * C [I][5] int64 integer costs, q [I] supplies.  Any pointer may be NULL. */
@@ -271,6 +280,56 @@ dd_status domdec_halo_pack(dd_ctx *ctx, int32_t row, void *buf, int64_t cap, int
  * problem).  The boxes are appended to the current pool (DD_ERR_NUMERIC if it
  * is full).  Synchronises. */
 dd_status domdec_halo_unpack(dd_ctx *ctx, int32_t row, const void *buf, int64_t bytes);
+
+/* ---- Multiscale domain decomposition ----------------
+ * App. A.2.1 "Multi-scale and eps-scaling" runs every
+ * solver coarse to fine (the strategy of [BoSch2020, Sec. 6.4]);
+ * the paper gives no procedure, so the library follows DESIGN.md readings
+ * R23-R25: layers N_l = N / 2^(L-1-l) with the same cell size, mu_l and nu_l
+ * 2x2 block sums of the next finer layer; eps = eps' h_l^2 on every layer;
+ * refinement nu_i'(y') = (nu_i(y) (m_i'/m_i)) (nu(y') / nu_l(y)) for a fine
+ * cell i' in coarse cell i and a fine pixel y' in coarse pixel y, then
+ * truncation + minimal box; the coarsest layer starts from the product
+ * coupling nu_i = m_i nu. */
+
+/* A context whose initial coupling is the product coupling mu (x) nu
+ * (nu_i = m_i nu on the box of supp(nu), truncated at options->trunc), built
+ * on the device.  problem->init_* are ignored.  Errors as domdec_init. */
+dd_status domdec_init_product(const dd_problem *problem, const dd_options *options, dd_ctx **out);
+
+/* A context for the next finer layer (R25): fine->N1 = 2 coarse N1 (same for
+ * N2), same cell size; fine->mu / nu (host) must coarsen (2x2 sums) to the
+ * coarse problem's mu / nu (DD_ERR_PRECOND otherwise).  The initial coupling
+ * is the refinement of the coarse context's current basic-cell marginals,
+ * computed on the device; fine->init_* are ignored.  The coarse context is
+ * not modified (its stream is used and synchronised). */
+dd_status domdec_refine(dd_ctx *coarse, const dd_problem *fine, const dd_options *options, dd_ctx **out);
+
+typedef struct {
+  int32_t levels;       /* layers L (1..16); the coarsest grid is N / 2^(L-1), with >= 2 basic cells per axis */
+  int32_t max_cycles;   /* cap of hybrid cycles per layer                                   */
+  int32_t flow_every;   /* flow update after every k-th cycle; 0 = pure domdec */
+  double conv;          /* layer done when both sweep-entry errors / ||mu|| <= conv (R14)   */
+} dd_ms_options;
+
+typedef struct {
+  int32_t levels;
+  int32_t N[16];        /* grid side of each layer (N1)                                      */
+  int32_t cycles[16];   /* hybrid cycles run per layer                                       */
+  int32_t flows[16];    /* non-stationary flow updates per layer                             */
+  int32_t converged[16];
+  double entry_error[16];   /* max of the A and B sweep-entry errors / ||mu|| of the last cycle */
+  double seconds[16];   /* wall time per layer (initial coupling / refinement included)      */
+  double total_seconds; /* wall time of the whole call                                       */
+} dd_ms_stats;
+
+/* Coarse-to-fine hybrid solve of the problem (init_* ignored; eps' =
+ * eps / h^2 is kept on every layer, R24).  On success *out is the finest
+ * layer's context in its final state (query it with marginal_error,
+ * primal_dual_gap, exports, or keep iterating).  stats may be NULL.
+ * Synchronises once per cycle (convergence test). */
+dd_status dd_multiscale_solve(const dd_problem *problem, const dd_options *options, const dd_ms_options *ms,
+                              dd_ctx **out, dd_ms_stats *stats);
 
 /* Release all device memory of ctx.  NULL is a no-op. */
 dd_status domdec_destroy(dd_ctx *ctx);

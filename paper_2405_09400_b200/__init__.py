@@ -7,5 +7,6 @@ torch.distributed for multi-process runs); the computation is entirely in the
 library's CUDA kernels.  There is no CPU fallback.
 """
 from ._lib import (DomDec, DomDecError, FlowStats, SweepStats, mincost_flow, mufu_peak, lib, sinkhorn_global,  # noqa: F401,E501
+                   multiscale_solve,
                    LIB_PATH, EXPORTED, PART_A, PART_B)
 from .build import build_library  # noqa: F401

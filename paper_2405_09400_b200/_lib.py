@@ -59,6 +59,22 @@ class FlowStats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class MsOptions(C.Structure):
+    _fields_ = [("levels", C.c_int32), ("max_cycles", C.c_int32), ("flow_every", C.c_int32), ("conv", C.c_double)]
+
+
+class MsStats(C.Structure):
+    _fields_ = [("levels", C.c_int32), ("N", C.c_int32 * 16), ("cycles", C.c_int32 * 16), ("flows", C.c_int32 * 16),
+                ("converged", C.c_int32 * 16), ("entry_error", C.c_double * 16), ("seconds", C.c_double * 16),
+                ("total_seconds", C.c_double)]
+
+    def as_dict(self):
+        L = self.levels
+        return {"levels": L, "N": list(self.N[:L]), "cycles": list(self.cycles[:L]), "flows": list(self.flows[:L]),
+                "converged": [bool(x) for x in self.converged[:L]], "entry_error": list(self.entry_error[:L]),
+                "seconds": list(self.seconds[:L]), "total_seconds": self.total_seconds}
+
+
 class Counters(C.Structure):
     _fields_ = [("sweeps", C.c_int64), ("flow_updates", C.c_int64), ("cells", C.c_int64), ("iters", C.c_int64),
                 ("mufu_ops", C.c_double), ("bytes", C.c_double)]
@@ -88,6 +104,9 @@ def lib():
                                           C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_int64)]
         L.domdec_export_alpha.argtypes = [vp, C.c_int, C.POINTER(C.c_double)]
         L.domdec_export_plan_cost.argtypes = [vp, C.POINTER(C.c_double)]
+        if hasattr(L, "domdec_export_cell_stats"):   # (absent from older development builds)
+            L.domdec_export_cell_stats.argtypes = [vp, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_double),
+                                                   C.POINTER(C.c_double), C.POINTER(C.c_int32)]
         L.flow_edge_costs.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.flow_apply.argtypes = [vp, C.POINTER(C.c_int64)]
         L.dd_mincost_flow.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
@@ -99,6 +118,11 @@ def lib():
         L.domdec_halo_pack.argtypes = [vp, C.c_int32, vp, C.c_int64, C.POINTER(C.c_int64)]
         L.domdec_halo_unpack.argtypes = [vp, C.c_int32, vp, C.c_int64]
         L.domdec_destroy.argtypes = [vp]
+        if hasattr(L, "dd_multiscale_solve"):   # (absent from older development builds)
+            L.domdec_init_product.argtypes = [C.POINTER(_Problem), C.POINTER(_Options), C.POINTER(vp)]
+            L.domdec_refine.argtypes = [vp, C.POINTER(_Problem), C.POINTER(_Options), C.POINTER(vp)]
+            L.dd_multiscale_solve.argtypes = [C.POINTER(_Problem), C.POINTER(_Options), C.POINTER(MsOptions),
+                                              C.POINTER(vp), C.POINTER(MsStats)]
         L.domdec_counters.argtypes = [vp, C.POINTER(Counters)]
         L.domdec_reset_counters.argtypes = [vp]
         L.dd_mufu_peak.argtypes = [C.c_int32, C.POINTER(C.c_double)]
@@ -107,19 +131,53 @@ def lib():
         L.dd_version.restype = C.c_char_p
         for fn in ("domdec_init", "domdec_sweep", "flow_update", "marginal_error", "primal_dual_gap",
                    "domdec_export_cells", "domdec_export_alpha", "domdec_export_plan_cost",
-                   "flow_edge_costs", "flow_apply", "dd_mincost_flow", "domdec_destroy", "domdec_counters",
+                   "domdec_export_cell_stats", "flow_edge_costs", "flow_apply", "dd_mincost_flow", "domdec_destroy", "domdec_counters",
                    "domdec_reset_counters", "dd_mufu_peak", "domdec_halo_pack", "domdec_halo_unpack",
-                   "dd_sinkhorn_global"):
-            getattr(L, fn).restype = C.c_int
+                   "dd_sinkhorn_global", "domdec_init_product", "domdec_refine", "dd_multiscale_solve",
+                   "domdec_export_cell_stats"):
+            if hasattr(L, fn):
+                getattr(L, fn).restype = C.c_int
         _lib = L
     return _lib
 
 
 EXPORTED = ("domdec_init", "domdec_sweep", "flow_update", "marginal_error", "primal_dual_gap",
-            "domdec_export_cells", "domdec_export_alpha", "domdec_export_plan_cost", "flow_edge_costs",
+            "domdec_export_cells", "domdec_export_alpha", "domdec_export_plan_cost", "domdec_export_cell_stats",
+            "flow_edge_costs",
             "flow_apply", "dd_mincost_flow", "domdec_destroy", "dd_last_error", "dd_version", "domdec_counters",
             "domdec_reset_counters", "dd_mufu_peak", "domdec_halo_pack", "domdec_halo_unpack",
-            "dd_sinkhorn_global")
+            "dd_sinkhorn_global", "domdec_init_product", "domdec_refine", "dd_multiscale_solve")
+
+
+def _problem(mu, nu, s, eps, h, E, off=None, ext=None, pos=None, data=None):
+    N1, N2 = mu.shape
+    return _Problem(N1, N2, float(h), float(eps), int(s), _ptr(mu, C.c_double), _ptr(nu, C.c_double),
+                    _ptr(off, C.c_int32) if off is not None else None, _ptr(ext, C.c_int32) if ext is not None else None,
+                    _ptr(pos, C.c_int64) if pos is not None else None,
+                    _ptr(data, C.c_double) if data is not None else None, int(E))
+
+
+def _options(err=1e-4, max_iter=2000, fixed_iter=0, trunc=1e-15, slot_cap=0, comp_cap=0, device=0, stream=None,
+             track_primal=False, row_begin=0, row_end=0):
+    return _Options(float(err), int(max_iter), int(fixed_iter), float(trunc), int(slot_cap), int(comp_cap),
+                    int(device), C.c_void_p(stream) if stream else None, int(bool(track_primal)),
+                    int(row_begin), int(row_end))
+
+
+def multiscale_solve(mu, nu, cell_size, eps, E, levels, conv=1e-4, max_cycles=1000, flow_every=1, **opts):
+    """dd_multiscale_solve (readings R23-R25): coarse-to-fine
+    hybrid domain decomposition of the N1 x N2 problem on [-1, 1]^2 (h = 2/N1,
+    eps in physical units, eps' = eps/h^2 kept on every layer).  Returns
+    (DomDec of the finest layer, stats dict)."""
+    mu_ = np.ascontiguousarray(mu, np.float64)
+    nu_ = np.ascontiguousarray(nu, np.float64)
+    P = _problem(mu_, nu_, cell_size, eps, 2.0 / mu_.shape[0], E)
+    O = _options(**opts)
+    M = MsOptions(int(levels), int(max_cycles), int(flow_every), float(conv))
+    st = MsStats()
+    ctx = C.c_void_p()
+    _check(lib().dd_multiscale_solve(C.byref(P), C.byref(O), C.byref(M), C.byref(ctx), C.byref(st)), None)
+    return DomDec._wrap(ctx, mu_, nu_, cell_size), st.as_dict()
 
 
 def _ptr(a, ctype):
@@ -139,25 +197,49 @@ class DomDec:
     (domdec_init); all further calls operate on device-resident state."""
 
     def __init__(self, mu, nu, cell_size, eps, h, init_off, init_ext, init_pos, init_data, mass_exponent,
-                 err=1e-4, max_iter=2000, fixed_iter=0, trunc=1e-15, slot_cap=0, comp_cap=0, device=0,
-                 stream=None, track_primal=False, row_begin=0, row_end=0):
-        self._keep = [np.ascontiguousarray(mu, np.float64), np.ascontiguousarray(nu, np.float64),
-                      np.ascontiguousarray(init_off, np.int32), np.ascontiguousarray(init_ext, np.int32),
-                      np.ascontiguousarray(init_pos, np.int64), np.ascontiguousarray(init_data, np.float64)]
-        mu_, nu_, off_, ext_, pos_, data_ = self._keep
+                 _how="init", _coarse=None, **opts):
+        self._keep = [np.ascontiguousarray(mu, np.float64), np.ascontiguousarray(nu, np.float64)]
+        if _how == "init":
+            self._keep += [np.ascontiguousarray(init_off, np.int32), np.ascontiguousarray(init_ext, np.int32),
+                           np.ascontiguousarray(init_pos, np.int64), np.ascontiguousarray(init_data, np.float64)]
+        mu_, nu_ = self._keep[:2]
         self.N1, self.N2 = mu_.shape
         self.s = int(cell_size)
         self.n1, self.n2 = self.N1 // self.s, self.N2 // self.s
         self.I = self.n1 * self.n2
-        P = _Problem(self.N1, self.N2, float(h), float(eps), self.s, _ptr(mu_, C.c_double), _ptr(nu_, C.c_double),
-                     _ptr(off_, C.c_int32), _ptr(ext_, C.c_int32), _ptr(pos_, C.c_int64), _ptr(data_, C.c_double),
-                     int(mass_exponent))
-        O = _Options(float(err), int(max_iter), int(fixed_iter), float(trunc), int(slot_cap), int(comp_cap),
-                     int(device), C.c_void_p(stream) if stream else None, int(bool(track_primal)),
-                     int(row_begin), int(row_end))
+        P = _problem(mu_, nu_, self.s, eps, h, mass_exponent, *(self._keep[2:] if _how == "init" else ()))
+        O = _options(**opts)
         ctx = C.c_void_p()
-        _check(lib().domdec_init(C.byref(P), C.byref(O), C.byref(ctx)), None)
+        if _how == "init":
+            _check(lib().domdec_init(C.byref(P), C.byref(O), C.byref(ctx)), None)
+        elif _how == "product":
+            _check(lib().domdec_init_product(C.byref(P), C.byref(O), C.byref(ctx)), None)
+        else:
+            _check(lib().domdec_refine(_coarse._ctx, C.byref(P), C.byref(O), C.byref(ctx)), None)
         self._ctx = ctx
+
+    @classmethod
+    def product(cls, mu, nu, cell_size, eps, h, mass_exponent, **opts):
+        """Context started from the product coupling mu (x) nu (domdec_init_product)."""
+        return cls(mu, nu, cell_size, eps, h, None, None, None, None, mass_exponent, _how="product", **opts)
+
+    def refine(self, mu_f, nu_f, eps_f, mass_exponent, **opts):
+        """Context of the next finer layer initialised with the refinement of
+        this context's marginals (domdec_refine, readings R23-R25)."""
+        N1 = np.asarray(mu_f).shape[0]
+        return DomDec(mu_f, nu_f, self.s, eps_f, 2.0 / N1, None, None, None, None, mass_exponent, _how="refine",
+                      _coarse=self, **opts)
+
+    @classmethod
+    def _wrap(cls, ctx, mu, nu, s):
+        self = cls.__new__(cls)
+        self._keep = [mu, nu]
+        self.N1, self.N2 = mu.shape
+        self.s = int(s)
+        self.n1, self.n2 = self.N1 // self.s, self.N2 // self.s
+        self.I = self.n1 * self.n2
+        self._ctx = ctx
+        return self
 
     @classmethod
     def from_problem(cls, p, **kw):
@@ -228,6 +310,18 @@ class DomDec:
         _check(lib().domdec_export_alpha(self._ctx, PART_A if part in ("A", 0) else PART_B, _ptr(a, C.c_double)),
                self._ctx)
         return a
+
+    def cell_stats(self, part):
+        """Per composite cell (iters, e0, e) of the last sweep on a partition."""
+        pp = PART_A if part in ("A", 0) else PART_B
+        n = C.c_int32()
+        _check(lib().domdec_export_cell_stats(self._ctx, pp, None, None, None, C.byref(n)), self._ctx)
+        it = np.zeros(n.value, np.int32)
+        e0 = np.zeros(n.value, np.float64)
+        e = np.zeros(n.value, np.float64)
+        _check(lib().domdec_export_cell_stats(self._ctx, pp, _ptr(it, C.c_int32), _ptr(e0, C.c_double),
+                                              _ptr(e, C.c_double), C.byref(n)), self._ctx)
+        return it, e0, e
 
     def export_plan_cost(self):
         q = np.zeros(self.I, np.float64)

@@ -1,5 +1,6 @@
 // api.cu — C-ABI entry points of libdomdec (include/domdec.h).
 #include <cmath>
+#include <cstddef>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -159,10 +160,13 @@ void free_ctx(dd_ctx* c) {
                   c->d_off[1], c->d_ext[0], c->d_ext[1], c->d_cells[0], c->d_cells[1], c->d_alpha[0],
                   c->d_alpha[1], c->d_gauge[0], c->d_gauge[1], c->d_stats[0], c->d_stats[1], c->d_totals[0],
                   c->d_totals[1], c->d_mom, c->d_xbar, c->d_var, c->d_cbar, c->d_C, c->d_w, c->d_mcf,
-                  c->d_flow_info, c->d_scratch, c->d_red, c->d_ovf, c->d_cum, c->d_ecell, c->d_pd, c->d_halo};
+                  c->d_flow_info, c->d_scratch, c->d_red, c->d_cls, c->d_cum, c->d_ecell, c->d_pd, c->d_halo};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  if (c->aux) cudaStreamDestroy(c->aux);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c;
 }
 
@@ -174,8 +178,29 @@ void free_ctx(dd_ctx* c) {
     if (s_ != DD_OK) return s_;    \
   } while (0)
 
-static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c) {
-  if (!P || !P->mu || !P->nu || !P->init_off || !P->init_ext || !P->init_pos || !P->init_data) {
+// Per basic cell box mass (initial-coupling check of the device init path).
+__global__ void k_box_mass(const double* __restrict__ pool, const long long* __restrict__ pos,
+                           const int* __restrict__ ext, const double* __restrict__ m, int I,
+                           unsigned long long* __restrict__ bad) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= I) return;
+  const long long len = (long long)ext[2 * i] * ext[2 * i + 1];
+  double s = 0.0;
+  bool ok = true;
+  for (long long t = 0; t < len; ++t) {
+    const double v = pool[pos[i] + t];
+    ok = ok && v >= 0.0 && isfinite(v);
+    s += v;
+  }
+  if (!ok || fabs(s - m[i]) > 1e-6 * m[i]) atomicAdd(bad, 1ull);
+}
+
+// init_impl: P's initial coupling comes either from host arrays (the public
+// domdec_init) or, with dev != NULL, from device arrays written by a kernel
+// of the library (multiscale refinement, multiscale.cu); then P->init_* are
+// ignored and the coupling is checked on the device.
+static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c, const DevInit* dev = nullptr) {
+  if (!P || !P->mu || !P->nu || (!dev && (!P->init_off || !P->init_ext || !P->init_pos || !P->init_data))) {
     c->err = "NULL problem pointer";
     return DD_ERR_ARG;
   }
@@ -252,16 +277,22 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c) 
     c->err = "sum(mu) != sum(nu)";
     return DD_ERR_PRECOND;
   }
-  std::vector<double> acc(NN, 0.0);
+  std::vector<double> acc(dev ? 0 : NN, 0.0);
   int maxext1 = 0, maxext2 = 0;
   long long maxbox = 0;
+  const int* hoff = dev ? dev->h_off : P->init_off;
+  const int* hext = dev ? dev->h_ext : P->init_ext;
   for (int i = 0; i < I; ++i) {
-    const int r0 = P->init_off[2 * i], c0 = P->init_off[2 * i + 1];
-    const int e1 = P->init_ext[2 * i], e2 = P->init_ext[2 * i + 1];
-    if (e1 < 1 || e2 < 1 || r0 < 0 || c0 < 0 || r0 + e1 > c->N1 || c0 + e2 > c->N2 || P->init_pos[i] < 0) {
+    const int r0 = hoff[2 * i], c0 = hoff[2 * i + 1];
+    const int e1 = hext[2 * i], e2 = hext[2 * i + 1];
+    if (e1 < 1 || e2 < 1 || r0 < 0 || c0 < 0 || r0 + e1 > c->N1 || c0 + e2 > c->N2 || (!dev && P->init_pos[i] < 0)) {
       c->err = "initial box " + std::to_string(i) + " outside the grid";
       return DD_ERR_PRECOND;
     }
+    maxext1 = std::max(maxext1, e1);
+    maxext2 = std::max(maxext2, e2);
+    maxbox = std::max(maxbox, (long long)e1 * e2);
+    if (dev) continue;   // values are checked on the device below
     double mass = 0;
     for (int a = 0; a < e1; ++a)
       for (int b = 0; b < e2; ++b) {
@@ -277,12 +308,10 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c) 
       c->err = "initial ||nu_i|| != m_i for cell " + std::to_string(i);
       return DD_ERR_PRECOND;
     }
-    maxext1 = std::max(maxext1, e1);
-    maxext2 = std::max(maxext2, e2);
-    maxbox = std::max(maxbox, (long long)e1 * e2);
   }
   double l1 = 0;
-  for (long long t = 0; t < NN; ++t) l1 += std::fabs(acc[t] - P->nu[t]);
+  if (!dev)
+    for (long long t = 0; t < NN; ++t) l1 += std::fabs(acc[t] - P->nu[t]);
   if (l1 > 1e-6 * snu) {
     c->err = "initial boxes do not reproduce nu (L1 = " + std::to_string(l1) + ")";
     return DD_ERR_PRECOND;
@@ -290,26 +319,14 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c) 
   // ---- capacities -------------------------
   const double tail = std::sqrt(c->eps_p * std::log(1e10));   // radius where nu_i drops ~1e-10 of its peak
   int side = std::max(maxext1, maxext2);
-  // small size class: typical composite hull; large class: everything that
-  // fits in 227 KB of shared memory.
-  c->ccap = c->opt.comp_cap > 0 ? c->opt.comp_cap : 2 * s + 2 * (int)std::ceil(tail) + 4;
-  c->ccap = std::min(c->ccap, std::max(c->N1, c->N2));
-  c->ccap_big = c->ccap;
-  while (c->ccap_big < std::max(c->N1, c->N2) && sweep_smem_bytes(c->ccap_big + 1, s) <= 200 * 1024) ++c->ccap_big;
-  if (const char* env = getenv("DD_CCAP_BIG"))   // testing knob: route more cells to the global-scratch class
-    c->ccap_big = std::max(c->ccap, std::min(c->ccap_big, atoi(env)));
-  if (sweep_smem_bytes(c->ccap, s) > 200 * 1024) {
-    c->err = "composite box capacity too large for shared memory (eps too large for this build)";
-    return DD_ERR_ARG;
-  }
   // variable-size pool (bump-allocated each sweep): average capacity per basic
   // cell from the eps blur, generous; the total is what matters
   side = std::max(side, 2 * s + 2 * (int)std::ceil(tail) + 12);
   long long init_total = 0;
-  for (int i = 0; i < I; ++i) init_total += (long long)P->init_ext[2 * i] * P->init_ext[2 * i + 1];
+  for (int i = 0; i < I; ++i) init_total += (long long)hext[2 * i] * hext[2 * i + 1];
+  if (dev) init_total = std::max(init_total, dev->total);
   const long long per_cell = c->opt.slot_cap > 0 ? c->opt.slot_cap : (long long)side * side;
   c->pool_cap = std::max<long long>((long long)I * per_cell, 2 * init_total);
-  c->ccap_huge = std::max(c->N1, c->N2);
   // ---- device --------------------------------------------------------------
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= c->device) {
@@ -330,8 +347,23 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c) 
   TRY(dalloc(c, &c->d_red, 64));
   TRY(dalloc(c, &c->d_cum, 1));
   TRY(dalloc(c, &c->d_poolctr, 2));
-  c->scratch_stride = (sweep_scratch_bytes(c->ccap_huge, s) + 255) & ~size_t(255);
-  TRY(dalloc(c, &c->d_scratch_huge, 16 * c->scratch_stride));
+  {
+    // size classes of the sweep (sweep.cu)
+    int nsm = 148;
+    DD_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+    const int maxcells = (c->n1 / 2 + 1) * (c->n2 / 2 + 1);
+    cudaError_t e = sweep_classes(s, std::max(c->N1, c->N2), nsm, maxcells, &c->cls, &c->scratch_stride);
+    if (e != cudaSuccess) {
+      c->err = std::string("sweep size classes: ") + cudaGetErrorString(e);
+      return DD_ERR_CUDA;
+    }
+    if (c->opt.comp_cap > 0)   // testing knob: route larger hulls to the global-scratch class
+      for (int k = 0; k < kClasses - 1; ++k) c->cls.ccap[k] = std::min(c->cls.ccap[k], c->opt.comp_cap);
+    TRY(dalloc(c, &c->d_scratch_huge, 16 * c->scratch_stride));
+    DD_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    DD_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    DD_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  }
   DD_CUDA(cudaMemsetAsync(c->d_cum, 0, sizeof(SweepTotals), c->stream));
   for (int b = 0; b < 2; ++b) {
     TRY(dalloc(c, &c->d_pool[b], (size_t)c->pool_cap));
@@ -354,7 +386,7 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c) 
     TRY(dalloc(c, &c->d_alpha[b], NN));
     TRY(dalloc(c, &c->d_gauge[b], (size_t)c->ncells[b] * 2));
     TRY(dalloc(c, &c->d_stats[b], c->ncells[b]));
-    if (b == 1) TRY(dalloc(c, &c->d_ovf, 2 * (size_t)std::max(c->ncells[0], c->ncells[1]) + 8));
+    if (b == 1) TRY(dalloc(c, &c->d_cls, 16 + (size_t)kClasses * std::max(c->ncells[0], c->ncells[1])));
     if (b == 1) TRY(dalloc(c, &c->d_ecell, (size_t)std::max(c->ncells[0], c->ncells[1])));
     TRY(dalloc(c, &c->d_totals[b], 1));
     DD_CUDA(cudaMemcpyAsync(c->d_cells[b], c->h_cells[b].data(), sizeof(CompCell) * c->ncells[b],
@@ -377,8 +409,35 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c) 
     }
   DD_CUDA(cudaMemcpyAsync(c->d_m, m.data(), I * 8, cudaMemcpyHostToDevice, st));
   DD_CUDA(cudaMemcpyAsync(c->d_q, q.data(), I * 8, cudaMemcpyHostToDevice, st));
-  // initial boxes -> pool[0] (slots)
-  {
+  // initial boxes -> pool[0]
+  if (dev) {
+    const unsigned long long ctr0[2] = {(unsigned long long)dev->total, 0ull};
+    DD_CUDA(cudaMemcpyAsync(c->d_pool[0], dev->d_pool, (size_t)dev->total * 8, cudaMemcpyDeviceToDevice, st));
+    DD_CUDA(cudaMemcpyAsync(c->d_pos[0], dev->d_pos, I * 8, cudaMemcpyDeviceToDevice, st));
+    DD_CUDA(cudaMemcpyAsync(c->d_off[0], dev->d_off, I * 8, cudaMemcpyDeviceToDevice, st));
+    DD_CUDA(cudaMemcpyAsync(c->d_ext[0], dev->d_ext, I * 8, cudaMemcpyDeviceToDevice, st));
+    DD_CUDA(cudaMemcpyAsync(c->d_poolctr, ctr0, 16, cudaMemcpyHostToDevice, st));
+    // feasibility of the device-made coupling: ||nu_i|| = m_i, sum_i nu_i = nu
+    unsigned long long* bad = (unsigned long long*)(c->d_red + 16);
+    DD_CUDA(cudaMemsetAsync(bad, 0, 8, st));
+    k_box_mass<<<(I + 127) / 128, 128, 0, st>>>(c->d_pool[0], c->d_pos[0], c->d_ext[0], c->d_m, I, bad);
+    DD_CUDA(cudaGetLastError());
+    DD_CUDA(cudaMemsetAsync(c->d_scratch, 0, NN * 8, st));
+    k_scatter_boxes<<<I, 128, 0, st>>>(c->d_pool[0], c->d_pos[0], c->d_off[0], c->d_ext[0], c->N2, c->d_scratch, 0);
+    DD_CUDA(cudaGetLastError());
+    k_l1_diff<<<1, 1024, 0, st>>>(c->d_scratch, c->d_nu, NN, c->d_red + 8);
+    DD_CUDA(cudaGetLastError());
+    unsigned long long nbad = 0;
+    double dl1 = 0;
+    DD_CUDA(cudaMemcpyAsync(&nbad, bad, 8, cudaMemcpyDeviceToHost, st));
+    DD_CUDA(cudaMemcpyAsync(&dl1, c->d_red + 8, 8, cudaMemcpyDeviceToHost, st));
+    DD_CUDA(cudaStreamSynchronize(st));
+    if (nbad || !(dl1 <= 1e-6 * snu)) {
+      c->err = "device-made initial coupling infeasible (" + std::to_string(nbad) + " cells, L1 = " +
+               std::to_string(dl1) + ")";
+      return DD_ERR_PRECOND;
+    }
+  } else {
     std::vector<double> pool((size_t)init_total);
     std::vector<long long> pos(I);
     long long at = 0;
@@ -401,6 +460,21 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c) 
   DD_CUDA(cudaStreamSynchronize(st));
   return DD_OK;
 }
+
+namespace dd {
+dd_status init_with_device_coupling(const dd_problem* P, const dd_options* O, const DevInit& dev, dd_ctx** out) {
+  *out = nullptr;
+  dd_ctx* c = new dd_ctx();
+  dd_status s = init_impl(P, O, c, &dev);
+  if (s != DD_OK) {
+    g_last_error = c->err;
+    free_ctx(c);
+    return s;
+  }
+  *out = c;
+  return DD_OK;
+}
+}  // namespace dd
 
 extern "C" {
 
@@ -446,7 +520,6 @@ dd_status domdec_sweep(dd_ctx* c, dd_partition part, dd_sweep_stats* stats) {
   p.pool_cap = c->pool_cap;
   p.scratch = c->d_scratch_huge;
   p.scratch_stride = c->scratch_stride;
-  p.ccap = c->ccap;
   p.alpha = c->d_alpha[b];
   p.gauge = c->d_gauge[b];
   p.alpha_valid = c->alpha_valid[b];
@@ -463,12 +536,10 @@ dd_status domdec_sweep(dd_ctx* c, dd_partition part, dd_sweep_stats* stats) {
   p.ecell = c->opt.track_primal ? c->d_ecell : nullptr;
   p.eps_p = c->eps_p;
   DD_CUDA(cudaMemsetAsync(c->d_totals[b], 0, sizeof(SweepTotals), c->stream));
-  const int mc = std::max(c->ncells[0], c->ncells[1]);
-  p.ovf_count = c->d_ovf;
-  p.ovf2_count = c->d_ovf + 1;
-  p.ovf_list = c->d_ovf + 8;
-  p.ovf2_list = c->d_ovf + 8 + mc;
-  DD_CUDA(launch_sweep(p, c->ccap, c->ccap_big, c->ccap_huge, c->stream));
+  p.cls_count = c->d_cls;
+  p.cls_fetch = c->d_cls + kClasses;
+  p.cls_list = c->d_cls + 16;
+  DD_CUDA(launch_sweep(p, c->cls, c->stream, c->aux, c->ev_fork, c->ev_join));
   c->cur = 1 - c->cur;
   ++c->n_sweeps;
   c->alpha_valid[b] = 1;
@@ -516,7 +587,13 @@ dd_status marginal_error(dd_ctx* c, double* l1_x, double* l1_y) {
   k_l1_diff<<<1, 1024, 0, c->stream>>>(c->d_scratch, c->d_nu, NN, c->d_red + 8);
   DD_CUDA(cudaGetLastError());
   DD_CUDA(cudaMemcpyAsync(&hy, c->d_red + 8, 8, cudaMemcpyDeviceToHost, c->stream));
+  unsigned long long invalid = 0;
+  DD_CUDA(cudaMemcpyAsync(&invalid, &c->d_cum->invalid, 8, cudaMemcpyDeviceToHost, c->stream));
   DD_CUDA(cudaStreamSynchronize(c->stream));
+  if (invalid) {
+    c->err = "marginal pool exhausted in an earlier sweep: the state is invalid";
+    return DD_ERR_NUMERIC;
+  }
   if (l1_x) *l1_x = hx;
   if (l1_y) *l1_y = hy;
   return DD_OK;
@@ -646,12 +723,37 @@ dd_status primal_dual_gap(dd_ctx* c, double* primal, double* dual, double* rel_g
   return pd_gap_impl(c, primal, dual, rel_gap, transport_cost);
 }
 
+dd_status domdec_export_cell_stats(dd_ctx* c, dd_partition part, int32_t* iters, double* e0, double* e,
+                                   int32_t* ncells) {
+  if (!c || (part != DD_PART_A && part != DD_PART_B)) return DD_ERR_ARG;
+  DD_CUDA(cudaSetDevice(c->device));
+  const int b = (int)part;
+  if (ncells) *ncells = c->ncells[b];
+  if (!(c->swept & (1 << b))) {
+    c->err = "partition never swept";
+    return DD_ERR_PRECOND;
+  }
+  std::vector<CellStats> h(c->ncells[b]);
+  DD_CUDA(cudaMemcpyAsync(h.data(), c->d_stats[b], h.size() * sizeof(CellStats), cudaMemcpyDeviceToHost, c->stream));
+  DD_CUDA(cudaStreamSynchronize(c->stream));
+  for (int k = 0; k < c->ncells[b]; ++k) {
+    if (iters) iters[k] = h[k].iters;
+    if (e0) e0[k] = (double)h[k].e0;
+    if (e) e[k] = (double)h[k].e;
+  }
+  return DD_OK;
+}
+
 dd_status domdec_counters(dd_ctx* c, dd_counters* out) {
   if (!c || !out) return DD_ERR_ARG;
   DD_CUDA(cudaSetDevice(c->device));
   SweepTotals t{};
   DD_CUDA(cudaMemcpyAsync(&t, c->d_cum, sizeof(t), cudaMemcpyDeviceToHost, c->stream));
   DD_CUDA(cudaStreamSynchronize(c->stream));
+  if (t.invalid) {
+    c->err = "marginal pool exhausted in an earlier sweep: the state is invalid";
+    return DD_ERR_NUMERIC;
+  }
   out->sweeps = c->n_sweeps;
   out->flow_updates = c->n_flows;
   out->cells = (int64_t)t.cells;
@@ -664,7 +766,8 @@ dd_status domdec_counters(dd_ctx* c, dd_counters* out) {
 dd_status domdec_reset_counters(dd_ctx* c) {
   if (!c) return DD_ERR_ARG;
   DD_CUDA(cudaSetDevice(c->device));
-  DD_CUDA(cudaMemsetAsync(c->d_cum, 0, sizeof(SweepTotals), c->stream));
+  // the invalid-state flag is sticky (not a counter)
+  DD_CUDA(cudaMemsetAsync(c->d_cum, 0, offsetof(SweepTotals, invalid), c->stream));
   c->n_sweeps = 0;
   c->n_flows = 0;
   return DD_OK;

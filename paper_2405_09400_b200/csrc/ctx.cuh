@@ -26,15 +26,15 @@ struct dd_ctx {
   long long* d_pos[2] = {nullptr, nullptr};          // [I] start of box i
   unsigned long long* d_poolctr = nullptr;           // [2] elements used per pool
   long long pool_cap = 0;                            // elements per pool
-  int ccap_huge = 0;
+  dd::SweepClasses cls{};                            // size classes (sweep.cu)
   unsigned char* d_scratch_huge = nullptr;           // global scratch of the huge class
   size_t scratch_stride = 0;
+  cudaStream_t aux = nullptr;                        // large size classes run here (fork/join)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int* d_off[2] = {nullptr, nullptr};
   int* d_ext[2] = {nullptr, nullptr};
   int cur = 0;
-  int ccap = 0;        // small size class (composite hull side)
-  int ccap_big = 0;    // large size class
-  int* d_ovf = nullptr; // [2 (counts) + 2 * max ncells] deferred-cell lists of the size classes
+  int* d_cls = nullptr; // [16 (counts, fetch counters) + kClasses * max ncells] size-class lists
   dd::CompCell* d_cells[2] = {nullptr, nullptr};
   int ncells[2] = {0, 0};
   std::vector<dd::CompCell> h_cells[2];
@@ -69,6 +69,18 @@ struct dd_ctx {
 };
 
 namespace dd {
+// Initial coupling already on the device (multiscale.cu): compact boxes with
+// their positions, plus host copies of off/ext for the capacity checks.
+struct DevInit {
+  const double* d_pool;
+  const long long* d_pos;
+  const int* d_off;
+  const int* d_ext;
+  long long total;        // pool entries used
+  const int* h_off;       // [I][2]
+  const int* h_ext;       // [I][2]
+};
+dd_status init_with_device_coupling(const dd_problem* P, const dd_options* O, const DevInit& dev, dd_ctx** out);
 dd_status flow_update_impl(dd_ctx* c, dd_flow_stats* stats);
 dd_status flow_costs_impl(dd_ctx* c);
 dd_status flow_apply_impl(dd_ctx* c);

@@ -269,11 +269,8 @@ static dd_status apply_w(dd_ctx* c, unsigned long long* d_counters, double* d_dr
   const int I = c->I;
   const int cur = c->cur, spare = 1 - c->cur;
   const size_t smem = (size_t)std::max(c->N1, c->N2) * 8;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
+  if (smem > 48 * 1024)   // per-device attribute: set on every launch
     DD_CUDA(cudaFuncSetAttribute(k_apply_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = smem;
-  }
   DD_CUDA(cudaMemsetAsync(c->d_poolctr + spare, 0, 8, c->stream));
   // owned rows only (stripe mode: their neighbours' rows must be current)
   (void)I;

@@ -6,7 +6,7 @@
 namespace dd {
 
 constexpr float kNeg = -1.0e30f;     // log of zero weight (reading R19), never NaN
-constexpr int kSweepThreads = 128;
+constexpr int kClasses = 5;          // size classes of the sweep (S, M, L, X, H)
 
 // One composite cell (Def. partitions).
 struct CompCell {
@@ -39,6 +39,8 @@ struct SweepTotals {
   double e0;
   double e;
   double dropped;
+  unsigned long long invalid;  // output pool exhausted: the state is invalid (sticky in the
+                               // cumulative totals, reported by every synchronising call)
 };
 
 struct SweepParams {
@@ -58,8 +60,7 @@ struct SweepParams {
   int* __restrict__ ext_out;
   unsigned long long* __restrict__ pool_ctr;   // bump allocator of pool_out (elements used)
   long long pool_cap;                 // capacity of pool_out (elements)
-  int ccap;                           // composite box side of the current size class
-  unsigned char* scratch;             // global scratch of the huge class (mode 2)
+  unsigned char* scratch;             // global scratch of the huge size class
   size_t scratch_stride;              // bytes per CTA
   float* __restrict__ alpha;          // [N1*N2] base-2 local-gauge potential of this partition
   int* __restrict__ gauge;            // [ncells][2] gauge origin used for alpha
@@ -72,14 +73,11 @@ struct SweepParams {
   CellStats* __restrict__ stats;
   SweepTotals* __restrict__ totals;
   SweepTotals* __restrict__ cum;      // cumulative over all sweeps (not reset)
-  int mode;                           // 0: one CTA per cell, defer cells with hull > ccap;
-                                      // 1: persistent CTAs over list 1 (large ccap, shared mem),
-                                      //    defer hulls > ccap to list 2;
-                                      // 2: persistent CTAs over list 2 (global-memory scratch)
-  int* __restrict__ ovf_list;         // [ncells] list 1
-  int* __restrict__ ovf_count;        // [1]
-  int* __restrict__ ovf2_list;        // [ncells] list 2
-  int* __restrict__ ovf2_count;       // [1]
+  // size classes: k_bin appends every composite
+  // cell to the list of the smallest class whose capacity holds its hull
+  int* __restrict__ cls_count;        // [kClasses] cells per class
+  int* __restrict__ cls_fetch;        // [kClasses] dynamic work counters
+  int* __restrict__ cls_list;         // [kClasses][ncells]
   double* __restrict__ mom;           // [I][6] plan moments of the last sweep (reading R13):
                                       // M0, M1 (2), G0, G1, M2 about the cell centre, px units
   const double* __restrict__ nu;      // [N1*N2] global nu (primal score only)
@@ -87,8 +85,15 @@ struct SweepParams {
   double eps_p;                       // eps' = eps / h^2
 };
 
-size_t sweep_smem_bytes(int ccap, int s);
-cudaError_t launch_sweep(SweepParams p, int ccap_small, int ccap_big, int ccap_huge, cudaStream_t st);
-size_t sweep_scratch_bytes(int ccap, int s);
+// Launch configuration of the size classes (host side, per context).
+struct SweepClasses {
+  int ccap[kClasses];      // hull side capacity of each class (ccap[H] = the grid)
+  int threads[kClasses];
+  int grid[kClasses];      // persistent CTAs per class
+  size_t smem[kClasses];   // dynamic shared memory per CTA (0 for H: global scratch)
+};
+cudaError_t sweep_classes(int s, int N, int nsm, int ncells, SweepClasses* out, size_t* scratch_stride);
+cudaError_t launch_sweep(const SweepParams& p, const SweepClasses& cls, cudaStream_t st, cudaStream_t aux,
+                         cudaEvent_t fork, cudaEvent_t join);
 
 }  // namespace dd

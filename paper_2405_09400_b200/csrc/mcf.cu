@@ -68,6 +68,15 @@ struct McfArgs {
   long long* wpS;         // [I] its prices (scaled costs)
   long long* wpT;         // [I]
   long long* wvalid;      // [1]
+  // stationarity certificate warm start: the labels of the last certificate
+  // that converged are a feasible potential d (d_j <= d_i + C_ij on every
+  // 4-neighbour arc).  If they still are for the new costs, the stationary
+  // flow is certified optimal in one pass; otherwise the Bellman-Ford starts
+  // from them (any finite start converges to a feasible potential iff there
+  // is no negative cycle), which near the optimum takes a few rounds instead
+  // of O(n1 + n2).
+  long long* certd;       // [I]
+  long long* cvalid;      // [1]
 };
 
 __device__ __forceinline__ int nbr(int i, int a, int n1, int n2) {
@@ -143,7 +152,7 @@ __device__ __noinline__ bool tiled_bf(const McfArgs& A, cg::grid_group& grid, co
       dS[i] = A.eS[i] < 0 ? 0 : kInf;
       dT[i] = A.eT[i] < 0 ? 0 : kInf;
     } else {
-      dS[i] = 0;
+      dS[i] = (mode == 2 && A.warm && *A.cvalid) ? A.certd[i] : 0;
       dT[i] = mode == 1 ? 0 : kInf;
     }
   }
@@ -534,6 +543,7 @@ __global__ void __launch_bounds__(512, 1) mcf_kernel(McfArgs A) {
 
   // ---- init: stationary flow, scaled costs, max |C| -------------------------
   const bool warm = A.warm && *A.wvalid;
+  const bool cwarm = A.warm && *A.cvalid;
   for (long long i = gt; i < I; i += gs) {
     for (int a = 0; a < 5; ++a) {
       const int j = nbr((int)i, a, n1, n2);
@@ -544,6 +554,7 @@ __global__ void __launch_bounds__(512, 1) mcf_kernel(McfArgs A) {
         const unsigned long long ab = (unsigned long long)(c < 0 ? -c : c);
         atomicMax(&A.ctr[0], ab);
         if (c < 0) atomicAdd(&A.ctr[1], 1ull);
+        if (cwarm && c + A.certd[i] - A.certd[j] < 0) atomicAdd(&A.ctr[2], 1ull);
       }
     }
     A.dist[0][i] = 0;
@@ -555,11 +566,21 @@ __global__ void __launch_bounds__(512, 1) mcf_kernel(McfArgs A) {
     A.addT[i] = 0;
   }
   grid.sync();
-  const bool any_negative = A.ctr[1] > 0;
-  if (!any_negative) {
+  // The stationary flow (w_ii = q_i) is the result of every early exit: A.w
+  // holds the warm flow at this point and must not be applied again.
+  auto stationary_exit = [&](int bf_rounds) {
+    for (long long i = gt; i < I; i += gs)
+      for (int a = 0; a < 5; ++a) A.w[5 * i + a] = (a == 0) ? A.q[i] : 0;
     if (gt == 0) {
-      A.info[0] = 0; A.info[1] = 1; A.info[2] = 1; A.info[3] = 0; A.info[4] = 0;
+      A.info[0] = 0; A.info[1] = 1; A.info[2] = 1; A.info[3] = 0; A.info[4] = 0; A.info[5] = bf_rounds;
+      A.info[6] = 0; A.info[12] = (long long)(gtimer() - tm_start);
     }
+  };
+  const bool any_negative = A.ctr[1] > 0;
+  // no negative arc cost, or the last certificate's labels are still a
+  // feasible potential: no negative cycle, the stationary flow is optimal
+  if (!any_negative || (cwarm && A.ctr[2] == 0)) {
+    stationary_exit(0);
     return;
   }
   // ---- Bellman-Ford certificate on (I, 4-nbr arcs, C) -----------------------
@@ -573,7 +594,11 @@ __global__ void __launch_bounds__(512, 1) mcf_kernel(McfArgs A) {
   const int cert_cap = warm ? (A.bf_rounds < 64 ? A.bf_rounds : 64) : A.bf_rounds;
   const int cert = tiled_bf(A, grid, 2, 0, 0, cert_cap, gt, gs, &rb) ? 1 : 0;
   if (cert) {
-    if (gt == 0) { A.info[0] = 0; A.info[1] = 1; A.info[2] = 1; A.info[3] = 0; A.info[4] = 0; A.info[5] = rb; }
+    if (A.warm) {   // keep the labels (a feasible potential) for the next certificate
+      for (long long i = gt; i < I; i += gs) A.certd[i] = A.dist[0][i];
+      if (gt == 0) *A.cvalid = 1;
+    }
+    stationary_exit(rb);
     return;
   }
   // ---- cost scaling -----------------------------------------------------------
@@ -847,7 +872,7 @@ static size_t ws_size(int I) {
   // cs, w handled by caller for w; workspace: cs[5I] eS eT addS addT pS0 pS1 pT0 pT1 d0 d1 ctr[16],
   // info[16], warm state wW[5I] wpS[I] wpT[I] wvalid
   return sizeof(long long) * (5ull * I + 12ull * I) + 16 * sizeof(unsigned long long) + 16 * sizeof(long long) +
-         sizeof(long long) * (7ull * I + 1) + 256;
+         sizeof(long long) * (7ull * I + 1) + sizeof(long long) * (I + 1) + 256;
 }
 
 dd_status mcf_solve_device(int n1, int n2, const int64_t* d_q, const int64_t* d_C, int64_t* d_w, void** d_ws,
@@ -894,7 +919,9 @@ dd_status mcf_solve_device(int n1, int n2, const int64_t* d_q, const int64_t* d_
   A.wW = p; p += 5LL * I;
   A.wpS = p; p += I;
   A.wpT = p; p += I;
-  A.wvalid = p;
+  A.wvalid = p; p += 1;
+  A.certd = p; p += I;
+  A.cvalid = p;
   A.warm = warm;
   A.warm_div = 1LL << 40;   // warm start: one eps = 1 phase (tools/mcf_sim.cpp: 3x fewer rounds than cold)
   if (const char* env = getenv("DD_MCF_WDIV")) A.warm_div = atoll(env) > 0 ? atoll(env) : A.warm_div;
@@ -926,12 +953,9 @@ dd_status mcf_solve_device(int n1, int n2, const int64_t* d_q, const int64_t* d_
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   // one CTA per SM at most: grid barriers get cheaper with fewer CTAs
   const int threads = 512;
-  static bool smem_set = false;
-  if (!smem_set) {
-    e = cudaFuncSetAttribute(mcf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmemBytes);
-    if (e != cudaSuccess) { err = std::string("mcf smem: ") + cudaGetErrorString(e); return DD_ERR_CUDA; }
-    smem_set = true;
-  }
+  // per-device function attribute: set on every launch (cheap)
+  e = cudaFuncSetAttribute(mcf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmemBytes);
+  if (e != cudaSuccess) { err = std::string("mcf smem: ") + cudaGetErrorString(e); return DD_ERR_CUDA; }
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mcf_kernel, threads, kTileSmemBytes);
   if (per <= 0) { err = "mcf kernel cannot be resident"; return DD_ERR_CUDA; }
   long long want = (I + threads - 1) / threads;

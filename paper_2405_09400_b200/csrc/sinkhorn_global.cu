@@ -42,15 +42,16 @@ __global__ void k_sg_prep(const double* __restrict__ p, const double* __restrict
 // fp64 word's low 9 exponent bits and top 23 mantissa bits are funnel-shifted
 // into place and the exponent rebased (E_f = E_d - 896 == low9 + 128 mod 512);
 // mantissa truncated (<= 1 float ulp); sign copied.  |v| < 2^-126 gives 0
-// (2^v = 1 to fp32 precision); |v| >= 256 gives -256 (2^v = 0 for v < 0; a
-// positive v that large overflows the shifted sum, which then falls back to
-// the max pass).  Integer ops only.
+// (2^v = 1 to fp32 precision); |v| >= 256 gives -256 for v < 0 (2^v = 0) and
+// +256 for v > 0 (2^256 overflows to +inf, so the shifted sum leaves
+// [2^-60, 2^60] and that output falls back to the max pass: a stale shift
+// never silently drops a dominant term).  Integer ops only.
 __device__ __forceinline__ float sg_d2f(double v) {
   const unsigned hi = (unsigned)__double2hiint(v), lo = (unsigned)__double2loint(v);
   const unsigned e = hi & 0x7ff00000u;
   const unsigned bits = (__funnelshift_l(lo, hi, 3) + (128u << 23)) | (hi & 0x80000000u);
   const float f = e < (897u << 20) ? 0.f : __uint_as_float(bits);
-  return e >= (1031u << 20) ? -256.f : f;
+  return e >= (1031u << 20) ? ((hi & 0x80000000u) ? -256.f : 256.f) : f;
 }
 
 __device__ __forceinline__ float sg_ex2(float x) {

@@ -1,0 +1,60 @@
+// sweep_launch.cuh — per-cell-size launch templates of the sweep (instantiated
+// once per cell size in sweep_s*.cu so the translation units compile in
+// parallel).  See sweep.cu for the size-class design.
+#pragma once
+#include "sweep.cuh"
+
+namespace dd {
+
+constexpr int kClassThreads[kClasses] = {128, 256, 512, 512, 512};
+constexpr int kClassMinBlocks[kClasses] = {7, 3, 2, 1, 1};
+
+template <int NX, int C, bool PR>
+cudaError_t launch_class(const SweepParams& p, const SweepClasses& cls, cudaStream_t st) {
+  constexpr bool GS = C == 4;
+  auto kern = sweep_kernel<NX, kClassThreads[C], kClassMinBlocks[C], PR, GS>;
+  if (cls.smem[C] > 48 * 1024) {   // per-device attribute: set on every launch (cheap)
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cls.smem[C]);
+    if (e != cudaSuccess) return e;
+  }
+  kern<<<cls.grid[C], kClassThreads[C], cls.smem[C], st>>>(p, C, cls.ccap[C]);
+  return cudaGetLastError();
+}
+
+template <int NX, bool PR>
+cudaError_t launch_all(const SweepParams& p, const SweepClasses& cls, cudaStream_t st, cudaStream_t aux) {
+  cudaError_t e;
+  // large classes on the auxiliary stream (biggest first), the bulk on the main one
+  if ((e = launch_class<NX, 4, PR>(p, cls, aux)) != cudaSuccess) return e;
+  if ((e = launch_class<NX, 3, PR>(p, cls, aux)) != cudaSuccess) return e;
+  if ((e = launch_class<NX, 2, PR>(p, cls, aux)) != cudaSuccess) return e;
+  if ((e = launch_class<NX, 1, PR>(p, cls, aux)) != cudaSuccess) return e;
+  return launch_class<NX, 0, PR>(p, cls, st);
+}
+
+template <int NX>
+cudaError_t launch_sweep_nx(const SweepParams& p, const SweepClasses& cls, cudaStream_t st, cudaStream_t aux) {
+  return p.ecell ? launch_all<NX, true>(p, cls, st, aux) : launch_all<NX, false>(p, cls, st, aux);
+}
+
+template <int NX, int C>
+int occupancy_of(size_t smem) {
+  auto kern = sweep_kernel<NX, kClassThreads[C], kClassMinBlocks[C], false, false>;
+  if (smem > 48 * 1024 &&   // the query counts 0 CTAs above the opt-in limit
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return -1;
+  int per = 0;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kClassThreads[C], smem) == cudaSuccess ? per : -1;
+}
+
+template <int NX>
+int sweep_occupancy_nx(int C, size_t smem) {
+  switch (C) {
+    case 0: return occupancy_of<NX, 0>(smem);
+    case 1: return occupancy_of<NX, 1>(smem);
+    case 2: return occupancy_of<NX, 2>(smem);
+    default: return occupancy_of<NX, 3>(smem);
+  }
+}
+
+}  // namespace dd

@@ -1,0 +1,84 @@
+"""GPU parity of the multiscale path (readings R23-R25):
+the product-coupling init and the refinement kernels against the oracle
+(bit-exact: same fp64 operations in the same order), and the whole
+coarse-to-fine hybrid solve against the oracle and the dense optimum."""
+import numpy as np
+import pytest
+
+import oracle as O
+from oracle import multiscale as M
+from parity import compare_states
+from synth import make_problem
+
+gpu = pytest.mark.gpu
+
+
+def _assert_boxes_identical(gb, ob):
+    assert len(gb) == len(ob)
+    for i, ((r0, c0, d), (s0, t0, e)) in enumerate(zip(gb, ob)):
+        assert (r0, c0, d.shape) == (s0, t0, e.shape), i
+        assert np.array_equal(d, e), i
+
+
+@gpu
+@pytest.mark.parametrize("N,s", [(16, 2), (32, 4)])
+def test_product_init_bit_exact(N, s):
+    from paper_2405_09400_b200 import DomDec
+    p = make_problem("gm", N, s, theta_deg=20, seed=1)
+    dd = DomDec.product(p.mu, p.nu, s, p.eps, p.h, p.E)
+    st = M.product_state(p.mu, p.nu, s, p.eps_prime, p.h)
+    _assert_boxes_identical(dd.boxes(), st.boxes)
+    dd.close()
+
+
+@gpu
+@pytest.mark.parametrize("N,s", [(32, 2), (64, 4)])
+def test_refine_bit_exact(N, s):
+    """A coarse GPU state after a few sweeps (exported, so both sides refine
+    the same coarse marginals) refined on the GPU and by the oracle: boxes
+    and values identical."""
+    from paper_2405_09400_b200 import DomDec
+    p = make_problem("gm", N, s, theta_deg=20, seed=2)
+    mu_c, nu_c = M.coarsen(p.mu), M.coarsen(p.nu)
+    hc = 2.0 / mu_c.shape[0]
+    coarse = DomDec.product(mu_c, nu_c, s, p.eps_prime * hc * hc, hc, p.E)
+    for part in ("A", "B", "A"):
+        coarse.sweep(part)
+    stc = M.product_state(mu_c, nu_c, s, p.eps_prime, hc)
+    stc.boxes = [[r0, c0, d.copy()] for r0, c0, d in coarse.boxes()]
+    stf = M.refine_state(stc, p.mu, p.nu)
+    fine = coarse.refine(p.mu, p.nu, p.eps, p.E)
+    _assert_boxes_identical(fine.boxes(), stf.boxes)
+    ex, ey = fine.marginal_error()
+    assert ey < 1e-12
+    with pytest.raises(Exception):   # the fine measures must coarsen to the coarse ones (R23)
+        coarse.refine(p.mu, np.roll(p.nu, 1, axis=0), p.eps, p.E)
+    fine.close()
+    coarse.close()
+
+
+@gpu
+def test_multiscale_matches_oracle_and_dense_optimum():
+    """dd_multiscale_solve on a 32^2 GM pair (layers 16^2, 32^2; s = 2;
+    eps' = 4; hybrid with flow updates) in tolerance mode against the oracle's
+    multiscale_solve: both converge (R14 at 1e-6), their transport costs
+    agree to 1e-5 relative and both are within 1e-4 of the dense global
+    optimum."""
+    from paper_2405_09400_b200 import multiscale_solve
+    p = make_problem("gm", 32, 2, theta_deg=20, seed=0)
+    dd, stats = multiscale_solve(p.mu, p.nu, 2, p.eps, p.E, levels=2, conv=1e-6, max_cycles=300, err=1e-6)
+    assert all(stats["converged"]), stats
+    st, hist = M.multiscale_solve(p.mu, p.nu, 2, p.eps_prime, levels=2, E=p.E, err=1e-6, conv=1e-6,
+                                  max_cycles=300)
+    assert all(r["converged"] for r in hist), hist
+    gc = float(np.sum(dd.export_plan_cost())) * p.h * p.h
+    oc = O.transport_cost(st)
+    assert abs(gc - oc) < 1e-5 * oc, (gc, oc)
+    plan, a, b, xs, ys = O.dense_sinkhorn(p.mu, p.nu, p.eps_prime, tol=1e-12)
+    from oracle.sinkhorn import sqdist
+    N = p.N
+    cstar = float(np.sum(sqdist(np.stack([xs // N, xs % N], 1), np.stack([ys // N, ys % N], 1)) * plan)) * p.h ** 2
+    assert abs(gc - cstar) < 1e-4 * cstar, (gc, cstar)
+    ex, ey = dd.marginal_error()
+    assert ey < 1e-8
+    dd.close()

@@ -49,6 +49,25 @@ def test_global_sinkhorn_parity_fixed_iterations(shape, eps_p, zero_frac):
 
 
 @gpu
+def test_global_sinkhorn_stale_shift_warm_start():
+    """from the second iteration each LSE output is shifted by its
+    previous value; after a wild warm start the shift is stale by
+    hundreds of log units, and a term far above it must overflow the shifted
+    sum into the max-pass fallback, never be dropped.  GPU vs the oracle's
+    dense Sinkhorn from the same initial potential."""
+    from paper_2405_09400_b200 import sinkhorn_global
+    p = make_problem("gm", 32, 2, theta_deg=20.0, seed=5)
+    rng = np.random.default_rng(7)
+    a0 = rng.normal(0.0, 500.0, p.mu.shape)
+    K = 6
+    a, b, it, e, ms = sinkhorn_global(p.mu, p.nu, p.eps_prime, err=0.0, max_iter=K, check_every=K, alpha0=a0)
+    plan, ao, bo, xs, ys = O.dense_sinkhorn(p.mu, p.nu, p.eps_prime, tol=0.0, max_iter=K, a0=a0)
+    scale = 1.0 + np.max(np.abs(ao))
+    assert np.max(np.abs(a.ravel()[xs] - ao)) <= 2e-5 * scale
+    assert np.max(np.abs(b.ravel()[ys] - bo)) <= 2e-5 * scale
+
+
+@gpu
 def test_global_sinkhorn_parity_gm_problem():
     p = make_problem("gm", 32, 2, theta_deg=20.0, seed=1)
     _compare(p.mu, p.nu, p.eps_prime, K=20)
