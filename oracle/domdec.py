@@ -222,7 +222,8 @@ def domdec_sweep(st: OracleState, kind: str, err: float = 1e-4, fixed_iter: int 
         if sample_mode:
             results[k] = {"boxes": cell_out, "a": a, "R": R, "C": Cc, "L": (L1, L2), "nuJ": nuJ,
                           "iters": it, "e0": e0, "e": e,
-                          "Q": {i: Q[i] for i in members}}
+                          "Q": {i: Q[i] for i in members}, "nu_pre": {i: nu_pre[i] for i in members},
+                          "PX": plan.sum(axis=1)}
     if sample_mode:
         return results
     st.boxes = new_boxes

@@ -35,7 +35,7 @@ def neighbour(i: int, a: int, n1: int, n2: int) -> int:
     return -1
 
 
-def edge_costs(st, Q=None, nus=None):
+def edge_costs(st, Q=None, nus=None, cells=None):
     """c_bar (I x 5, px^2 units, NaN for arcs leaving the grid), c_bar_ii = 0.
     For i != j, with the product candidate:
         c_bar_ij = (1/m_i) sum_{x in X_j} sum_y |x - y|^2 (mu(x)/m_j) nu_i(y) - Q_i
@@ -44,7 +44,7 @@ def edge_costs(st, Q=None, nus=None):
     (reading R13: the paper instantiates pi_i for this step).
     Direct double sums over pixels (no moment shortcut).  Q and nus (list of
     (r0, c0, array)) may be given explicitly; by default both come from
-    st.last."""
+    st.last.  cells: optional subset of source cells i (other rows stay NaN)."""
     if Q is None:
         Q = st.last["Q"]
         if nus is None:
@@ -54,7 +54,7 @@ def edge_costs(st, Q=None, nus=None):
     n1, n2, s = st.n1, st.n2, st.s
     I = n1 * n2
     cbar = np.full((I, 5), np.nan)
-    for i in range(I):
+    for i in (range(I) if cells is None else cells):
         r0, c0, d = nus[i]
         yr, yc = np.nonzero(d > 0)
         vals = d[yr, yc]
@@ -73,6 +73,97 @@ def edge_costs(st, Q=None, nus=None):
             d2 = (xr[:, None] - Y1[None, :]) ** 2 + (xc[:, None] - Y2[None, :]) ** 2
             tot = float(np.sum(d2 * mux[:, None] * vals[None, :]))
             cbar[i, a] = tot / (st.m[i] * st.m[j]) - Q[i]
+    return cbar
+
+
+def gamma_conditional(st, i: int, j: int, eps_gamma_p: float, tol: float = 1e-12, max_iter: int = 200000):
+    """The plan gamma_ij in Pi(mu_i/m_i, mu_j/m_j) of a gluing edge candidate
+    (Def. glued-plan): the optimal entropic plan for the cost
+    |x - x'|^2 with regularisation eps_gamma_p (pixel^2 units; Remark
+    eps-gamma PAPER.md:543-559: eps -> inf gives the product coupling, eps -> 0
+    an optimal plan), by dense log-domain Sinkhorn (with eps-scaling) to an L1
+    marginal error <= tol.  Returned as its disintegration against the first marginal,
+    gamma~(x' | x) = gamma(x, x') / (mu(x) / m_i) (rows x in X_i, columns
+    x' in X_j, both row-major), and the pixel coordinates of X_i and X_j."""
+    s, n2 = st.s, st.n2
+    from .partitions import cell_pixels
+    from .sinkhorn import lse, sqdist
+    ri, ci = cell_pixels(i, n2, s)
+    rj, cj = cell_pixels(j, n2, s)
+    xi = np.stack([ri, ci], 1).astype(np.float64)
+    xj = np.stack([rj, cj], 1).astype(np.float64)
+    pa = st.mu[ri, ci] / st.m[i]
+    pb = st.mu[rj, cj] / st.m[j]
+    Cm = sqdist(xi, xj) / eps_gamma_p
+    la, lb = np.log(pa), np.log(pb)
+    D = sqdist(xi, xj)
+    # eps-scaling (a standard device for small eps, whose plain Sinkhorn
+    # iteration contracts like 1 - exp(-max c / eps)): halve eps from max c
+    # down to eps_gamma_p, warm-starting the potentials (in units of the
+    # current eps, rescaled at each stage), then iterate to tol
+    eps_stages = []
+    e = max(float(D.max()), eps_gamma_p)
+    while e > eps_gamma_p:
+        eps_stages.append(e)
+        e /= 2.0
+    eps_stages.append(eps_gamma_p)
+    a = np.zeros(len(pa))
+    b = np.zeros(len(pb))
+    prev = eps_stages[0]
+    for k, e in enumerate(eps_stages):
+        a *= prev / e
+        b *= prev / e
+        prev = e
+        Cm = D / e
+        last = k == len(eps_stages) - 1
+        for _ in range(max_iter if last else 200):
+            b = -lse(a[:, None] + la[:, None] - Cm, axis=0)
+            a = -lse(b[None, :] + lb[None, :] - Cm, axis=1)
+            if last:
+                g = np.exp(a[:, None] + b[None, :] - Cm + la[:, None] + lb[None, :])
+                if np.abs(g.sum(axis=0) - pb).sum() <= tol:
+                    break
+    g = np.exp(a[:, None] + b[None, :] - Cm + la[:, None] + lb[None, :])
+    return g / g.sum(axis=1, keepdims=True), xi, xj
+
+
+def glued_edge_costs(st, eps_gamma_p: float):
+    """c_bar (I x 5, px^2) with gluing edge candidates (Def. glued-plan,
+    PAPER.md:531-541) built from entropic plans gamma_ij
+    (gamma_conditional) and the last sweep's plans pi_i (keep_plans=True):
+        pi_hat_ij(x', y) = (1/m_i) sum_{x in X_i} gamma~(x' | x) pi_i(x, y),
+        c_bar_ij = <c, pi_hat_ij> - <c, pi_i>/m_i
+                 = (1/m_i) sum_x sum_x' sum_y gamma~(x'|x) pi_i(x,y) (|x'-y|^2 - |x-y|^2)
+    by direct sums (reading R26: pi_i enters as is; its X-marginal is mu_i up
+    to the Sinkhorn tolerance, the case in which this is exactly Eq.
+    glued-plan).  c_bar_ii = 0; NaN on arcs leaving the grid."""
+    from .partitions import composite_partition
+    from .sinkhorn import sqdist
+    plans = st.last.get("plans")
+    if not plans:
+        raise ValueError("glued_edge_costs needs the last sweep's plans (keep_plans=True)")
+    n1, n2 = st.n1, st.n2
+    I = n1 * n2
+    cbar = np.full((I, 5), np.nan)
+    comp = composite_partition(n1, n2, st.last["kind"])
+    for k, members in enumerate(comp):
+        R, Cc, ly, a, b, plan = plans[k]
+        cell_of = (R // st.s) * n2 + (Cc // st.s)
+        ly = np.asarray(ly, np.float64)
+        for i in members:
+            sel = cell_of == i
+            P = plan[sel]                                   # pi_i(x, y), rows in X_i row-major
+            X = np.stack([R[sel], Cc[sel]], 1).astype(np.float64)
+            own = float(np.sum(P * sqdist(X, ly)))           # <c, pi_i> in px^2
+            cbar[i, 0] = 0.0
+            for aa in range(1, 5):
+                j = neighbour(i, aa, n1, n2)
+                if j < 0:
+                    continue
+                gt, xi, xj = gamma_conditional(st, i, j, eps_gamma_p)
+                assert np.array_equal(xi, X)
+                M = P @ sqdist(xj, ly).T                    # sum_y pi(x, y) |x' - y|^2
+                cbar[i, aa] = (float(np.sum(gt * M)) - own) / st.m[i]
     return cbar
 
 
