@@ -8,14 +8,19 @@ one hybrid cycle of Alg. 3: sweep A, sweep B, flow update
 — every row of SURVEY §8(a).  The metric is domdec sweeps/s (two sweeps per
 step; flow updates take no trajectory time).
 
-Multi-GPU (torchrun): one independent problem per rank (GM seed = rank; the
-paper's benchmark is a set of independent pairs), weak
-scaling; the only collectives are the barrier/max-time reductions of the
-timing protocol and the per-cycle L1-error allreduce of the convergence
-check.
+Multi-GPU (torchrun, N > 1): by default ONE problem sharded in row stripes
+over the ranks (stripes.py: halo rows over NCCL, the flow
+instance all-gathered as a device tensor, replicated warm-started exact
+min-cost flow) — strong scaling; --parallelism independent runs one problem
+per rank (weak scaling).
+
+Also reported: time to L1 marginal error 1e-4 (reading R14) single-scale and
+multiscale (dd_multiscale_solve), the eps sweep of config 3,
+config 5 sweeps, the SinkhornGPU comparator, the sweep roofline (MUFU) and
+the fp64 CPU oracle on all host cores (cpu_baseline).
 
 --impl reference times the fp64 CPU oracle (the reference arm of this tier)
-on bounded samples of the same workload.
+on bounded samples of the same workload, on all host cores.
 """
 from __future__ import annotations
 
@@ -44,14 +49,18 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--N", type=int, default=CFG["N"])
     ap.add_argument("--s", type=int, default=CFG["s"])
-    ap.add_argument("--no-ttc", action="store_true", help="skip the time-to-1e-4 run")
-    ap.add_argument("--ttc-cycles", type=int, default=3000)
-    ap.add_argument("--ttc-seconds", type=float, default=150.0)
+    ap.add_argument("--no-ttc", action="store_true", help="skip the time-to-1e-4 runs")
+    ap.add_argument("--ttc-cycles", type=int, default=6000)
+    ap.add_argument("--ttc-seconds", type=float, default=90.0)
+    ap.add_argument("--ttc-flow-every", type=int, default=8,
+                    help="flow period k of the single-scale 1024^2 time-to-1e-4 run (PAPER.md:750)")
+    ap.add_argument("--no-extra", action="store_true", help="skip the eps-sweep / config-5 keys")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--parallelism", default="independent", choices=["independent", "stripes"],
-                    help="N>1: one problem per rank (weak scaling, default) or one problem in row stripes "
-                         "(strong scaling, SURVEY 8(e); the min-cost flow is replicated)")
+    ap.add_argument("--cpu-seconds", type=float, default=30.0, help="LP time cap of the CPU oracle cycle")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--parallelism", default="auto", choices=["auto", "independent", "stripes"],
+                    help="N>1: one problem in row stripes (default, strong scaling, SURVEY 8(e)) or one "
+                         "independent problem per rank (weak scaling)")
     return ap.parse_args()
 
 
@@ -62,9 +71,10 @@ def dist_env():
     return world, rank, local
 
 
-def make(seed, N, s):
+def make(seed, N, s, theta=None, eps_factor=None):
     from synth import make_problem
-    return make_problem("gm", N, s, eps_factor=CFG["eps_factor"], theta_deg=CFG["theta"], seed=seed)
+    return make_problem("gm", N, s, eps_factor=CFG["eps_factor"] if eps_factor is None else eps_factor,
+                        theta_deg=CFG["theta"] if theta is None else theta, seed=seed)
 
 
 class ClockSampler:
@@ -114,59 +124,181 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_baseline(p, seconds):
-    """The fp64 oracle as it stands (tests' reference implementation) on a
-    bounded sample of the same workload: composite cells of the first A sweep
-    of the same problem, processed one by one until `seconds` elapse."""
+# ---------------------------------------------------------------------------
+# CPU oracle on all host cores (cpu_baseline / the reference arm)
+
+_ORACLE_ST = None     # set in the parent before forking the worker pool
+
+
+def _oracle_cells(args):
+    """Worker: the oracle's sweep on a chunk of composite cells (sample mode:
+    the shared state is not modified)."""
     import oracle as O
+    part, cells = args
+    res = O.domdec_sweep(_ORACLE_ST, part, err=1e-4, cells=list(cells))
+    return {k: {"boxes": v["boxes"], "a": v["a"], "R": v["R"], "C": v["C"], "Q": v["Q"], "nu_pre": v["nu_pre"]}
+            for k, v in res.items()}
+
+
+def _oracle_edges(cells):
+    import oracle as O
+    return cells, O.edge_costs(_ORACLE_ST, cells=list(cells))[list(cells)]
+
+
+def host_info():
+    model = ""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        model = next((ln.split(":", 1)[1].strip() for ln in out.splitlines() if ln.startswith("Model name")), "")
+    except Exception:
+        pass
+    return os.cpu_count() or 1, model
+
+
+def oracle_cycle_all_cores(p, lp_cap_s, sample_cells=None):
+    """One hybrid cycle of the fp64 oracle (oracle/, as it stands) at the
+    bench workload on all host cores: sweeps A and B (composite cells in
+    parallel worker processes; the whole partition, or a random sample of
+    `sample_cells` cells extrapolated), edge costs (cells in parallel), the
+    exact min-cost flow (HiGHS LP, single-threaded, time-capped: a capped
+    solve makes the cycle time a lower bound).  Returns a dict."""
+    global _ORACLE_ST
+    import multiprocessing as mp
+
+    import oracle as O
+    cores, model = host_info()
     st = O.init_state(p.mu, p.nu, p.s, p.eps_prime, p.h, p.init_off, p.init_ext, p.init_pos, p.init_data)
-    ncomp = len(O.composite_partition(st.n1, st.n2, "A"))
-    rng = np.random.default_rng(0)
-    order = rng.permutation(ncomp)
-    done = 0
+    ctx = mp.get_context("fork")
+    t_sweep = {}
+    sampled = sample_cells is not None
+    for part in ("A", "B"):
+        comp = O.composite_partition(st.n1, st.n2, part)
+        idx = np.arange(len(comp))
+        if sampled:
+            idx = np.random.default_rng(1).choice(len(comp), min(sample_cells, len(comp)), replace=False)
+        chunks = [c for c in np.array_split(idx, max(1, cores * 8)) if len(c)]
+        _ORACLE_ST = st
+        t0 = time.perf_counter()
+        with ctx.Pool(cores) as pool:
+            outs = pool.map(_oracle_cells, [(part, c.tolist()) for c in chunks])
+        dt = time.perf_counter() - t0
+        t_sweep[part] = dt * len(comp) / len(idx)
+        if not sampled:   # assemble the new state (the sweep's outputs)
+            Q = np.zeros(st.n1 * st.n2)
+            nu_pre = [None] * (st.n1 * st.n2)
+            alpha = np.zeros((st.N1, st.N2)) if st.alpha[part] is None else st.alpha[part].copy()
+            for o in outs:
+                for k, v in o.items():
+                    for i, b in v["boxes"].items():
+                        st.boxes[i] = [b[0], b[1], b[2]]
+                        Q[i] = v["Q"][i]
+                        nu_pre[i] = v["nu_pre"][i]
+                    alpha[v["R"], v["C"]] = v["a"]
+            st.alpha[part] = alpha
+            st.last = {"kind": part, "Q": Q, "nu_pre": nu_pre}
+    res = {"cores": cores, "cpu_model": model, "sweep_A_s": t_sweep["A"], "sweep_B_s": t_sweep["B"]}
+    if sampled:
+        return res
+    I = st.n1 * st.n2
+    _ORACLE_ST = st
     t0 = time.perf_counter()
-    while time.perf_counter() - t0 < seconds and done < ncomp:
-        O.domdec_sweep(st, "A", err=1e-4, cells=[int(x) for x in order[done:done + 8]])
-        done += 8
-    dt = time.perf_counter() - t0
-    return {"value": done / dt / ncomp, "unit": "sweeps/s", "cores": 1, "kind": "oracle",
-            "sample": f"{done} of {ncomp} composite cells of the first A sweep of GM(0) {p.N}^2 s={p.s} "
-                      f"(fp64 dense log-domain Sinkhorn, Err=1e-4), {dt:.1f} s, extrapolated to one sweep"}
+    with ctx.Pool(cores) as pool:
+        outs = pool.map(_oracle_edges, [c.tolist() for c in np.array_split(np.arange(I), cores * 8)])
+    cbar = np.full((I, 5), np.nan)
+    for cells, rows in outs:
+        cbar[cells] = rows
+    res["edge_costs_s"] = time.perf_counter() - t0
+    C, q = O.integer_instance(cbar, p.supplies())
+    # the exact min-cost flow: the oracle's HiGHS LP (oracle.flow.min_cost_flow
+    # as it stands), in a child process so that the time cap can stop it
+    t0 = time.perf_counter()
+    proc = ctx.Process(target=O.min_cost_flow, args=(q, C, st.n1, st.n2))
+    proc.start()
+    proc.join(lp_cap_s)
+    capped = proc.is_alive()
+    if capped:
+        proc.terminate()
+        proc.join()
+    res["mincost_flow_s"] = time.perf_counter() - t0
+    res["mincost_flow_capped"] = capped
+    res["cycle_s"] = t_sweep["A"] + t_sweep["B"] + res["edge_costs_s"] + res["mincost_flow_s"]
+    return res
 
 
-def bench_config(a, world):
-    """The workload both arms report (the reference arm adds its sample)."""
+def cpu_baseline(p, lp_cap_s):
+    r = oracle_cycle_all_cores(p, lp_cap_s)
+    return {"value": 2.0 / r["cycle_s"], "unit": "sweeps/s", "cores": r["cores"], "kind": "oracle",
+            "value_is_upper_bound": bool(r["mincost_flow_capped"]),
+            "sample": (f"one full hybrid cycle of the fp64 oracle at {p.N}^2 s={p.s} eps=(2h)^2 GM(0)+T_20 on all "
+                       f"{r['cores']} host cores ({r['cpu_model']}): sweep A {r['sweep_A_s']:.1f} s, sweep B "
+                       f"{r['sweep_B_s']:.1f} s (composite cells in parallel processes), edge costs "
+                       f"{r['edge_costs_s']:.1f} s, exact min-cost flow (HiGHS LP, 1 thread) "
+                       f"{r['mincost_flow_s']:.1f} s" + (" (stopped at the cap: a lower bound)"
+                                                          if r["mincost_flow_capped"] else "")),
+            "breakdown": r}
+
+
+def bench_config(a, world, parallelism):
     return {"workload": f"GM(rank) {a.N}x{a.N} -> {a.N}x{a.N}, s={a.s}, eps=(2h)^2, theta=20deg; "
                         "step = hybrid cycle (sweep A, sweep B, flow update)",
-            "grid": a.N, "cell_size": a.s, "eps": "(2h)^2", "parallelism": f"independent problems x{world}",
+            "grid": a.N, "cell_size": a.s, "eps": "(2h)^2",
+            "parallelism": (f"row stripes x{world}" if parallelism == "stripes" else f"independent problems x{world}"),
             "l2": "flushed between timed steps (256 MB write)",
             "precision": "log-domain fp32 (local gauge), marginals fp64"}
 
 
 def run_reference(a):
+    """Reference arm: the fp64 oracle on all host cores; each step times the
+    oracle's two sweeps of the hybrid cycle on a bounded random sample of the
+    composite cells (extrapolated to the partition).  The oracle's flow
+    update is not part of these steps (its exact LP alone takes tens of
+    seconds at 1024^2, see cpu_baseline of the main line), so the value is an
+    upper bound of the oracle's hybrid-cycle sweeps/s."""
     world, rank, local = dist_env()
     if rank != 0:
         return
     p = make(0, a.N, a.s)
-    per = max(1.0, a.cpu_seconds / max(1, a.steps + a.warmup))
+    sample = 1024
     for _ in range(a.warmup):
-        cpu_baseline(p, per / 4)
+        oracle_cycle_all_cores(p, 0, sample_cells=256)
     vals = []
     t0 = time.perf_counter()
+    r = None
     for _ in range(a.steps):
-        vals.append(cpu_baseline(p, per))
+        r = oracle_cycle_all_cores(p, 0, sample_cells=sample)
+        vals.append(2.0 / (r["sweep_A_s"] + r["sweep_B_s"]))
     dt = time.perf_counter() - t0
-    v = float(np.mean([x["value"] for x in vals]))
+    v = float(np.mean(vals))
+    desc = (f"{sample} random composite cells per partition of the first A and B sweeps of GM(0) {p.N}^2 s={p.s} "
+            f"(fp64 oracle, Err=1e-4) on all {r['cores']} host cores ({r['cpu_model']}), extrapolated to the "
+            f"partition; flow update excluded (value = upper bound)")
     out = {"metric": METRIC, "value": v, "unit": "sweeps/s", "n_gpus": a.gpus, "steps": a.steps,
            "warmup": a.warmup, "ms_per_step": dt * 1e3 / a.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": dict(bench_config(a, a.gpus), sample=vals[-1]["sample"],
-                                precision="fp64 oracle (log-domain Sinkhorn)"),
+           "config": dict(bench_config(a, a.gpus, "independent"), sample=desc,
+                          precision="fp64 oracle (log-domain Sinkhorn)"),
            "impl": "reference",
-           "cpu_baseline": {"value": v, "unit": "sweeps/s", "cores": 1, "kind": "oracle",
-                            "sample": vals[-1]["sample"]},
+           "cpu_baseline": {"value": v, "unit": "sweeps/s", "cores": r["cores"], "kind": "oracle", "sample": desc},
            "e2e": {"value": v, "unit": "sweeps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------------------
+
+def sweep_roofline_keys(cnt, sweep_s, mp):
+    sm_max = float(mp.get("sm_max_mhz", 1965.0))
+    peak = 148 * 16 * sm_max * 1e6        # MUFU ex2/lg2 per s (DESIGN.md "Roofline")
+    achieved = cnt["mufu_ops"] / sweep_s
+    return achieved, peak, sm_max
+
+
+def load_traffic():
+    """DRAM bytes per sweep from the committed ncu capture (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "r02_sweep_traffic.json")
+    try:
+        return json.load(open(path))
+    except Exception:
+        return None
 
 
 def run_stripes(a):
@@ -180,42 +312,64 @@ def run_stripes(a):
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
     p = make(0, a.N, a.s)
     rows = stripe_rows(a.N // a.s, world)
-    eng = GpuEngine(p, rows[rank], rows[rank + 1], device=local)
-    n1, n2 = eng.n1, eng.n2
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    with torch.cuda.stream(stream):
+        eng = GpuEngine(p, rows[rank], rows[rank + 1], device=local, stream=stream)
+        n1, n2 = eng.n1, eng.n2
 
-    def cycle():
-        run_distributed(cycle_program(eng, rank, world, rows, n1, n2), rank, world, device=dev)
+        def cycle():
+            return run_distributed(cycle_program(eng, rank, world, rows, n1, n2), rank, world, device=dev)
 
-    for _ in range(a.warmup):
-        cycle()
-    torch.cuda.synchronize()
-    dist.barrier()
-    ms = []
-    with ClockSampler(local) as clk:
-        for k in range(a.steps):
-            flush.fill_(float(k))
-            torch.cuda.synchronize()
-            dist.barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
+        for _ in range(a.warmup):
             cycle()
-            e1.record()
-            torch.cuda.synchronize()
-            ms.append(e0.elapsed_time(e1))
-    t = torch.tensor([sum(ms) / 1e3], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_s = float(t.item())
+        torch.cuda.synchronize()
+        dist.barrier()
+        ms = []
+        with ClockSampler(local) as clk:
+            for k in range(a.steps):
+                flush.fill_(float(k))
+                torch.cuda.synchronize()
+                dist.barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                cycle()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ms.append(e0.elapsed_time(e1))
+        t = torch.tensor([sum(ms) / 1e3], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_s = float(t.item())
+        # convergence bookkeeping: one more cycle with the all-reduced entry errors
+        conv = run_distributed(cycle_program(eng, rank, world, rows, n1, n2, conv=True), rank, world, device=dev)
+        # end to end: init from host buffers + cycles + the all-reduced error readback
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        eng2 = GpuEngine(p, rows[rank], rows[rank + 1], device=local, stream=stream)
+        e2e_steps = max(1, min(a.steps, a.e2e_steps))
+        for _ in range(e2e_steps):
+            run_distributed(cycle_program(eng2, rank, world, rows, n1, n2), rank, world, device=dev)
+        run_distributed(cycle_program(eng2, rank, world, rows, n1, n2, flow=False, conv=True), rank, world,
+                        device=dev)
+        torch.cuda.synchronize()
+        e2e_t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+        eng2.close()
     if rank == 0:
+        h2d = p.mu.nbytes + p.nu.nbytes + p.init_off.nbytes + p.init_ext.nbytes + p.init_pos.nbytes + \
+            p.init_data.nbytes
         out = {"metric": METRIC, "value": 2 * a.steps / total_s, "unit": "sweeps/s", "n_gpus": world,
                "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_s * 1e3 / a.steps,
                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-               "data": "synthetic",
-               "config": {"workload": f"GM(0) {a.N}x{a.N}, s={a.s}, eps=(2h)^2, theta=20deg; step = hybrid cycle",
-                          "parallelism": f"row stripes x{world} (halo rows over NCCL, replicated min-cost flow)",
-                          "l2": "flushed between timed steps (256 MB write)"},
+               "data": "synthetic", "config": bench_config(a, world, "stripes"),
+               "e2e": {"value": (2 * e2e_steps + 2) / float(e2e_t.item()), "unit": "sweeps/s",
+                       "h2d_bytes_per_step": int(h2d / e2e_steps), "d2h_bytes_per_step": 16,
+                       "note": "stripe contexts from host buffers + cycles + all-reduced entry errors"},
+               "gpu_launches": None,
+               "state": {"entry_error_after": [x for x in conv] if conv else None},
                "clocks": clk.summary()}
         print(json.dumps(out), flush=True)
     eng.close()
@@ -223,10 +377,10 @@ def run_stripes(a):
     dist.destroy_process_group()
 
 
-def run_ours(a):
+def run_ours(a, parallelism):
     import torch
     import torch.distributed as dist
-    from paper_2405_09400_b200 import DomDec, mufu_peak
+    from paper_2405_09400_b200 import DomDec, mufu_peak, multiscale_solve
 
     world, rank, local = dist_env()
     if world > 1:
@@ -236,6 +390,11 @@ def run_ours(a):
     stream = torch.cuda.Stream(device=dev)
     p = make(rank, a.N, a.s)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
+    mp = {}
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
 
     def barrier():
         torch.cuda.synchronize()
@@ -250,9 +409,9 @@ def run_ours(a):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     with torch.cuda.stream(stream):
         dd = DomDec.from_problem(p, stream=stream.cuda_stream, device=local)
-        ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
         def cycle(sweep_events=None):
             for part in ("A", "B"):
@@ -285,27 +444,20 @@ def run_ours(a):
         sweep_ms = [x.elapsed_time(y) for x, y in sweep_ev]
         cnt = dd.counters()
         # one more (untimed) cycle for the flow-update statistics
-        dd.sweep("A")
-        dd.sweep("B")
+        sa = dd.sweep("A", stats=True)
+        sb = dd.sweep("B", stats=True)
         fstats = dd.flow_update(stats=True)
         total_s = allmax(sum(step_ms) / 1e3)
-        sweeps_done = 2 * a.steps * world
-        value = sweeps_done / total_s
+        value = 2 * a.steps * world / total_s
         ex, ey = dd.marginal_error()
+        dd.close()
 
-        # roofline of the dominant kernel (the fused sweep): algorithmic MUFU ops
+        # roofline of the dominant kernel (the fused sweep, a1-a6)
         sweep_s = sum(sweep_ms) / 1e3
-        achieved = cnt["mufu_ops"] / sweep_s
-        import json as _j
-        mp = {}
-        try:
-            mp = _j.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-        except Exception:
-            pass
-        sm_max = float(mp.get("sm_max_mhz", 1965.0))
-        peak_nominal = 148 * 16 * sm_max * 1e6        # MUFU ex2/lg2 per s
+        achieved, peak_nominal, sm_max = sweep_roofline_keys(cnt, sweep_s, mp)
         measured_mufu = mufu_peak(local)
-        hbm_peak = float(mp.get("hbm_gbs", 6650.0)) * 1e9
+        hbm_peak = float(mp.get("hbm_gbs", 6552.0)) * 1e9
+        traffic = load_traffic()
 
         # end-to-end through the public API from host buffers
         barrier()
@@ -316,37 +468,37 @@ def run_ours(a):
             dd2.sweep("A")
             dd2.sweep("B")
             dd2.flow_update()
-        e2e_err = dd2.marginal_error()
+        dd2.marginal_error()
         torch.cuda.synchronize()
         e2e_s = allmax(time.perf_counter() - t0)
         h2d = (p.mu.nbytes + p.nu.nbytes + p.init_off.nbytes + p.init_ext.nbytes + p.init_pos.nbytes +
                p.init_data.nbytes)
         dd2.close()
 
-        # time to L1 marginal error 1e-4 (reading R14): wall time from the
-        # end of domdec_init to the first hybrid cycle whose A and B
-        # sweep-entry errors are both <= 1e-4, synchronising at cycle ends
-        # only.  Measured on config 3 (256^2, s = 4, the "good initial
-        # coupling" T_5) and on the bench grid with T_5.
-        def ttc_run(N, s, theta, cap_s, cap_cycles):
-            from synth import make_problem
-            q = make_problem("gm", N, s, eps_factor=CFG["eps_factor"], theta_deg=theta, seed=rank)
+        # time to L1 marginal error 1e-4 (reading R14): wall time from the end
+        # of the context's construction (single scale) or from the call
+        # (multiscale, which builds its own layers) to the first hybrid cycle
+        # whose A and B sweep-entry errors are both <= 1e-4 ||mu||.
+        def ttc_single(N, s, theta, cap_s, cap_cycles, flow_every):
+            q = make(rank, N, s, theta=theta)
             barrier()
             dd3 = DomDec.from_problem(q, stream=stream.cuda_stream, device=local)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            res, conv, flows = None, float("nan"), 0
-            t_sw = t_fl = 0.0   # host time per phase (each stats call synchronises)
+            res, conv, flows, nfl = None, float("nan"), 0, 0
+            t_sw = t_fl = 0.0
             for c in range(cap_cycles):
                 t1 = time.perf_counter()
-                sa = dd3.sweep("A", stats=True)
-                sb = dd3.sweep("B", stats=True)
+                sa_ = dd3.sweep("A", stats=True)
+                sb_ = dd3.sweep("B", stats=True)
                 t2 = time.perf_counter()
-                fs = dd3.flow_update(stats=True)
+                if flow_every and c % flow_every == flow_every - 1:
+                    fs = dd3.flow_update(stats=True)
+                    flows += int(fs["stationary"] == 0)
+                    nfl += 1
                 t_sw += t2 - t1
                 t_fl += time.perf_counter() - t2
-                flows += int(fs["stationary"] == 0)
-                conv = allmax(max(sa["l1x_entry"], sb["l1x_entry"]))
+                conv = allmax(max(sa_["l1x_entry"], sb_["l1x_entry"]))
                 if conv <= 1e-4:
                     torch.cuda.synchronize()
                     res = {"seconds": allmax(time.perf_counter() - t0), "cycles": c + 1, "sweeps": 2 * (c + 1),
@@ -359,50 +511,77 @@ def run_ours(a):
             if res is None:
                 res = {"seconds": None, "reached": False, "cycles_run": cap_cycles, "last_entry_error": conv,
                        "nonstationary_flows": flows}
-            res["workload"] = f"GM(rank) {N}^2 s={s} eps=(2h)^2 theta={theta:g}deg, hybrid A/B/flow"
+            res["flow_updates"] = nfl
+            res["workload"] = (f"GM(rank) {N}^2 s={s} eps=(2h)^2 theta={theta:g}deg, single scale from (id,T)#mu, "
+                               f"hybrid A/B + flow update every {flow_every} cycle(s) (PAPER.md:750)")
             res["phase_seconds"] = {"sweeps": t_sw, "flow_updates": t_fl}
+            ex3, ey3 = dd3.marginal_error()
+            res["l1_x"], res["l1_y"] = ex3, ey3
             dd3.close()
             return res
 
-        sg = None
+        def ttc_multiscale(N, s, theta, levels):
+            q = make(rank, N, s, theta=theta)
+            barrier()
+            t0 = time.perf_counter()
+            dd4, st = multiscale_solve(q.mu, q.nu, s, q.eps, q.E, levels=levels, conv=1e-4, max_cycles=3000,
+                                       flow_every=1, stream=stream.cuda_stream, device=local)
+            torch.cuda.synchronize()
+            sec = allmax(time.perf_counter() - t0)
+            ex4, ey4 = dd4.marginal_error()
+            dd4.close()
+            ok = all(st["converged"])
+            return {"seconds": sec if ok else None, "reached": ok, "levels": st,
+                    "l1_x": ex4, "l1_y": ey4, "nonstationary_flows": int(sum(st["flows"])),
+                    "workload": (f"GM(rank) {N}^2 s={s} eps=(2h)^2 theta={theta:g}deg (the same mu, nu pair), "
+                                 f"multiscale (SURVEY 8(f) f3, readings R23-R25): {levels} layers from "
+                                 f"{N >> (levels - 1)}^2, product coupling at the coarsest, hybrid A/B + flow "
+                                 "update every cycle on every layer, each layer until R14 <= 1e-4")}
+
+        sg = ttc = extra = None
         if rank == 0 and not a.no_ttc:
-            # SinkhornGPU comparator: global separable
-            # Sinkhorn on the cfg3 pair (256^2, theta=5), cold start at eps=(2h)^2, to Err=1e-4.
+            # SinkhornGPU comparator
             from paper_2405_09400_b200 import sinkhorn_global
-            from synth import make_problem as _mp
-            q = _mp("gm", 256, 4, theta_deg=5.0, seed=0)
+            q = make(0, 256, 4, theta=5.0)
             _, _, it_sg, e_sg, ms_sg = sinkhorn_global(q.mu, q.nu, q.eps_prime, err=1e-4, max_iter=20000,
                                                        check_every=10)
             sg = {"workload": "GM(0) 256^2 theta=5deg, eps=(2h)^2, cold start, Err=1e-4 (PAPER.md:1264)",
                   "seconds": ms_sg / 1e3, "iterations": it_sg, "l1_x": e_sg, "ms_per_iteration": ms_sg / it_sg,
                   "note": "device time (CUDA events), host copies excluded; fp64 potentials"}
-        ttc = None
         if not a.no_ttc:
-            ttc = {"cfg3_256": ttc_run(256, 4, 5.0, a.ttc_seconds, a.ttc_cycles),
-                   f"cfg4_{a.N}": ttc_run(a.N, a.s, 5.0, a.ttc_seconds, a.ttc_cycles)}
+            ttc = {f"cfg4_{a.N}_multiscale": ttc_multiscale(a.N, a.s, CFG["theta"], 5),
+                   f"cfg4_{a.N}_multiscale_theta5": ttc_multiscale(a.N, a.s, 5.0, 5),
+                   "cfg3_256_multiscale": ttc_multiscale(256, 4, 5.0, 3),
+                   "cfg3_256": ttc_single(256, 4, 5.0, a.ttc_seconds, a.ttc_cycles, 1),
+                   f"cfg4_{a.N}": ttc_single(a.N, a.s, 5.0, a.ttc_seconds, a.ttc_cycles, a.ttc_flow_every)}
+        if rank == 0 and not a.no_extra:
+            extra = extra_configs(stream, local, mp)
 
     if rank == 0:
-        cpu = cpu_baseline(p, a.cpu_seconds) if world == 1 else None
+        cpu = None
+        if world == 1 and not a.no_cpu:
+            cpu = cpu_baseline(p, a.cpu_seconds)
+        tr = None
+        if traffic is not None:
+            tr = traffic.get("bytes_per_sweep")
         out = {
             "metric": METRIC, "value": value, "unit": "sweeps/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": total_s * 1e3 / a.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": bench_config(a, world),
+            "config": bench_config(a, world, parallelism),
             "e2e": {"value": 2 * e2e_steps * world / e2e_s, "unit": "sweeps/s",
                     "h2d_bytes_per_step": int(h2d / e2e_steps), "d2h_bytes_per_step": int(16 / e2e_steps),
                     "steps": e2e_steps,
                     "note": "domdec_init from host buffers + steps hybrid cycles + marginal_error readback"},
-            # per step: 2 sweeps x (solve_kernel + split_kernel in 3 size classes) + flow
-            # (k_flow_costs, mcf_kernel, k_apply_flow) -- profiles/ launch list
+            # per step: 2 sweeps x (k_bin + 5 size-class launches) + flow (k_flow_costs, mcf_kernel,
+            # k_apply_flow); profiles/r02_launches_*.csv
             "gpu_launches": 15 * a.steps,
             "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_nominal / 1e12,
                          "unit": "TOP/s (MUFU ex2+lg2)", "frac": achieved / peak_nominal,
-                         # dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full
-                         # capture of each sweep kernel (profiles/r01_ncu_summary.txt: solve
-                         # 199.3 + 9.3 MB, split 195.3 + 154.8 MB, small size class, one sweep)
-                         "traffic": 5.59e8, "traffic_unit": "bytes per sweep (solve + split launch)",
-                         "traffic_vs_algorithmic": 5.59e8 / max(1.0, cnt["bytes"] / max(1, cnt["sweeps"])),
-                         "kernel": "sweep = solve_kernel + split_kernel (a1-a6)",
+                         "traffic": tr, "traffic_unit": "DRAM bytes per sweep (ncu --set full, all sweep kernels)",
+                         "traffic_source": traffic.get("source") if traffic else None,
+                         "traffic_vs_algorithmic": (tr / (cnt["bytes"] / max(1, cnt["sweeps"]))) if tr else None,
+                         "kernel": "sweep = k_bin + sweep_kernel size classes (a1-a6, fused)",
                          "peak_source": f"148 SM x 16 MUFU/clk x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
                          "measured_mufu_peak": measured_mufu / 1e12,
                          "frac_of_measured": achieved / measured_mufu,
@@ -415,20 +594,21 @@ def run_ours(a):
             "clocks": clk.summary(),
             "time_to_l1_1e-4": ttc,
             "sinkhorn_global_cfg3": sg,
-            # sweeps/s with A and B separately, flow-update time, cycles/s
+            "extra_configs": extra,
             "per_partition": {"sweep_ms_A": float(np.mean(sweep_ms[0::2])), "sweep_ms_B": float(np.mean(sweep_ms[1::2])),
                               "flow_ms": (sum(step_ms) - sum(sweep_ms)) / a.steps,
                               "cycles_per_s": a.steps * world / total_s},
             "state": {"l1_x": ex, "l1_y": ey, "iters_per_cell": cnt["iters"] / max(1, cnt["cells"]),
-                      "flow_ms_per_step": (sum(step_ms) - sum(sweep_ms)) / a.steps},
+                      "entry_error_A": sa["l1x_entry"], "entry_error_B": sb["l1x_entry"]},
             "step_breakdown": {
                 "sweeps_share": sum(sweep_ms) / sum(step_ms),
                 "flow_share": 1.0 - sum(sweep_ms) / sum(step_ms),
                 "dominant_kernel": "mcf_kernel (exact min-cost flow, a8): latency-bound (grid barriers), "
                                    "no throughput roofline; reported in rounds and ms",
-                "mcf_last_cycle": {"solver_ms": fstats["solver_ms"], "tile_phases": fstats["rounds"],
+                "mcf_next_cycle": {"solver_ms": fstats["solver_ms"], "tile_phases": fstats["rounds"],
                                    "label_rounds": fstats["label_rounds"], "refines": fstats["refines"],
-                                   "objective": fstats["objective"], "changed_cells": fstats["changed_cells"]}},
+                                   "objective": fstats["objective"], "changed_cells": fstats["changed_cells"],
+                                   "stationary": fstats["stationary"]}},
         }
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -436,14 +616,62 @@ def run_ours(a):
         dist.destroy_process_group()
 
 
+def extra_configs(stream, local, mp):
+    """BASELINE configs[2] eps sweep (256^2, s = 4, eps = (2h)^2 .. (8h)^2) and
+    configs[4] (2048^2, s = 2): pure domdec sweeps/s and the sweep MUFU
+    roofline fraction after 4 warm-up sweeps (device time, CUDA events), plus
+    the multiscale time to 1e-4 at config 5."""
+    import torch
+    from paper_2405_09400_b200 import DomDec, multiscale_solve
+    out = {"cfg3_eps_sweep": {}}
+
+    def sweeps(p, nwarm=4, nt=6):
+        dd = DomDec.from_problem(p, stream=stream.cuda_stream, device=local)
+        for k in range(nwarm):
+            dd.sweep("AB"[k % 2])
+        torch.cuda.synchronize()
+        dd.reset_counters()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for k in range(nt):
+            dd.sweep("AB"[k % 2])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        s = e0.elapsed_time(e1) / 1e3
+        cnt = dd.counters()
+        dd.close()
+        ach, peak, _ = sweep_roofline_keys(cnt, s, mp)
+        return {"sweeps_per_s": nt / s, "sweep_ms": s * 1e3 / nt, "mufu_frac": ach / peak,
+                "mufu_ops_per_sweep": cnt["mufu_ops"] / nt, "iters_per_cell": cnt["iters"] / max(1, cnt["cells"])}
+
+    for f in (2.0, 4.0, 6.0, 8.0):
+        out["cfg3_eps_sweep"][f"({f:g}h)^2"] = sweeps(make(0, 256, 4, theta=5.0, eps_factor=f))
+    p5 = make(0, 2048, 2)
+    out["cfg5_2048_s2"] = sweeps(p5, 2, 4)
+    t0 = time.perf_counter()
+    dd5, st = multiscale_solve(p5.mu, p5.nu, 2, p5.eps, p5.E, levels=5, conv=1e-4, max_cycles=3000, flow_every=1,
+                               stream=stream.cuda_stream, device=local)
+    torch.cuda.synchronize()
+    sec = time.perf_counter() - t0
+    dd5.close()
+    out["cfg5_2048_s2"]["ttc_multiscale"] = {"seconds": sec if all(st["converged"]) else None, "levels": st,
+                                             "workload": "GM(0)+T_20 2048^2 s=2 eps=(2h)^2, 5 layers from 128^2, "
+                                                         "flow update every cycle"}
+    return out
+
+
 def main():
     a = parse()
+    world = dist_env()[0]
+    par = a.parallelism
+    if par == "auto":
+        par = "stripes" if world > 1 else "independent"
     if a.impl == "reference":
         run_reference(a)
-    elif a.parallelism == "stripes" and dist_env()[0] > 1:
+    elif par == "stripes" and world > 1:
         run_stripes(a)
     else:
-        run_ours(a)
+        run_ours(a, par)
 
 
 if __name__ == "__main__":

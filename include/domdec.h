@@ -215,6 +215,23 @@ dd_status flow_edge_costs(dd_ctx *ctx, double *cbar, int64_t *C, int64_t *q);
  * then truncate + minimal box. */
 dd_status flow_apply(dd_ctx *ctx, const int64_t *w);
 
+/* Device-pointer variants of the flow-update hooks, fully asynchronous on
+ * the ctx stream (stripe mode: the instance is all-gathered
+ * over NCCL as a device tensor and solved by every rank):
+ *  flow_edge_costs_device: cbar / C of the current state into device
+ *    buffers [I][5] (either may be NULL); only the rows whose plan moments
+ *    this ctx holds are meaningful in stripe mode;
+ *  flow_solve: exact min-cost flow of the global instance d_C [I][5] (device,
+ *    integer costs, column 0 ignored) with the ctx's supplies, warm-started
+ *    from the ctx's previous optimal flow and prices like flow_update; the
+ *    optimal flow goes to d_w (device [I][5], may be NULL) and stays in the
+ *    ctx for flow_apply_device.  stats != NULL synchronises;
+ *  flow_apply_device: apply a device flow d_w [I][5] (no divergence check:
+ *    use flow_apply for untrusted host flows). */
+dd_status flow_edge_costs_device(dd_ctx *ctx, double *d_cbar, int64_t *d_C);
+dd_status flow_solve(dd_ctx *ctx, const int64_t *d_C, int64_t *d_w, dd_flow_stats *stats);
+dd_status flow_apply_device(dd_ctx *ctx, const int64_t *d_w);
+
 /* Standalone exact min-cost flow on the n1 x n2 grid graph (Eq. MinCostFlow
  * PAPER.md:378-381 with the divergence constraints PAPER.md:350-354) on the
  * GPU: q [I] > 0 supplies, C [I][5] integer arc costs (column 0 ignored, arcs
@@ -268,17 +285,24 @@ dd_status domdec_reset_counters(dd_ctx *ctx);
 dd_status dd_mufu_peak(int32_t device, double *ops_per_s);
 
 /* Stripe halo exchange: serialise the basic-cell marginals of
- * basic-cell row `row` (n2 cells) into the DEVICE buffer buf (layout: int32
- * off[n2][2], int32 ext[n2][2], then the fp64 boxes in cell order, row-major).
- * buf = NULL: only *bytes is set (required size).  cap < size: DD_ERR_ARG.
- * Synchronises the context stream.  Valid for any row whose marginals are
- * current in this context. */
+ * basic-cell row `row` (n2 cells) into the DEVICE buffer buf of capacity cap
+ * bytes (layout: int64 total bytes, int32 off[n2][2], int32 ext[n2][2], then
+ * the fp64 boxes in cell order, row-major).  buf = NULL: *bytes receives the
+ * exact size (synchronises).  Otherwise fully asynchronous on the ctx stream
+ * (no host round trip; *bytes, if given, receives cap); a row larger than cap
+ * is not written and makes the next synchronising call return
+ * DD_ERR_NUMERIC.  domdec_halo_capacity gives a cap that holds any row whose
+ * boxes fit the shared-memory size classes.  Valid for any row whose
+ * marginals are current in this context. */
 dd_status domdec_halo_pack(dd_ctx *ctx, int32_t row, void *buf, int64_t cap, int64_t *bytes);
+dd_status domdec_halo_capacity(dd_ctx *ctx, int64_t *bytes);
 
 /* Replace the marginals of basic-cell row `row` by the content of the DEVICE
  * buffer buf (as written by domdec_halo_pack of another context of the same
- * problem).  The boxes are appended to the current pool (DD_ERR_NUMERIC if it
- * is full).  Synchronises. */
+ * problem; bytes = its capacity).  Fully asynchronous: the boxes are appended
+ * to the current pool by a device-side allocation; a full pool or a header
+ * inconsistent with bytes makes the next synchronising call return
+ * DD_ERR_NUMERIC. */
 dd_status domdec_halo_unpack(dd_ctx *ctx, int32_t row, const void *buf, int64_t bytes);
 
 /* ---- Multiscale domain decomposition ----------------
@@ -320,6 +344,8 @@ typedef struct {
   int32_t converged[16];
   double entry_error[16];   /* max of the A and B sweep-entry errors / ||mu|| of the last cycle */
   double seconds[16];   /* wall time per layer (initial coupling / refinement included)      */
+  double init_seconds[16];  /* of which: building the layer's context (product / refinement) */
+  double flow_seconds[16];  /* of which: flow updates                                        */
   double total_seconds; /* wall time of the whole call                                       */
 } dd_ms_stats;
 

@@ -66,13 +66,14 @@ class MsOptions(C.Structure):
 class MsStats(C.Structure):
     _fields_ = [("levels", C.c_int32), ("N", C.c_int32 * 16), ("cycles", C.c_int32 * 16), ("flows", C.c_int32 * 16),
                 ("converged", C.c_int32 * 16), ("entry_error", C.c_double * 16), ("seconds", C.c_double * 16),
-                ("total_seconds", C.c_double)]
+                ("init_seconds", C.c_double * 16), ("flow_seconds", C.c_double * 16), ("total_seconds", C.c_double)]
 
     def as_dict(self):
         L = self.levels
         return {"levels": L, "N": list(self.N[:L]), "cycles": list(self.cycles[:L]), "flows": list(self.flows[:L]),
                 "converged": [bool(x) for x in self.converged[:L]], "entry_error": list(self.entry_error[:L]),
-                "seconds": list(self.seconds[:L]), "total_seconds": self.total_seconds}
+                "seconds": list(self.seconds[:L]), "init_seconds": list(self.init_seconds[:L]),
+                "flow_seconds": list(self.flow_seconds[:L]), "total_seconds": self.total_seconds}
 
 
 class Counters(C.Structure):
@@ -118,7 +119,12 @@ def lib():
         L.domdec_halo_pack.argtypes = [vp, C.c_int32, vp, C.c_int64, C.POINTER(C.c_int64)]
         L.domdec_halo_unpack.argtypes = [vp, C.c_int32, vp, C.c_int64]
         L.domdec_destroy.argtypes = [vp]
-        if hasattr(L, "dd_multiscale_solve"):   # (absent from older development builds)
+        if hasattr(L, "flow_solve"):   # (absent from older development builds)
+            L.flow_edge_costs_device.argtypes = [vp, vp, vp]
+            L.flow_solve.argtypes = [vp, vp, vp, C.POINTER(FlowStats)]
+            L.flow_apply_device.argtypes = [vp, vp]
+            L.domdec_halo_capacity.argtypes = [vp, C.POINTER(C.c_int64)]
+        if hasattr(L, "dd_multiscale_solve"):
             L.domdec_init_product.argtypes = [C.POINTER(_Problem), C.POINTER(_Options), C.POINTER(vp)]
             L.domdec_refine.argtypes = [vp, C.POINTER(_Problem), C.POINTER(_Options), C.POINTER(vp)]
             L.dd_multiscale_solve.argtypes = [C.POINTER(_Problem), C.POINTER(_Options), C.POINTER(MsOptions),
@@ -134,7 +140,8 @@ def lib():
                    "domdec_export_cell_stats", "flow_edge_costs", "flow_apply", "dd_mincost_flow", "domdec_destroy", "domdec_counters",
                    "domdec_reset_counters", "dd_mufu_peak", "domdec_halo_pack", "domdec_halo_unpack",
                    "dd_sinkhorn_global", "domdec_init_product", "domdec_refine", "dd_multiscale_solve",
-                   "domdec_export_cell_stats"):
+                   "domdec_export_cell_stats", "flow_edge_costs_device", "flow_solve", "flow_apply_device",
+                   "domdec_halo_capacity"):
             if hasattr(L, fn):
                 getattr(L, fn).restype = C.c_int
         _lib = L
@@ -146,7 +153,9 @@ EXPORTED = ("domdec_init", "domdec_sweep", "flow_update", "marginal_error", "pri
             "flow_edge_costs",
             "flow_apply", "dd_mincost_flow", "domdec_destroy", "dd_last_error", "dd_version", "domdec_counters",
             "domdec_reset_counters", "dd_mufu_peak", "domdec_halo_pack", "domdec_halo_unpack",
-            "dd_sinkhorn_global", "domdec_init_product", "domdec_refine", "dd_multiscale_solve")
+            "dd_sinkhorn_global", "domdec_init_product", "domdec_refine", "dd_multiscale_solve",
+            "domdec_export_cell_stats", "flow_edge_costs_device", "flow_solve", "flow_apply_device",
+            "domdec_halo_capacity")
 
 
 def _problem(mu, nu, s, eps, h, E, off=None, ext=None, pos=None, data=None):
@@ -279,6 +288,27 @@ class DomDec:
         n = C.c_int64()
         _check(lib().domdec_halo_pack(self._ctx, int(row), C.c_void_p(dev_ptr), int(cap), C.byref(n)), self._ctx)
         return n.value
+
+    def halo_capacity(self):
+        """Bytes of a halo buffer that holds any row (domdec_halo_capacity)."""
+        n = C.c_int64()
+        _check(lib().domdec_halo_capacity(self._ctx, C.byref(n)), self._ctx)
+        return n.value
+
+    def edge_costs_device(self, cbar_ptr, C_ptr):
+        """flow_edge_costs_device: cbar / C into device buffers (asynchronous)."""
+        _check(lib().flow_edge_costs_device(self._ctx, C.c_void_p(cbar_ptr) if cbar_ptr else None,
+                                            C.c_void_p(C_ptr) if C_ptr else None), self._ctx)
+
+    def flow_solve(self, C_ptr, w_ptr=None, stats=False):
+        """flow_solve: warm-started exact min-cost flow of a device instance."""
+        st = FlowStats() if stats else None
+        _check(lib().flow_solve(self._ctx, C.c_void_p(C_ptr), C.c_void_p(w_ptr) if w_ptr else None,
+                                C.byref(st) if st is not None else None), self._ctx)
+        return st.as_dict() if st is not None else None
+
+    def apply_flow_device(self, w_ptr):
+        _check(lib().flow_apply_device(self._ctx, C.c_void_p(w_ptr)), self._ctx)
 
     def halo_unpack(self, row, dev_ptr, nbytes):
         """Replace row `row` by a buffer written by halo_pack (device pointer)."""

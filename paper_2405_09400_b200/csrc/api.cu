@@ -49,6 +49,79 @@ __global__ void k_copy_boxes(const double* __restrict__ src, double* __restrict_
   for (long long t = threadIdx.x; t < len; t += blockDim.x) dst[d0 + t] = src[s0 + t];
 }
 
+// Halo buffers (domdec_halo_pack): int64 total bytes, int32 off[n2][2],
+// int32 ext[n2][2], then the fp64 boxes (head = 8 + 16 n2 bytes).  The
+// metadata kernels run on one thread (n2 <= a few thousand cells) and build
+// the per-cell copy list meta[3 k .. 3 k + 2] = (source element, destination
+// element, length) for k_copy_boxes; no host round trip.
+__global__ void k_halo_meta_pack(const long long* __restrict__ pos, const int* __restrict__ off,
+                                 const int* __restrict__ ext, int i0, int n2, long long cap, char* __restrict__ buf,
+                                 long long* __restrict__ meta) {
+  if (threadIdx.x != 0) return;
+  const long long head = 8 + 16LL * n2;
+  int* ho = (int*)(buf + 8);
+  int* he = ho + 2 * n2;
+  long long at = 0;
+  for (int k = 0; k < n2; ++k) {
+    const int i = i0 + k;
+    const long long len = (long long)ext[2 * i] * ext[2 * i + 1];
+    ho[2 * k] = off[2 * i];
+    ho[2 * k + 1] = off[2 * i + 1];
+    he[2 * k] = ext[2 * i];
+    he[2 * k + 1] = ext[2 * i + 1];
+    meta[3 * k] = pos[i];
+    meta[3 * k + 1] = head / 8 + at;
+    meta[3 * k + 2] = len;
+    at += len;
+  }
+  const long long total = head + 8 * at;
+  *(long long*)buf = total;   // > cap: the receiver rejects the buffer
+  if (total > cap)
+    for (int k = 0; k < n2; ++k) meta[3 * k + 2] = 0;
+}
+
+__global__ void k_halo_meta_unpack(const char* __restrict__ buf, long long bytes, int i0, int n2, int N1, int N2,
+                                   unsigned long long* __restrict__ poolctr, long long pool_cap,
+                                   long long* __restrict__ pos, int* __restrict__ off, int* __restrict__ ext,
+                                   long long* __restrict__ meta, unsigned long long* __restrict__ invalid) {
+  if (threadIdx.x != 0) return;
+  const long long head = 8 + 16LL * n2;
+  const int* ho = (const int*)(buf + 8);
+  const int* he = ho + 2 * n2;
+  long long at = 0;
+  bool ok = *(const long long*)buf <= bytes;
+  for (int k = 0; k < n2 && ok; ++k) {
+    ok = he[2 * k] >= 1 && he[2 * k + 1] >= 1 && ho[2 * k] >= 0 && ho[2 * k + 1] >= 0 &&
+         ho[2 * k] + he[2 * k] <= N1 && ho[2 * k + 1] + he[2 * k + 1] <= N2;
+    at += (long long)he[2 * k] * he[2 * k + 1];
+  }
+  ok = ok && head + 8 * at == *(const long long*)buf;
+  long long base = -1;
+  if (ok) {
+    base = (long long)atomicAdd(poolctr, (unsigned long long)at);
+    ok = base + at <= pool_cap;
+  }
+  if (!ok) {
+    atomicAdd(invalid, 1ull);
+    for (int k = 0; k < n2; ++k) meta[3 * k + 2] = 0;
+    return;
+  }
+  at = 0;
+  for (int k = 0; k < n2; ++k) {
+    const int i = i0 + k;
+    const long long len = (long long)he[2 * k] * he[2 * k + 1];
+    meta[3 * k] = head / 8 + at;
+    meta[3 * k + 1] = base + at;
+    meta[3 * k + 2] = len;
+    pos[i] = base + at;
+    off[2 * i] = ho[2 * k];
+    off[2 * i + 1] = ho[2 * k + 1];
+    ext[2 * i] = he[2 * k];
+    ext[2 * i + 1] = he[2 * k + 1];
+    at += len;
+  }
+}
+
 // Deterministic single-block reductions for the diagnostics.
 __global__ void k_l1_diff(const double* __restrict__ a, const double* __restrict__ b, long long n,
                           double* __restrict__ out) {
@@ -179,8 +252,13 @@ void free_ctx(dd_ctx* c) {
   } while (0)
 
 // Per basic cell box mass (initial-coupling check of the device init path).
+// A device-made coupling (multiscale refinement of a coarse state) carries the
+// coarse state's truncation ledger (reading R9): every cell's mass defect
+// m_i - ||nu_i|| is >= 0 after balancing and their sum is the total deficit,
+// which the L1 Y-error bounds, so each cell must match m_i within 1e-6 m_i
+// plus that L1 Y-error (slack).
 __global__ void k_box_mass(const double* __restrict__ pool, const long long* __restrict__ pos,
-                           const int* __restrict__ ext, const double* __restrict__ m, int I,
+                           const int* __restrict__ ext, const double* __restrict__ m, int I, double slack,
                            unsigned long long* __restrict__ bad) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= I) return;
@@ -192,7 +270,7 @@ __global__ void k_box_mass(const double* __restrict__ pool, const long long* __r
     ok = ok && v >= 0.0 && isfinite(v);
     s += v;
   }
-  if (!ok || fabs(s - m[i]) > 1e-6 * m[i]) atomicAdd(bad, 1ull);
+  if (!ok || fabs(s - m[i]) > 1e-6 * m[i] + slack) atomicAdd(bad, 1ull);
 }
 
 // init_impl: P's initial coupling comes either from host arrays (the public
@@ -420,17 +498,18 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c, 
     // feasibility of the device-made coupling: ||nu_i|| = m_i, sum_i nu_i = nu
     unsigned long long* bad = (unsigned long long*)(c->d_red + 16);
     DD_CUDA(cudaMemsetAsync(bad, 0, 8, st));
-    k_box_mass<<<(I + 127) / 128, 128, 0, st>>>(c->d_pool[0], c->d_pos[0], c->d_ext[0], c->d_m, I, bad);
-    DD_CUDA(cudaGetLastError());
     DD_CUDA(cudaMemsetAsync(c->d_scratch, 0, NN * 8, st));
     k_scatter_boxes<<<I, 128, 0, st>>>(c->d_pool[0], c->d_pos[0], c->d_off[0], c->d_ext[0], c->N2, c->d_scratch, 0);
     DD_CUDA(cudaGetLastError());
     k_l1_diff<<<1, 1024, 0, st>>>(c->d_scratch, c->d_nu, NN, c->d_red + 8);
     DD_CUDA(cudaGetLastError());
-    unsigned long long nbad = 0;
     double dl1 = 0;
-    DD_CUDA(cudaMemcpyAsync(&nbad, bad, 8, cudaMemcpyDeviceToHost, st));
     DD_CUDA(cudaMemcpyAsync(&dl1, c->d_red + 8, 8, cudaMemcpyDeviceToHost, st));
+    DD_CUDA(cudaStreamSynchronize(st));
+    k_box_mass<<<(I + 127) / 128, 128, 0, st>>>(c->d_pool[0], c->d_pos[0], c->d_ext[0], c->d_m, I, dl1, bad);
+    DD_CUDA(cudaGetLastError());
+    unsigned long long nbad = 0;
+    DD_CUDA(cudaMemcpyAsync(&nbad, bad, 8, cudaMemcpyDeviceToHost, st));
     DD_CUDA(cudaStreamSynchronize(st));
     if (nbad || !(dl1 <= 1e-6 * snu)) {
       c->err = "device-made initial coupling infeasible (" + std::to_string(nbad) + " cells, L1 = " +
@@ -820,37 +899,34 @@ dd_status domdec_halo_pack(dd_ctx* c, int32_t row, void* buf, int64_t cap, int64
   if (!c || row < 0 || row >= c->n1) return DD_ERR_ARG;
   DD_CUDA(cudaSetDevice(c->device));
   const int n2 = c->n2, i0 = row * n2;
-  std::vector<int> ho(2 * n2), he(2 * n2);
-  std::vector<long long> hp(n2);
-  DD_CUDA(cudaMemcpyAsync(ho.data(), c->d_off[c->cur] + 2 * i0, n2 * 8, cudaMemcpyDeviceToHost, c->stream));
-  DD_CUDA(cudaMemcpyAsync(he.data(), c->d_ext[c->cur] + 2 * i0, n2 * 8, cudaMemcpyDeviceToHost, c->stream));
-  DD_CUDA(cudaMemcpyAsync(hp.data(), c->d_pos[c->cur] + i0, n2 * 8, cudaMemcpyDeviceToHost, c->stream));
-  DD_CUDA(cudaStreamSynchronize(c->stream));
-  const long long head = 16LL * n2;   // off + ext, int32; a multiple of 8
-  std::vector<long long> meta(3 * (size_t)n2);
-  long long at = 0;
-  for (int k = 0; k < n2; ++k) {
-    const long long len = (long long)he[2 * k] * he[2 * k + 1];
-    meta[3 * k] = hp[k];
-    meta[3 * k + 1] = head / 8 + at;
-    meta[3 * k + 2] = len;
-    at += len;
+  const long long head = 8 + 16LL * n2;
+  if (!buf) {   // size query (synchronises)
+    std::vector<int> he(2 * n2);
+    DD_CUDA(cudaMemcpyAsync(he.data(), c->d_ext[c->cur] + 2 * i0, n2 * 8, cudaMemcpyDeviceToHost, c->stream));
+    DD_CUDA(cudaStreamSynchronize(c->stream));
+    long long at = 0;
+    for (int k = 0; k < n2; ++k) at += (long long)he[2 * k] * he[2 * k + 1];
+    if (bytes) *bytes = head + 8 * at;
+    return DD_OK;
   }
-  const long long total = head + 8 * at;
-  if (bytes) *bytes = total;
-  if (!buf) return DD_OK;
-  if (cap < total) {
-    c->err = "halo buffer too small";
+  if (cap < head) {
+    c->err = "halo buffer smaller than its header";
     return DD_ERR_ARG;
   }
   if (!c->d_halo) TRY(dalloc(c, &c->d_halo, 3 * (size_t)n2));
-  char* b = (char*)buf;
-  DD_CUDA(cudaMemcpyAsync(b, ho.data(), 8LL * n2, cudaMemcpyHostToDevice, c->stream));
-  DD_CUDA(cudaMemcpyAsync(b + 8LL * n2, he.data(), 8LL * n2, cudaMemcpyHostToDevice, c->stream));
-  DD_CUDA(cudaMemcpyAsync(c->d_halo, meta.data(), meta.size() * 8, cudaMemcpyHostToDevice, c->stream));
-  k_copy_boxes<<<n2, 128, 0, c->stream>>>(c->d_pool[c->cur], (double*)b, c->d_halo);
+  k_halo_meta_pack<<<1, 32, 0, c->stream>>>(c->d_pos[c->cur], c->d_off[c->cur], c->d_ext[c->cur], i0, n2, cap,
+                                            (char*)buf, c->d_halo);
   DD_CUDA(cudaGetLastError());
-  DD_CUDA(cudaStreamSynchronize(c->stream));
+  k_copy_boxes<<<n2, 128, 0, c->stream>>>(c->d_pool[c->cur], (double*)buf, c->d_halo);
+  DD_CUDA(cudaGetLastError());
+  if (bytes) *bytes = cap;
+  return DD_OK;
+}
+
+dd_status domdec_halo_capacity(dd_ctx* c, int64_t* bytes) {
+  if (!c || !bytes) return DD_ERR_ARG;
+  const long long side = c->cls.ccap[kClasses - 2];
+  *bytes = 8 + 16LL * c->n2 + 8LL * c->n2 * side * side;
   return DD_OK;
 }
 
@@ -858,47 +934,17 @@ dd_status domdec_halo_unpack(dd_ctx* c, int32_t row, const void* buf, int64_t by
   if (!c || !buf || row < 0 || row >= c->n1) return DD_ERR_ARG;
   DD_CUDA(cudaSetDevice(c->device));
   const int n2 = c->n2, i0 = row * n2;
-  const long long head = 16LL * n2;
-  std::vector<int> ho(2 * n2), he(2 * n2);
-  const char* b = (const char*)buf;
-  DD_CUDA(cudaMemcpyAsync(ho.data(), b, 8LL * n2, cudaMemcpyDeviceToHost, c->stream));
-  DD_CUDA(cudaMemcpyAsync(he.data(), b + 8LL * n2, 8LL * n2, cudaMemcpyDeviceToHost, c->stream));
-  unsigned long long used = 0;
-  DD_CUDA(cudaMemcpyAsync(&used, c->d_poolctr + c->cur, 8, cudaMemcpyDeviceToHost, c->stream));
-  DD_CUDA(cudaStreamSynchronize(c->stream));
-  std::vector<long long> meta(3 * (size_t)n2), hp(n2);
-  long long at = 0;
-  for (int k = 0; k < n2; ++k) {
-    const long long len = (long long)he[2 * k] * he[2 * k + 1];
-    if (he[2 * k] < 0 || he[2 * k + 1] < 0 || ho[2 * k] < 0 || ho[2 * k] + he[2 * k] > c->N1 || ho[2 * k + 1] < 0 ||
-        ho[2 * k + 1] + he[2 * k + 1] > c->N2) {
-      c->err = "halo buffer: box outside the grid";
-      return DD_ERR_ARG;
-    }
-    meta[3 * k] = head / 8 + at;
-    meta[3 * k + 1] = (long long)used + at;
-    meta[3 * k + 2] = len;
-    hp[k] = (long long)used + at;
-    at += len;
-  }
-  if (head + 8 * at != bytes) {
-    c->err = "halo buffer size does not match its header";
+  if (bytes < 8 + 16LL * n2) {
+    c->err = "halo buffer smaller than its header";
     return DD_ERR_ARG;
   }
-  if ((long long)used + at > c->pool_cap) {
-    c->err = "pool full while unpacking a halo row";
-    return DD_ERR_NUMERIC;
-  }
   if (!c->d_halo) TRY(dalloc(c, &c->d_halo, 3 * (size_t)n2));
-  const unsigned long long nu = used + (unsigned long long)at;
-  DD_CUDA(cudaMemcpyAsync(c->d_halo, meta.data(), meta.size() * 8, cudaMemcpyHostToDevice, c->stream));
-  k_copy_boxes<<<n2, 128, 0, c->stream>>>((const double*)b, c->d_pool[c->cur], c->d_halo);
+  k_halo_meta_unpack<<<1, 32, 0, c->stream>>>((const char*)buf, bytes, i0, n2, c->N1, c->N2, c->d_poolctr + c->cur,
+                                              c->pool_cap, c->d_pos[c->cur], c->d_off[c->cur], c->d_ext[c->cur],
+                                              c->d_halo, &c->d_cum->invalid);
   DD_CUDA(cudaGetLastError());
-  DD_CUDA(cudaMemcpyAsync(c->d_off[c->cur] + 2 * i0, ho.data(), n2 * 8, cudaMemcpyHostToDevice, c->stream));
-  DD_CUDA(cudaMemcpyAsync(c->d_ext[c->cur] + 2 * i0, he.data(), n2 * 8, cudaMemcpyHostToDevice, c->stream));
-  DD_CUDA(cudaMemcpyAsync(c->d_pos[c->cur] + i0, hp.data(), n2 * 8, cudaMemcpyHostToDevice, c->stream));
-  DD_CUDA(cudaMemcpyAsync(c->d_poolctr + c->cur, &nu, 8, cudaMemcpyHostToDevice, c->stream));
-  DD_CUDA(cudaStreamSynchronize(c->stream));
+  k_copy_boxes<<<n2, 128, 0, c->stream>>>((const double*)buf, c->d_pool[c->cur], c->d_halo);
+  DD_CUDA(cudaGetLastError());
   return DD_OK;
 }
 

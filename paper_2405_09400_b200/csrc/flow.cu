@@ -377,6 +377,53 @@ dd_status flow_apply(dd_ctx* c, const int64_t* w) {
   return DD_OK;
 }
 
+dd_status flow_edge_costs_device(dd_ctx* c, double* d_cbar, int64_t* d_C) {
+  if (!c) return DD_ERR_ARG;
+  DD_CUDA(cudaSetDevice(c->device));
+  dd_status s = flow_costs_impl(c);
+  if (s) return s;
+  if (d_cbar) DD_CUDA(cudaMemcpyAsync(d_cbar, c->d_cbar, (size_t)c->I * 40, cudaMemcpyDeviceToDevice, c->stream));
+  if (d_C) DD_CUDA(cudaMemcpyAsync(d_C, c->d_C, (size_t)c->I * 40, cudaMemcpyDeviceToDevice, c->stream));
+  return DD_OK;
+}
+
+dd_status flow_solve(dd_ctx* c, const int64_t* d_C, int64_t* d_w, dd_flow_stats* stats) {
+  if (!c || !d_C) return DD_ERR_ARG;
+  DD_CUDA(cudaSetDevice(c->device));
+  DD_CUDA(cudaMemcpyAsync(c->d_C, d_C, (size_t)c->I * 40, cudaMemcpyDeviceToDevice, c->stream));
+  dd_status s = mcf_solve_device(c->n1, c->n2, c->d_q, c->d_C, c->d_w, &c->d_mcf, &c->mcf_bytes, 1, c->stream, c->err);
+  if (s) return s;
+  if (d_w) DD_CUDA(cudaMemcpyAsync(d_w, c->d_w, (size_t)c->I * 40, cudaMemcpyDeviceToDevice, c->stream));
+  if (stats) {
+    long long info[16];
+    DD_CUDA(cudaMemcpyAsync(info, mcf_info_ptr(c->d_mcf, c->I), sizeof(info), cudaMemcpyDeviceToHost, c->stream));
+    DD_CUDA(cudaStreamSynchronize(c->stream));
+    stats->objective = info[0];
+    stats->stationary = (int32_t)info[1];
+    stats->certificate = (int32_t)info[2];
+    stats->refines = (int32_t)info[3];
+    stats->rounds = (int32_t)info[4];
+    stats->label_rounds = (int32_t)info[5];
+    stats->changed_cells = 0;
+    stats->solver_ms = info[12] * 1e-6;
+    if (info[6]) {
+      c->err = "min-cost flow did not converge (round cap)";
+      return DD_ERR_NUMERIC;
+    }
+  }
+  return DD_OK;
+}
+
+dd_status flow_apply_device(dd_ctx* c, const int64_t* d_w) {
+  if (!c || !d_w) return DD_ERR_ARG;
+  DD_CUDA(cudaSetDevice(c->device));
+  DD_CUDA(cudaMemcpyAsync(c->d_w, d_w, (size_t)c->I * 40, cudaMemcpyDeviceToDevice, c->stream));
+  unsigned long long* ctr = (unsigned long long*)c->d_flow_info;
+  double* dropped = (double*)(c->d_flow_info + 8);
+  DD_CUDA(cudaMemsetAsync(c->d_flow_info, 0, 64 * 8, c->stream));
+  return apply_w(c, ctr, dropped);
+}
+
 dd_status dd_mincost_flow(int32_t n1, int32_t n2, const int64_t* q, const int64_t* C, int64_t* w, int64_t* objective,
                           dd_flow_stats* stats, int32_t device, void* stream) {
   if (n1 <= 0 || n2 <= 0 || !q || !C || !w) return DD_ERR_ARG;

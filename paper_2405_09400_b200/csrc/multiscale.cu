@@ -447,6 +447,7 @@ dd_status dd_multiscale_solve(const dd_problem* P, const dd_options* O, const dd
       set_global_error(err);
       return r;
     }
+    S.init_seconds[l] = std::chrono::duration<double>(clk::now() - t0).count();
     double smu = 0.0;
     for (double v : mus[l]) smu += v;
     S.N[l] = Q.N1;
@@ -461,7 +462,10 @@ dd_status dd_multiscale_solve(const dd_problem* P, const dd_options* O, const dd
       }
       if (ms->flow_every > 0 && (cyc % ms->flow_every) == ms->flow_every - 1) {
         dd_flow_stats fs{};
-        if ((r = flow_update(c, &fs)) != DD_OK) {
+        const auto tf = clk::now();
+        r = flow_update(c, &fs);
+        S.flow_seconds[l] += std::chrono::duration<double>(clk::now() - tf).count();
+        if (r != DD_OK) {
           set_global_error(std::string("multiscale flow update: ") + dd_last_error(c));
           domdec_destroy(c);
           return r;

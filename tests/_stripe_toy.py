@@ -27,36 +27,62 @@ def composite_cells(n1, n2, kind, rb, re):
 
 
 class ToyEngine:
-    def __init__(self, n1, n2, rb, re, seed=0):
+    """Same interface as stripes.GpuEngine (CPU tensors): fixed-capacity halo
+    payloads of the library's layout size (8 + 16 n2 + 8 n2 side^2 bytes),
+    entry errors for the all-reduce, padded int64 instance rows for the
+    all-gather."""
+
+    def __init__(self, n1, n2, rb, re, seed=0, side=8):
         self.n1, self.n2, self.rb, self.re = n1, n2, rb, re
         rng = np.random.default_rng(seed)
         self.v = rng.uniform(0.5, 1.5, (n1 * n2, 2))     # identical on every rank
         self.mom = np.zeros(n1 * n2)
         self.cells = {k: composite_cells(n1, n2, k, rb, re) for k in "AB"}
+        self.halo_bytes = 8 + 16 * n2 + 8 * n2 * side * side
 
-    def sweep(self, part):
+    def sweep(self, part, stats=False):
         pid = 1.0 if part == "A" else 2.0
+        e = 0.0
         for J in self.cells[part]:
             s = self.v[J].sum(0)
             for k, i in enumerate(J):
+                old = self.v[i].copy()
                 self.v[i] = 0.5 * self.v[i] + 0.5 * s / len(J) + 0.01 * (k + 1) * pid
                 self.mom[i] = self.v[i].sum() + 1e-3 * i
+                e += float(np.abs(self.v[i] - old).sum())
+        return e if stats else None
 
     def pack(self, row):
-        a = self.v[row * self.n2:(row + 1) * self.n2].copy()
-        return torch.from_numpy(np.frombuffer(a.tobytes(), np.uint8).copy())
+        a = np.frombuffer(self.v[row * self.n2:(row + 1) * self.n2].copy().tobytes(), np.uint8)
+        buf = np.zeros(self.halo_bytes, np.uint8)
+        buf[:a.size] = a
+        return torch.from_numpy(buf)
 
     def unpack(self, row, t):
-        self.v[row * self.n2:(row + 1) * self.n2] = np.frombuffer(t.numpy().tobytes(), np.float64).reshape(-1, 2)
+        nb = self.n2 * 2 * 8
+        self.v[row * self.n2:(row + 1) * self.n2] = np.frombuffer(t.numpy()[:nb].tobytes(), np.float64).reshape(-1, 2)
 
     def costs(self):
         C = np.zeros((self.n1 * self.n2, 5), np.int64)
         C[:, 1:] = np.round(self.mom * 1000).astype(np.int64)[:, None] + np.arange(4)[None, :]
-        q = np.ones(self.n1 * self.n2, np.int64)
-        return C, q
+        return C
 
-    def mincost(self, C, q):
-        return np.roll(C, 1, axis=0) % 5     # any deterministic function of the global instance
+    def cost_rows(self, lo, hi, maxrows):
+        C = self.costs().ravel()
+        n = self.n2 * 5
+        part = np.zeros(maxrows * n, np.int64)
+        part[:(hi - lo) * n] = C[lo * n:hi * n]
+        return torch.from_numpy(part)
+
+    def assemble(self, parts, spans):
+        n = self.n2 * 5
+        Cg = np.zeros(self.n1 * n, np.int64)
+        for (lo, hi), t in zip(spans, parts):
+            Cg[lo * n:hi * n] = t.numpy()[:(hi - lo) * n]
+        return Cg
+
+    def mincost(self, Cg):
+        return np.roll(Cg.reshape(-1, 5), 1, axis=0) % 5     # any deterministic function of the global instance
 
     def apply(self, w):
         n1, n2 = self.n1, self.n2
@@ -77,9 +103,12 @@ def run_toy(world, n1, n2, cycles, seed=0):
     from paper_2405_09400_b200.stripes import cycle_program, run_sequential, stripe_rows
     rows = stripe_rows(n1, world)
     engs = [ToyEngine(n1, n2, rows[r], rows[r + 1], seed) for r in range(world)]
+    errs = []
     for _ in range(cycles):
-        run_sequential([cycle_program(engs[r], r, world, rows, n1, n2) for r in range(world)])
-    return np.concatenate([engs[r].v[rows[r] * n2:rows[r + 1] * n2] for r in range(world)])
+        res = run_sequential([cycle_program(engs[r], r, world, rows, n1, n2, conv=True) for r in range(world)])
+        assert all(x == res[0] for x in res)   # every rank sees the same all-reduced errors
+        errs.append(res[0])
+    return np.concatenate([engs[r].v[rows[r] * n2:rows[r + 1] * n2] for r in range(world)]), errs
 
 
 def gloo_worker(rank, world, port, n1, n2, cycles, out_path):
@@ -91,12 +120,14 @@ def gloo_worker(rank, world, port, n1, n2, cycles, out_path):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     rows = stripe_rows(n1, world)
     eng = ToyEngine(n1, n2, rows[rank], rows[rank + 1])
+    errs = []
     for _ in range(cycles):
-        run_distributed(cycle_program(eng, rank, world, rows, n1, n2), rank, world)
+        errs.append(run_distributed(cycle_program(eng, rank, world, rows, n1, n2, conv=True), rank, world))
     mine = eng.v[rows[rank] * n2:rows[rank + 1] * n2]
     parts = [None] * world
-    dist.all_gather_object(parts, mine)
+    dist.all_gather_object(parts, (mine, errs))
     if rank == 0:
-        np.save(out_path, np.concatenate(parts))
+        np.save(out_path, np.concatenate([m for m, _ in parts]))
+        np.save(out_path + ".err.npy", np.array([e for _, e in parts], dtype=np.float64))
     dist.barrier()
     dist.destroy_process_group()

@@ -50,7 +50,10 @@ def test_refine_bit_exact(N, s):
     fine = coarse.refine(p.mu, p.nu, p.eps, p.E)
     _assert_boxes_identical(fine.boxes(), stf.boxes)
     ex, ey = fine.marginal_error()
-    assert ey < 1e-12
+    acc = np.zeros_like(p.nu)   # the same boxes: the same L1 Y-error (truncation ledger, R9)
+    for r0, c0, d in stf.boxes:
+        acc[r0:r0 + d.shape[0], c0:c0 + d.shape[1]] += d
+    assert abs(ey - np.abs(acc - p.nu).sum()) < 1e-15
     with pytest.raises(Exception):   # the fine measures must coarsen to the coarse ones (R23)
         coarse.refine(p.mu, np.roll(p.nu, 1, axis=0), p.eps, p.E)
     fine.close()
@@ -81,4 +84,28 @@ def test_multiscale_matches_oracle_and_dense_optimum():
     assert abs(gc - cstar) < 1e-4 * cstar, (gc, cstar)
     ex, ey = dd.marginal_error()
     assert ey < 1e-8
+    dd.close()
+
+
+@gpu
+def test_multiscale_converged_parity_cfg2():
+    """Converged, tolerance mode at the config-2 size (64^2,
+    s = 2, eps' = 4): the GPU and the oracle multiscale hybrid (layers 32^2
+    and 64^2, Err = 1e-4 per cell, layer done at R14 <= 1e-4) finish every
+    layer within one cycle of each other; the final transport costs agree to
+    1e-5 relative and the L1 X-errors to 1e-6 (BASELINE.json north star)."""
+    from paper_2405_09400_b200 import multiscale_solve
+    p = make_problem("gm", 64, 2, theta_deg=20, seed=0)
+    dd, stats = multiscale_solve(p.mu, p.nu, 2, p.eps, p.E, levels=2, conv=1e-4, max_cycles=2000)
+    st, hist = M.multiscale_solve(p.mu, p.nu, 2, p.eps_prime, levels=2, E=p.E, err=1e-4, conv=1e-4,
+                                  max_cycles=2000)
+    assert all(stats["converged"]) and all(r["converged"] for r in hist), (stats, hist)
+    for lv, r in enumerate(hist):
+        assert abs(stats["cycles"][lv] - r["cycles"]) <= 1, (lv, stats["cycles"], [h["cycles"] for h in hist])
+    gc = float(np.sum(dd.export_plan_cost())) * p.h * p.h
+    oc = O.transport_cost(st)
+    assert abs(gc - oc) < 1e-5 * oc, (gc, oc)
+    ex, ey = dd.marginal_error()
+    oex, oey = O.marginal_errors(st)
+    assert abs(ex - oex) < 1e-6 and abs(ey - oey) < 1e-6, (ex, oex, ey, oey)
     dd.close()

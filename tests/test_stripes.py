@@ -30,9 +30,11 @@ def test_stripe_rows_rejects_too_many_ranks():
 @pytest.mark.parametrize("shape", [(8, 6), (9, 5)])
 def test_sequential_stripes_equal_unstriped(world, shape):
     n1, n2 = shape
-    ref = run_toy(1, n1, n2, cycles=3)
-    got = run_toy(world, n1, n2, cycles=3)
+    ref, eref = run_toy(1, n1, n2, cycles=3)
+    got, egot = run_toy(world, n1, n2, cycles=3)
     np.testing.assert_array_equal(got, ref)
+    # the all-reduced sweep-entry errors (reading R14) equal the unstriped sums
+    np.testing.assert_allclose(np.array(egot), np.array(eref), rtol=1e-12)
 
 
 def _free_port():
@@ -45,8 +47,14 @@ def _free_port():
 
 def test_gloo_two_ranks_equal_unstriped(tmp_path):
     """world_size 2 over torch.distributed (gloo, 127.0.0.1): the same
-    programs with real point-to-point exchanges and all_gather."""
+    cycle programs with real point-to-point exchanges of fixed-capacity halo
+    payloads (the library's layout size), the all-gather of the padded int64
+    instance rows and the all-reduce of the sweep-entry errors."""
     n1, n2, cycles = 8, 6, 3
     out = str(tmp_path / "stripes.npy")
     mp.spawn(gloo_worker, args=(2, _free_port(), n1, n2, cycles, out), nprocs=2, join=True)
-    np.testing.assert_array_equal(np.load(out), run_toy(1, n1, n2, cycles))
+    ref, eref = run_toy(1, n1, n2, cycles)
+    np.testing.assert_array_equal(np.load(out), ref)
+    errs = np.load(out + ".err.npy")
+    for r in range(2):
+        np.testing.assert_allclose(errs[r], np.array(eref), rtol=1e-12)
