@@ -149,13 +149,12 @@ def lib():
 
 
 EXPORTED = ("domdec_init", "domdec_sweep", "flow_update", "marginal_error", "primal_dual_gap",
-            "domdec_export_cells", "domdec_export_alpha", "domdec_export_plan_cost", "domdec_export_cell_stats",
-            "flow_edge_costs",
-            "flow_apply", "dd_mincost_flow", "domdec_destroy", "dd_last_error", "dd_version", "domdec_counters",
-            "domdec_reset_counters", "dd_mufu_peak", "domdec_halo_pack", "domdec_halo_unpack",
-            "dd_sinkhorn_global", "domdec_init_product", "domdec_refine", "dd_multiscale_solve",
-            "domdec_export_cell_stats", "flow_edge_costs_device", "flow_solve", "flow_apply_device",
-            "domdec_halo_capacity")
+            "domdec_export_cells", "domdec_export_alpha", "domdec_export_plan_cost",
+            "domdec_export_cell_stats", "flow_edge_costs", "flow_apply", "dd_mincost_flow", "domdec_destroy",
+            "dd_last_error", "dd_version", "domdec_counters", "domdec_reset_counters", "dd_mufu_peak",
+            "domdec_halo_pack", "domdec_halo_unpack", "dd_sinkhorn_global", "domdec_init_product",
+            "domdec_refine", "dd_multiscale_solve", "flow_edge_costs_device", "flow_solve",
+            "flow_apply_device", "domdec_halo_capacity")
 
 
 def _problem(mu, nu, s, eps, h, E, off=None, ext=None, pos=None, data=None):
