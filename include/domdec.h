@@ -215,6 +215,21 @@ dd_status flow_edge_costs(dd_ctx *ctx, double *cbar, int64_t *C, int64_t *q);
  * then truncate + minimal box. */
 dd_status flow_apply(dd_ctx *ctx, const int64_t *w);
 
+/* Edge candidates of the flow update (Def. edge-candidates PAPER.md:409-412,
+ * Remark eps-gamma PAPER.md:543-559).  candidate 0: the
+ * product candidate mu_j/m_j (x) nu_i/m_i (default, reading R12); 1: the
+ * gluing candidate (Def. glued-plan) with gamma_ij the
+ * entropic OT plan between mu_i/m_i and mu_j/m_j for |x - x'|^2 with
+ * regularisation eps_gamma_p (pixel^2 units; the paper's (dx/2)^2 is 0.25;
+ * small values approach the optimal plan).  Selecting 1 computes the static
+ * gamma tables (fp64 Sinkhorn with eps-scaling, one warp per arc;
+ * DD_ERR_NUMERIC if an arc misses the 1e-12 marginal tolerance; cell_size
+ * <= 8) and makes every later sweep also record per pixel the plan's
+ * X-marginal and conditional mean displacement, from which flow_update's
+ * edge costs follow (reading R26).  The next flow update needs a
+ * sweep run after this call.  Synchronises. */
+dd_status flow_set_candidate(dd_ctx *ctx, int32_t candidate, double eps_gamma_p);
+
 /* Device-pointer variants of the flow-update hooks, fully asynchronous on
  * the ctx stream (stripe mode: the instance is all-gathered
  * over NCCL as a device tensor and solved by every rank):

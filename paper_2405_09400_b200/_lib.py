@@ -124,6 +124,7 @@ def lib():
             L.flow_solve.argtypes = [vp, vp, vp, C.POINTER(FlowStats)]
             L.flow_apply_device.argtypes = [vp, vp]
             L.domdec_halo_capacity.argtypes = [vp, C.POINTER(C.c_int64)]
+            L.flow_set_candidate.argtypes = [vp, C.c_int32, C.c_double]
         if hasattr(L, "dd_multiscale_solve"):
             L.domdec_init_product.argtypes = [C.POINTER(_Problem), C.POINTER(_Options), C.POINTER(vp)]
             L.domdec_refine.argtypes = [vp, C.POINTER(_Problem), C.POINTER(_Options), C.POINTER(vp)]
@@ -141,7 +142,7 @@ def lib():
                    "domdec_reset_counters", "dd_mufu_peak", "domdec_halo_pack", "domdec_halo_unpack",
                    "dd_sinkhorn_global", "domdec_init_product", "domdec_refine", "dd_multiscale_solve",
                    "domdec_export_cell_stats", "flow_edge_costs_device", "flow_solve", "flow_apply_device",
-                   "domdec_halo_capacity"):
+                   "domdec_halo_capacity", "flow_set_candidate"):
             if hasattr(L, fn):
                 getattr(L, fn).restype = C.c_int
         _lib = L
@@ -154,7 +155,7 @@ EXPORTED = ("domdec_init", "domdec_sweep", "flow_update", "marginal_error", "pri
             "dd_last_error", "dd_version", "domdec_counters", "domdec_reset_counters", "dd_mufu_peak",
             "domdec_halo_pack", "domdec_halo_unpack", "dd_sinkhorn_global", "domdec_init_product",
             "domdec_refine", "dd_multiscale_solve", "flow_edge_costs_device", "flow_solve",
-            "flow_apply_device", "domdec_halo_capacity")
+            "flow_apply_device", "domdec_halo_capacity", "flow_set_candidate")
 
 
 def _problem(mu, nu, s, eps, h, E, off=None, ext=None, pos=None, data=None):
@@ -287,6 +288,11 @@ class DomDec:
         n = C.c_int64()
         _check(lib().domdec_halo_pack(self._ctx, int(row), C.c_void_p(dev_ptr), int(cap), C.byref(n)), self._ctx)
         return n.value
+
+    def set_candidate(self, kind="product", eps_gamma_p=0.25):
+        """flow_set_candidate: "product" (R12) or "glued" (gluing candidates with
+        entropic gamma_ij)."""
+        _check(lib().flow_set_candidate(self._ctx, 0 if kind == "product" else 1, float(eps_gamma_p)), self._ctx)
 
     def halo_capacity(self):
         """Bytes of a halo buffer that holds any row (domdec_halo_capacity)."""

@@ -233,7 +233,7 @@ void free_ctx(dd_ctx* c) {
                   c->d_off[1], c->d_ext[0], c->d_ext[1], c->d_cells[0], c->d_cells[1], c->d_alpha[0],
                   c->d_alpha[1], c->d_gauge[0], c->d_gauge[1], c->d_stats[0], c->d_stats[1], c->d_totals[0],
                   c->d_totals[1], c->d_mom, c->d_xbar, c->d_var, c->d_cbar, c->d_C, c->d_w, c->d_mcf,
-                  c->d_flow_info, c->d_scratch, c->d_red, c->d_cls, c->d_cum, c->d_ecell, c->d_pd, c->d_halo};
+                  c->d_flow_info, c->d_scratch, c->d_red, c->d_cls, c->d_cum, c->d_pxm, c->d_gam, c->d_mu64, c->d_ecell, c->d_pd, c->d_halo};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -403,8 +403,12 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c, 
   long long init_total = 0;
   for (int i = 0; i < I; ++i) init_total += (long long)hext[2 * i] * hext[2 * i + 1];
   if (dev) init_total = std::max(init_total, dev->total);
-  const long long per_cell = c->opt.slot_cap > 0 ? c->opt.slot_cap : (long long)side * side;
-  c->pool_cap = std::max<long long>((long long)I * per_cell, 2 * init_total);
+  // a typical box side from the eps blur for every cell plus twice the
+  // initial data (the largest initial box must not size every cell's share:
+  // a refined multiscale layer has a few very wide boxes)
+  const int typ = 2 * s + 2 * (int)std::ceil(tail) + 12;
+  const long long per_cell = c->opt.slot_cap > 0 ? c->opt.slot_cap : (long long)typ * typ;
+  c->pool_cap = (long long)I * per_cell + 2 * init_total;
   // ---- device --------------------------------------------------------------
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= c->device) {
@@ -417,6 +421,7 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c, 
   TRY(dalloc(c, &c->d_mu, NN));
   TRY(dalloc(c, &c->d_log2mu, NN));
   TRY(dalloc(c, &c->d_nu, NN));
+  TRY(dalloc(c, &c->d_mu64, NN));
   TRY(dalloc(c, &c->d_m, I));
   TRY(dalloc(c, &c->d_q, I));
   TRY(dalloc(c, &c->d_mom, (size_t)I * 6));
@@ -475,6 +480,7 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c, 
   // mu / nu / masses / supplies
   DD_CUDA(cudaMemcpyAsync(c->d_nu, P->nu, NN * 8, cudaMemcpyHostToDevice, st));
   DD_CUDA(cudaMemcpyAsync(c->d_scratch, P->mu, NN * 8, cudaMemcpyHostToDevice, st));
+  DD_CUDA(cudaMemcpyAsync(c->d_mu64, P->mu, NN * 8, cudaMemcpyHostToDevice, st));
   k_init_mu<<<(unsigned)((NN + 255) / 256), 256, 0, st>>>(c->d_scratch, c->d_mu, c->d_log2mu, NN);
   DD_CUDA(cudaGetLastError());
   std::vector<int64_t> q(I);
@@ -611,6 +617,7 @@ dd_status domdec_sweep(dd_ctx* c, dd_partition part, dd_sweep_stats* stats) {
   p.totals = c->d_totals[b];
   p.cum = c->d_cum;
   p.mom = c->d_mom;
+  p.pxm = c->candidate ? c->d_pxm : nullptr;
   p.nu = c->d_nu;
   p.ecell = c->opt.track_primal ? c->d_ecell : nullptr;
   p.eps_p = c->eps_p;

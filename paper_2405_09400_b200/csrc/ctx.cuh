@@ -20,6 +20,7 @@ struct dd_ctx {
   float* d_mu = nullptr;
   float* d_log2mu = nullptr;
   double* d_nu = nullptr;
+  double* d_mu64 = nullptr;    // mu in fp64 (static tables of the gluing candidates)
   double* d_m = nullptr;
   int64_t* d_q = nullptr;
   double* d_pool[2] = {nullptr, nullptr};
@@ -52,6 +53,11 @@ struct dd_ctx {
   long long* d_halo = nullptr; // [3 * n2] halo pack/unpack metadata
   bool primal_valid = false;   // the last sweep recorded d_ecell
   double* d_mom = nullptr;   // [I][6] plan moments of the last sweep (R13)
+  // gluing edge candidates (flow_set_candidate)
+  int candidate = 0;           // 0 = product (R12), 1 = glued with entropic gamma_ij
+  double eps_gamma_p = 0.25;   // eps_gamma / h^2
+  double* d_pxm = nullptr;     // [N1*N2][3] PX(x), E[y - x | x] of the last sweep
+  double* d_gam = nullptr;     // [I][4][s^2][3] (b, delta) of gamma~_ij per pixel (static)
   double* d_ecell = nullptr; // [max ncells] primal score per composite cell of the last sweep / h^2
   double* d_pd = nullptr;    // [4 N1 N2 + ...] primal-dual gap scratch (allocated on first use)
   // flow update

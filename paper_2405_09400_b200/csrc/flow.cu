@@ -221,6 +221,152 @@ __global__ void k_apply_flow(const long long* __restrict__ w, const long long* _
   }
 }
 
+// ---- gluing edge candidates (Def. glued-plan
+// PAPER.md:531-541, Remark eps-gamma PAPER.md:543-559) ----------------------
+// gamma_ij in Pi(mu_i/m_i, mu_j/m_j) is the entropic OT plan for |x - x'|^2
+// with regularisation eps_g (pixel^2 units), computed once per problem (it
+// depends on mu only): one warp per (cell i, arc a), fp64 log-domain Sinkhorn
+// with eps-scaling (factor 4 per stage, 20 iterations per stage, then to an
+// L1 marginal error <= tol).  Stored per pixel x of X_i (row-major) as the
+// moments of its disintegration gamma~(. | x) about the cell centre z_i:
+// b = E[x'] - z_i (2) and delta = E|x' - z_i|^2 (1).
+constexpr int kGamWarps = 4;   // warps per block of k_gamma
+__global__ void k_gamma(const double* __restrict__ mu, int N2, int s, int n1, int n2, const double* __restrict__ m,
+                        double eps_g, double tol, int max_iter, double* __restrict__ gam,
+                        unsigned long long* __restrict__ nonconv) {
+  __shared__ double sh[kGamWarps][6][64];   // la, lb, fa, fb, pb, tmp
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const long long wid = (long long)blockIdx.x * kGamWarps + wl;
+  const int I = n1 * n2;
+  if (wid >= 4LL * I) return;
+  const int i = (int)(wid / 4), a = 1 + (int)(wid % 4);
+  const int j = nbr_cell(i, a, n1, n2);
+  const int P = s * s;
+  double* out = gam + (size_t)(4LL * i + (a - 1)) * P * 3;
+  if (j < 0) {
+    for (int p = lane; p < P; p += 32) out[3 * p] = out[3 * p + 1] = out[3 * p + 2] = 0.0;
+    return;
+  }
+  double* la = sh[wl][0];
+  double* lb = sh[wl][1];
+  double* fa = sh[wl][2];
+  double* fb = sh[wl][3];
+  double* pb = sh[wl][4];
+  const int i1 = i / n2, i2 = i % n2, j1 = j / n2, j2 = j % n2;
+  for (int p = lane; p < P; p += 32) {
+    la[p] = log(mu[(long long)(i1 * s + p / s) * N2 + i2 * s + p % s] / m[i]);
+    const double vb = mu[(long long)(j1 * s + p / s) * N2 + j2 * s + p % s] / m[j];
+    lb[p] = log(vb);
+    pb[p] = vb;
+    fa[p] = 0.0;
+    fb[p] = 0.0;
+  }
+  __syncwarp();
+  // D(p, q) = |x_p - x'_q|^2 in pixels (x' = x + (j - i) s offset)
+  const int dy = (j1 - i1) * s, dx = (j2 - i2) * s;
+  auto D = [&](int p, int q) {
+    const double d1 = (double)(q / s + dy - p / s), d2 = (double)(q % s + dx - p % s);
+    return d1 * d1 + d2 * d2;
+  };
+  double dmax = 0.0;
+  for (int p = 0; p < P; ++p)
+    for (int q = lane; q < P; q += 32) dmax = fmax(dmax, D(p, q));
+  for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  double e = fmax(dmax, eps_g), prev = e;
+  bool done = false;
+  int iters_left = max_iter;
+  while (!done) {
+    const bool last = e <= eps_g;
+    if (last) e = eps_g;
+    for (int p = lane; p < P; p += 32) { fa[p] *= prev / e; fb[p] *= prev / e; }
+    __syncwarp();
+    prev = e;
+    const double ie = 1.0 / e;
+    for (int it = 0; it < (last ? iters_left : 20); ++it) {
+      for (int q = lane; q < P; q += 32) {   // Y-side (second marginal) update
+        double mx = -INFINITY;
+        for (int p = 0; p < P; ++p) mx = fmax(mx, fa[p] + la[p] - D(p, q) * ie);
+        double sm = 0.0;
+        for (int p = 0; p < P; ++p) sm += exp(fa[p] + la[p] - D(p, q) * ie - mx);
+        fb[q] = -(mx + log(sm));
+      }
+      __syncwarp();
+      for (int p = lane; p < P; p += 32) {   // X-side update
+        double mx = -INFINITY;
+        for (int q = 0; q < P; ++q) mx = fmax(mx, fb[q] + lb[q] - D(p, q) * ie);
+        double sm = 0.0;
+        for (int q = 0; q < P; ++q) sm += exp(fb[q] + lb[q] - D(p, q) * ie - mx);
+        fa[p] = -(mx + log(sm));
+      }
+      __syncwarp();
+      if (last && (it % 10 == 9 || it == iters_left - 1)) {
+        double err = 0.0;   // L1 error of the second marginal
+        for (int q = lane; q < P; q += 32) {
+          double cs = 0.0;
+          for (int p = 0; p < P; ++p) cs += exp(fa[p] + fb[q] + la[p] + lb[q] - D(p, q) * ie);
+          err += fabs(cs - pb[q]);
+        }
+        for (int o = 16; o > 0; o >>= 1) err += __shfl_xor_sync(0xffffffffu, err, o);
+        if (err <= tol) break;
+        if (it == iters_left - 1 && lane == 0) atomicAdd(nonconv, 1ull);
+      }
+    }
+    if (last) done = true;
+    else e *= 0.25;
+  }
+  // moments of gamma~(. | x_p) about the cell centre z_i
+  const double zc = 0.5 * (double)(s - 1);
+  for (int p = lane; p < P; p += 32) {
+    double w = 0.0, b1 = 0.0, b2 = 0.0, dd = 0.0;
+    for (int q = 0; q < P; ++q) {
+      const double g = exp(fa[p] + fb[q] + lb[q] - D(p, q) / prev);
+      const double y1 = (double)(q / s + dy) - zc, y2 = (double)(q % s + dx) - zc;
+      w += g;
+      b1 += g * y1;
+      b2 += g * y2;
+      dd += g * (y1 * y1 + y2 * y2);
+    }
+    out[3 * p] = b1 / w;
+    out[3 * p + 1] = b2 / w;
+    out[3 * p + 2] = dd / w;
+  }
+}
+
+// Edge costs with gluing candidates (reading R26): for i != j,
+//   m_i c_bar_ij = sum_{x in X_i} PX(x) [(delta(x) - |u|^2) - 2 (b(x) - u) . (u + E[y - x | x])],
+// u = x - z_i, from the per-pixel records of the last sweep (PX, E[y - x | x])
+// and the static gamma tables; the product candidate is the special case
+// b = xbar_j - z_i, delta = V_j + |xbar_j - z_i|^2.
+__global__ void k_flow_costs_glued(const double* __restrict__ pxm, const double* __restrict__ gam,
+                                   const double* __restrict__ m, int N2, int n1, int n2, int s,
+                                   double* __restrict__ cbar, long long* __restrict__ C) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n1 * n2) return;
+  const int i1 = i / n2, i2 = i - i1 * n2, P = s * s;
+  const double zc = 0.5 * (double)(s - 1);
+  cbar[5 * i] = 0.0;
+  C[5 * i] = 0;
+  for (int a = 1; a < 5; ++a) {
+    if (nbr_cell(i, a, n1, n2) < 0) {
+      cbar[5 * i + a] = nan("");
+      C[5 * i + a] = 0;
+      continue;
+    }
+    const double* g = gam + (size_t)(4LL * i + (a - 1)) * P * 3;
+    double acc = 0.0;
+    for (int p = 0; p < P; ++p) {
+      const long long pix = (long long)(i1 * s + p / s) * N2 + i2 * s + p % s;
+      const double px = pxm[3 * pix], e1 = pxm[3 * pix + 1], e2 = pxm[3 * pix + 2];
+      const double u1 = (double)(p / s) - zc, u2 = (double)(p % s) - zc;
+      const double b1 = g[3 * p], b2 = g[3 * p + 1], dl = g[3 * p + 2];
+      acc += px * ((dl - (u1 * u1 + u2 * u2)) - 2.0 * ((b1 - u1) * (u1 + e1) + (b2 - u2) * (u2 + e2)));
+    }
+    const double cb = acc / m[i];
+    cbar[5 * i + a] = cb;
+    C[5 * i + a] = __double2ll_rn(cb * 1024.0);   // reading R11: round half even
+  }
+}
+
 __global__ void k_check_flow(const long long* __restrict__ w, const long long* __restrict__ q, int n1, int n2,
                              unsigned long long* __restrict__ bad) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -284,8 +430,17 @@ static dd_status apply_w(dd_ctx* c, unsigned long long* d_counters, double* d_dr
 }
 
 dd_status flow_costs_impl(dd_ctx* c) {
-  k_flow_costs<<<(c->I + 127) / 128, 128, 0, c->stream>>>(c->d_mom, c->d_xbar, c->d_var, c->d_m, c->n1, c->n2, c->s,
-                                                         c->d_cbar, (long long*)c->d_C);
+  if (c->candidate == 1) {
+    if (!c->d_gam) {
+      c->err = "gluing candidates selected but the gamma tables are missing";
+      return DD_ERR_PRECOND;
+    }
+    k_flow_costs_glued<<<(c->I + 127) / 128, 128, 0, c->stream>>>(c->d_pxm, c->d_gam, c->d_m, c->N2, c->n1, c->n2,
+                                                                 c->s, c->d_cbar, (long long*)c->d_C);
+  } else {
+    k_flow_costs<<<(c->I + 127) / 128, 128, 0, c->stream>>>(c->d_mom, c->d_xbar, c->d_var, c->d_m, c->n1, c->n2,
+                                                           c->s, c->d_cbar, (long long*)c->d_C);
+  }
   DD_CUDA(cudaGetLastError());
   return DD_OK;
 }
@@ -373,6 +528,41 @@ dd_status flow_apply(dd_ctx* c, const int64_t* w) {
   if (cnt[1]) {
     c->err = "flow apply: pool capacity exceeded or a cell annihilated (state invalid)";
     return DD_ERR_NUMERIC;
+  }
+  return DD_OK;
+}
+
+dd_status flow_set_candidate(dd_ctx* c, int32_t candidate, double eps_gamma_p) {
+  if (!c || (candidate != 0 && candidate != 1) || (candidate == 1 && !(eps_gamma_p > 0))) return DD_ERR_ARG;
+  DD_CUDA(cudaSetDevice(c->device));
+  c->candidate = candidate;
+  if (candidate == 0) return DD_OK;
+  const long long NN = (long long)c->N1 * c->N2;
+  const int P = c->s * c->s;
+  if (!c->d_pxm) {
+    DD_CUDA(cudaMalloc(&c->d_pxm, NN * 24));
+    DD_CUDA(cudaMemsetAsync(c->d_pxm, 0, NN * 24, c->stream));
+  }
+  if (!c->d_gam || c->eps_gamma_p != eps_gamma_p) {
+    if (!c->d_gam) DD_CUDA(cudaMalloc(&c->d_gam, (size_t)c->I * 4 * P * 3 * 8));
+    c->eps_gamma_p = eps_gamma_p;
+    if (P > 64) {
+      c->err = "gluing candidates need cell_size <= 8";
+      return DD_ERR_ARG;
+    }
+    unsigned long long* nc = (unsigned long long*)(c->d_flow_info + 32);
+    DD_CUDA(cudaMemsetAsync(nc, 0, 8, c->stream));
+    const long long warps = 4LL * c->I;
+    k_gamma<<<(unsigned)((warps + kGamWarps - 1) / kGamWarps), 32 * kGamWarps, 0, c->stream>>>(
+        c->d_mu64, c->N2, c->s, c->n1, c->n2, c->d_m, eps_gamma_p, 1e-12, 20000, c->d_gam, nc);
+    DD_CUDA(cudaGetLastError());
+    unsigned long long hnc = 0;
+    DD_CUDA(cudaMemcpyAsync(&hnc, nc, 8, cudaMemcpyDeviceToHost, c->stream));
+    DD_CUDA(cudaStreamSynchronize(c->stream));
+    if (hnc) {
+      c->err = "gamma_ij Sinkhorn did not reach its tolerance for " + std::to_string(hnc) + " arcs";
+      return DD_ERR_NUMERIC;
+    }
   }
   return DD_OK;
 }

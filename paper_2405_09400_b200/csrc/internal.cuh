@@ -83,6 +83,8 @@ struct SweepParams {
   const double* __restrict__ nu;      // [N1*N2] global nu (primal score only)
   double* __restrict__ ecell;         // [ncells] primal score of each returned plan / h^2
   double eps_p;                       // eps' = eps / h^2
+  double* __restrict__ pxm;           // [N1*N2][3] or NULL: per pixel PX(x) and E[y - x | x]
+                                      // of the last sweep's plan (gluing candidates, f1)
 };
 
 // Launch configuration of the size classes (host side, per context).

@@ -787,6 +787,12 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
         const double uu1 = (double)(k1 % s) - cen, uu2 = (double)(k2 % s) - cen;   // x - z_i
         const double px = (double)MU[t] * exp2((double)A2[t] - (double)A2n[t]);
         const double uu = uu1 * uu1 + uu2 * uu2;
+        if (p.pxm) {   // per pixel record for the gluing candidates (f1)
+          const long long pix = (long long)(cc.r0 + k1) * p.N2 + cc.c0 + k2;
+          p.pxm[3 * pix] = px;
+          p.pxm[3 * pix + 1] = Ee1;
+          p.pxm[3 * pix + 2] = Ee2;
+        }
         v[0] = px;
         v[1] = px * (uu1 + Ee1);
         v[2] = px * (uu2 + Ee2);
