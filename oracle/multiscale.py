@@ -21,9 +21,12 @@ Readings (R23-R25; the paper is silent on the details):
       evaluated in exactly this order in fp64, then truncated at tau with a
       minimal box (a5).  It is a feasible coupling: sum_i' nu_i' = nu and
       ||nu_i'|| = m_i' (up to the truncation ledger, R9), and coarsening it
-      back gives the coarse marginals (pinned).  Potentials are not
-      transferred: the first sweep of each partition on a layer starts from
-      alpha = 0 (reading R7).
+      back gives the coarse marginals (pinned).
+  R25' warm start: the physical dual potential is kept across the
+      refinement, so in units of eps (which drops 4x, R24) the fine
+      partition-A potential is a_f(x') = 4 a_l(parent(x')) (every fine A-cell
+      lies in one coarse A-cell, so the coarse per-cell constants are
+      harmless); partition B starts from alpha = 0 (reading R7).
   The coarsest layer starts from the product coupling pi = mu (x) nu, i.e.
   nu_i = m_i nu (a feasible coupling for any pair of measures).
 """
@@ -96,6 +99,8 @@ def refine_state(stc: OracleState, mu_f: np.ndarray, nu_f: np.ndarray, tau: floa
     st = OracleState(N1, N2, s, stc.eps_p, stc.h / 2.0, np.asarray(mu_f, np.float64),
                      np.asarray(nu_f, np.float64), m, n1, n2, boxes)
     st.dropped = stc.dropped + dropped
+    if stc.alpha.get("A") is not None:   # R25'
+        st.alpha["A"] = 4.0 * np.kron(stc.alpha["A"], np.ones((2, 2)))
     return st
 
 

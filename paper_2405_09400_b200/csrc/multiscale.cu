@@ -146,6 +146,39 @@ __global__ void k_refine(const double* __restrict__ pool_c, const long long* __r
     }
 }
 
+// Warm start of the fine layer's partition A from the coarse layer's A
+// potential (reading R25'): the physical potential alpha is kept, so in units
+// of eps the fine a is 4 times the coarse a at the parent pixel (eps drops 4x
+// per layer, R24).  Every fine A-cell lies inside one coarse A-cell (it is a
+// coarse basic cell), so the coarse per-cell gauge constants stay constant
+// over a fine cell.  The coarse value is taken back to the global gauge (up
+// to its cell constant) as A + 2 w (K - g).kappa (the re-gauge of the sweep
+// kernel), and the fine cell stores it with its gauge origin at its X-block
+// corner (D = 0), minus the value at that corner.  One CTA per fine A-cell.
+__global__ void k_alpha_refine(const float* __restrict__ alpha_c, const int* __restrict__ gauge_c, int N2c, int s,
+                               const CompCell* __restrict__ cells_f, int N2f, float w, float* __restrict__ alpha_f,
+                               int* __restrict__ gauge_f) {
+  const CompCell cc = cells_f[blockIdx.x];
+  const int ncolc = (N2c / s + 1) / 2;   // A-cell columns of the coarse grid
+  auto coarse_value = [&](int r, int c) {   // 4 (log2 units) x global-gauge coarse potential at fine pixel (r, c)
+    const int rc = r >> 1, cl = c >> 1;
+    const int K1 = rc - rc % (2 * s), K2 = cl - cl % (2 * s);
+    const int Jc = (rc / (2 * s)) * ncolc + cl / (2 * s);
+    const float a = alpha_c[(long long)rc * N2c + cl] +
+                    2.f * w * ((float)(K1 - gauge_c[2 * Jc]) * (rc - K1) + (float)(K2 - gauge_c[2 * Jc + 1]) * (cl - K2));
+    return 4.f * a;
+  };
+  const float ref = coarse_value(cc.r0, cc.c0);
+  for (int t = threadIdx.x; t < cc.n1 * cc.n2; t += blockDim.x) {
+    const int r = cc.r0 + t / cc.n2, c = cc.c0 + t % cc.n2;
+    alpha_f[(long long)r * N2f + c] = coarse_value(r, c) - ref;
+  }
+  if (threadIdx.x == 0) {
+    gauge_f[2 * blockIdx.x] = cc.r0;
+    gauge_f[2 * blockIdx.x + 1] = cc.c0;
+  }
+}
+
 std::string cuda_msg(const char* what, cudaError_t e) { return std::string(what) + ": " + cudaGetErrorString(e); }
 
 // Device buffers of one device-made initial coupling.
@@ -340,6 +373,18 @@ static dd_status refine_ctx(dd_ctx* c, const dd_problem* P, const dd_options* O,
     res = e == cudaErrorMemoryAllocation ? DD_ERR_OOM : DD_ERR_CUDA;
   } else if (res == DD_OK) {
     res = finish_staging(S, If, P, O, st, out, err);
+    if (res == DD_OK && c->alpha_valid[0] && !c->stripe && !(*out)->stripe) {
+      dd_ctx* f = *out;
+      k_alpha_refine<<<f->ncells[0], 64, 0, f->stream>>>(c->d_alpha[0], c->d_gauge[0], c->N2, s, f->d_cells[0], N2,
+                                                        (float)(1.4426950408889634 / f->eps_p), f->d_alpha[0],
+                                                        f->d_gauge[0]);
+      if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(f->stream)) != cudaSuccess) {
+        err = cuda_msg("refine: potential", e);
+        res = DD_ERR_CUDA;
+      } else {
+        f->alpha_valid[0] = 1;
+      }
+    }
   }
   cudaStreamSynchronize(st);
   for (void* p : {(void*)dnuf, (void*)dnuc, (void*)dry, (void*)dmf, (void*)dl1})

@@ -361,8 +361,9 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
   int* ints = (int*)(smem + Ls.ints);
   const int4 hull = cell_hull(p, cc, ints);
   const int L1 = hull.x, L2 = hull.y, b1 = hull.z, b2 = hull.w, BB = b1 * b2;
-  float* P1 = P0 + BB;                  // log2 nu_J
-  float* P2 = P0 + 2 * BB;              // BK
+  const int b2p = b2 + (b2 & 1);        // even row stride of BK (8-byte aligned pairs)
+  float* P1 = P0 + BB;                  // log2 nu_J - w l2^2
+  float* P2 = P0 + 2 * BB;              // BK [b1][b2p] (may extend into the 4th R2 array)
   float* Ub = (float*)(smem + Ls.U);
   float* Rb = Ub + NX * ccap;           // UK
   float* Vb = (float*)(smem + Ls.V);
@@ -386,7 +387,8 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
   for (int t = tid; t < BB; t += T) {
     const double v = nuJ[t];
     nsum += v;
-    P1[t] = v > 0.0 ? lg2f((float)v) : kNeg;   // log2 nu_J (zeros -> kNeg, R19)
+    const int l2 = t % b2;   // LNK = log2 nu_J - w l2^2 (zeros -> kNeg, R19)
+    P1[t] = v > 0.0 ? lg2f((float)v) - w * (float)(l2 * l2) : kNeg;
   }
   double muXJ = 0.0;
   for (int q = 0; q < nmem; ++q) muXJ += p.m[cc.mem[q]];
@@ -446,7 +448,9 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
   bool first = true;
   float* UK = Rb;                     // [NX][b2]  U - w k1^2
   float* VK = Vb + NX * ccap;         // [b1][NX]  V - w l1^2
-  float* BK = P2;                     // [b1][b2]  B + log2 nu_J - w l2^2
+  float* BK = P2;                     // [b1][b2p] B + log2 nu_J - w l2^2
+  if (b2 & 1)                         // padding column: a zero-weight term for X1's pairs
+    for (int l1 = tid; l1 < b1; l1 += T) BK[l1 * b2p + b2] = kNeg;
   const float w2 = 2.f * w;
   const float fo1 = (float)o1, fo2 = (float)o2;
   constexpr int HX = NX / 2;
@@ -462,128 +466,162 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
   const bool x2_valid = x2_pair < HX * NX;
   for (;;) {
     ++it;
-    // Y-half stage 1: U(k1, l2) = LSE_k2 [A + log2 mu - w (k2 - l2~)^2]
-    for (int o = tid, k1 = tid / b2, l2 = tid % b2; o < NX * b2;
-         o += T, k1 += T / b2, l2 += T % b2, (l2 >= b2 ? (l2 -= b2, ++k1) : 0)) {
-      const float x = (float)l2 - fo2;
-      const float wx = w2 * x;   // term q: fma(q, w2 x, a_q) (immediate q, no per-q constants live)
-      const float* ar = AL + k1 * NX;
-      float a[NX];
+    // Y-half stage 1: U(k1, l2) = LSE_k2 [A + log2 mu - w (k2 - l2~)^2].
+    // Terms in pairs (FFMA2 / FADD2 on {q, q+1}); the shift c is the max
+    // (first pass) or the previous output; a shifted sum outside
+    // [2^-60, 2^60] only sets a flag, and a thread with a flagged output
+    // recomputes all its outputs of the stage with a max shift (cold path).
+    {
+      bool bad = false;
+      auto y1_out = [&](const int o, const int k1, const int l2, const bool maxpass) {
+        const float x = (float)l2 - fo2;
+        const float wx = w2 * x;
+        const float2* ar = reinterpret_cast<const float2*>(AL + k1 * NX);
+        float2 a[HX];
 #pragma unroll
-      for (int q = 0; q < NX; ++q) a[q] = ar[q];
-      float c;
-      if (first) {
-        c = kNeg;
+        for (int q = 0; q < HX; ++q) a[q] = ar[q];
+        const float2 wx2 = make_float2(wx, wx);
+        float2 z[HX];
 #pragma unroll
-        for (int q = 0; q < NX; ++q) c = fmaxf(c, fmaf((float)q, wx, a[q]));
-      } else {
-        c = Ub[o] + w * x * x;
+        for (int q = 0; q < HX; ++q) z[q] = __ffma2_rn(make_float2((float)(2 * q), (float)(2 * q + 1)), wx2, a[q]);
+        float s0;   // U = s0 + lg2(sum) - w x^2 ... with c = s0' + w x^2 (see below)
+        float c;
+        if (maxpass) {
+          c = kNeg;
+#pragma unroll
+          for (int q = 0; q < HX; ++q) c = fmaxf(c, fmaxf(z[q].x, z[q].y));
+          s0 = c - w * x * x;
+        } else {
+          s0 = Ub[o];               // previous U: the shift is U_old + w x^2
+          c = fmaf(w * x, x, s0);
+        }
+        const float2 nc = make_float2(-c, -c);
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < HX; ++q) {
+          const float2 t = __fadd2_rn(z[q], nc);
+          acc = __fadd2_rn(acc, make_float2(ex2f(t.x), ex2f(t.y)));
+        }
+        const float sum = acc.x + acc.y;
+        bad |= !(sum > 0x1p-60f && sum < 0x1p60f);
+        const float U = s0 + lg2f(sum);
+        Ub[o] = U;
+        UK[o] = U - w * (float)(k1 * k1);
+      };
+      for (int o = tid, k1 = tid / b2, l2 = tid % b2; o < NX * b2;
+           o += T, k1 += T / b2, l2 += T % b2, (l2 >= b2 ? (l2 -= b2, ++k1) : 0))
+        y1_out(o, k1, l2, first);
+      if (bad) {   // cold path: this thread's outputs again with a true max shift
+        for (int o = tid, k1 = tid / b2, l2 = tid % b2; o < NX * b2;
+             o += T, k1 += T / b2, l2 += T % b2, (l2 >= b2 ? (l2 -= b2, ++k1) : 0))
+          y1_out(o, k1, l2, true);
       }
-      float sum = 0.f;
-#pragma unroll
-      for (int q = 0; q < NX; ++q) sum += ex2f(fmaf((float)q, wx, a[q]) - c);
-      if (!(sum > 0x1p-60f && sum < 0x1p60f)) {
-        c = kNeg;
-        for (int q = 0; q < NX; ++q) c = fmaxf(c, fmaf((float)q, wx, a[q]));
-        sum = 0.f;
-        for (int q = 0; q < NX; ++q) sum += ex2f(fmaf((float)q, wx, a[q]) - c);
-      }
-      const float U = c + lg2f(sum) - w * x * x;
-      Ub[o] = U;
-      UK[o] = U - w * (float)(k1 * k1);
     }
     __syncthreads();
-    // Y-half stage 2: B(l1, l2) = -LSE_k1 [U(k1, l2) - w (k1 - l1~)^2]
-    auto y2_column = [&](const int l2, const int l1_0, const int l1_step) {
-      float u[NX];
+    // Y-half stage 2: B(l1, l2) = -LSE_k1 [U(k1, l2) - w (k1 - l1~)^2]; the
+    // thread's column inputs stay in registers as pairs; BK rows have the
+    // even stride b2p (row b2p-1 of an odd b2 holds kNeg for X1's pairs).
+    {
+      bool bad = false;
+      auto y2_column = [&](const int l2, const int l1_0, const int l1_step, const bool maxpass) {
+        float2 u[HX];
 #pragma unroll
-      for (int q = 0; q < NX; ++q) u[q] = UK[q * b2 + l2];
-      const float wl2 = w * (float)(l2 * l2);
-      for (int l1 = l1_0; l1 < b1; l1 += l1_step) {
-        const int o = l1 * b2 + l2;
-        const float x = (float)l1 - fo1;
-        const float wx = w2 * x;
-        float c;
-        if (first) {
-          c = kNeg;
+        for (int q = 0; q < HX; ++q) u[q] = make_float2(UK[(2 * q) * b2 + l2], UK[(2 * q + 1) * b2 + l2]);
+        for (int l1 = l1_0; l1 < b1; l1 += l1_step) {
+          const int o = l1 * b2 + l2;
+          const float x = (float)l1 - fo1;
+          const float wx = w2 * x;
+          const float2 wx2 = make_float2(wx, wx);
+          float2 z[HX];
 #pragma unroll
-          for (int q = 0; q < NX; ++q) c = fmaxf(c, fmaf((float)q, wx, u[q]));
-        } else {
-          c = -P0[o] + w * x * x;
+          for (int q = 0; q < HX; ++q) z[q] = __ffma2_rn(make_float2((float)(2 * q), (float)(2 * q + 1)), wx2, u[q]);
+          float s0, c;
+          if (maxpass) {
+            c = kNeg;
+#pragma unroll
+            for (int q = 0; q < HX; ++q) c = fmaxf(c, fmaxf(z[q].x, z[q].y));
+            s0 = c - w * x * x;
+          } else {
+            s0 = -P0[o];            // previous B: the shift is -B_old + w x^2
+            c = fmaf(w * x, x, s0);
+          }
+          const float2 nc = make_float2(-c, -c);
+          float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int q = 0; q < HX; ++q) {
+            const float2 t = __fadd2_rn(z[q], nc);
+            acc = __fadd2_rn(acc, make_float2(ex2f(t.x), ex2f(t.y)));
+          }
+          const float sum = acc.x + acc.y;
+          bad |= !(sum > 0x1p-60f && sum < 0x1p60f);
+          const float Bv = -(s0 + lg2f(sum));
+          P0[o] = Bv;
+          BK[l1 * b2p + l2] = Bv + P1[o];   // P1 = log2 nu_J - w l2^2
         }
-        float sum = 0.f;
-#pragma unroll
-        for (int q = 0; q < NX; ++q) sum += ex2f(fmaf((float)q, wx, u[q]) - c);
-        if (!(sum > 0x1p-60f && sum < 0x1p60f)) {
-          c = kNeg;
-          for (int q = 0; q < NX; ++q) c = fmaxf(c, fmaf((float)q, wx, u[q]));
-          sum = 0.f;
-          for (int q = 0; q < NX; ++q) sum += ex2f(fmaf((float)q, wx, u[q]) - c);
-        }
-        const float Bv = -(c + lg2f(sum) - w * x * x);
-        P0[o] = Bv;
-        BK[o] = Bv + P1[o] - wl2;
+      };
+      if (b2 <= T) {
+        if (y2_rg < RG) y2_column(y2_col, y2_rg, RG, first);
+        if (bad) y2_column(y2_col, y2_rg, RG, true);
+      } else {   // hull wider than the CTA
+        for (int l2 = tid; l2 < b2; l2 += T) y2_column(l2, 0, 1, first);
+        if (bad)
+          for (int l2 = tid; l2 < b2; l2 += T) y2_column(l2, 0, 1, true);
       }
-    };
-    if (b2 <= T) {
-      if (y2_rg < RG) y2_column(y2_col, y2_rg, RG);
-    } else {   // hull wider than the CTA
-      for (int l2 = tid; l2 < b2; l2 += T) y2_column(l2, 0, 1);
     }
     __syncthreads();
     // X-half stage 1: V(l1, k2) = LSE_l2 [B + log2 nu_J - w (k2 - l2~)^2],
-    // two outputs (k2 = qa, qa + HX) per thread sharing the loaded BK
+    // two outputs (k2 = qa, qa + HX) per thread sharing every loaded BK pair
+    // (LDS.64 of {l2, l2+1}, FFMA2 / FADD2 on the pair).
     for (int t = tid; t < b1 * HX; t += T) {
       const int l1 = t / HX, qa = t % HX, qb = qa + HX;
       const float kta = (float)qa + fo2, ktb = (float)qb + fo2;   // k2 - l2~ = kt - l2
       const float ga = w2 * kta, gb = w2 * ktb;
-      const float* br = BK + l1 * b2;
+      const float2* br = reinterpret_cast<const float2*>(BK + l1 * b2p);
+      const int np = b2p >> 1;
       float ca, cb;
-      if (first) {
+      const bool maxpass = first;
+      auto maxshift = [&]() {
         ca = kNeg;
         cb = kNeg;
-        float lf = 0.f;
-        for (int l2 = 0; l2 < b2; ++l2, lf += 1.f) {
-          const float bk = br[l2];
-          ca = fmaxf(ca, fmaf(ga, lf, bk));
-          cb = fmaxf(cb, fmaf(gb, lf, bk));
+        float2 lf = make_float2(0.f, 1.f);
+        for (int k = 0; k < np; ++k) {
+          const float2 bk = br[k];
+          const float2 za = __ffma2_rn(make_float2(ga, ga), lf, bk), zb = __ffma2_rn(make_float2(gb, gb), lf, bk);
+          ca = fmaxf(ca, fmaxf(za.x, za.y));
+          cb = fmaxf(cb, fmaxf(zb.x, zb.y));
+          lf = __fadd2_rn(lf, make_float2(2.f, 2.f));
         }
+      };
+      if (maxpass) {
+        maxshift();
       } else {
         ca = Vb[l1 * NX + qa] + w * kta * kta;
         cb = Vb[l1 * NX + qb] + w * ktb * ktb;
       }
-      float sa = 0.f, sb = 0.f, sa1 = 0.f, sb1 = 0.f;
-      float lf = 0.f;
-      int l2 = 0;
-      for (; l2 + 1 < b2; l2 += 2, lf += 2.f) {
-        const float bk0 = br[l2], bk1 = br[l2 + 1];
-        sa += ex2f(fmaf(ga, lf, bk0) - ca);
-        sb += ex2f(fmaf(gb, lf, bk0) - cb);
-        sa1 += ex2f(fmaf(ga, lf + 1.f, bk1) - ca);
-        sb1 += ex2f(fmaf(gb, lf + 1.f, bk1) - cb);
-      }
-      if (l2 < b2) {
-        const float bk0 = br[l2];
-        sa += ex2f(fmaf(ga, lf, bk0) - ca);
-        sb += ex2f(fmaf(gb, lf, bk0) - cb);
-      }
-      sa += sa1;
-      sb += sb1;
-      if (!(sa > 0x1p-60f && sa < 0x1p60f) || !(sb > 0x1p-60f && sb < 0x1p60f)) {
-        ca = kNeg;
-        cb = kNeg;
-        float lg = 0.f;
-        for (int q = 0; q < b2; ++q, lg += 1.f) {
-          ca = fmaxf(ca, fmaf(ga, lg, br[q]));
-          cb = fmaxf(cb, fmaf(gb, lg, br[q]));
+      auto sums = [&](float2& sa, float2& sb) {
+        const float2 nca = make_float2(-ca, -ca), ncb = make_float2(-cb, -cb);
+        const float2 g2a = make_float2(ga, ga), g2b = make_float2(gb, gb);
+        sa = make_float2(0.f, 0.f);
+        sb = make_float2(0.f, 0.f);
+        float2 lf = make_float2(0.f, 1.f);
+#pragma unroll 2
+        for (int k = 0; k < np; ++k) {
+          const float2 bk = br[k];
+          const float2 ta = __fadd2_rn(__ffma2_rn(g2a, lf, bk), nca);
+          const float2 tb = __fadd2_rn(__ffma2_rn(g2b, lf, bk), ncb);
+          sa = __fadd2_rn(sa, make_float2(ex2f(ta.x), ex2f(ta.y)));
+          sb = __fadd2_rn(sb, make_float2(ex2f(tb.x), ex2f(tb.y)));
+          lf = __fadd2_rn(lf, make_float2(2.f, 2.f));
         }
-        sa = 0.f;
-        sb = 0.f;
-        lg = 0.f;
-        for (int q = 0; q < b2; ++q, lg += 1.f) {
-          sa += ex2f(fmaf(ga, lg, br[q]) - ca);
-          sb += ex2f(fmaf(gb, lg, br[q]) - cb);
-        }
+      };
+      float2 s2a, s2b;
+      sums(s2a, s2b);
+      float sa = s2a.x + s2a.y, sb = s2b.x + s2b.y;
+      if (!(sa > 0x1p-60f && sa < 0x1p60f) || !(sb > 0x1p-60f && sb < 0x1p60f)) {   // once per 2 x b2 terms
+        maxshift();
+        sums(s2a, s2b);
+        sa = s2a.x + s2a.y;
+        sb = s2b.x + s2b.y;
       }
       const float Va = ca + lg2f(sa) - w * kta * kta;
       const float Vbv = cb + lg2f(sb) - w * ktb * ktb;
@@ -745,7 +783,7 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
       const float kt = (float)k2 + fo2;   // lt2 - k2 = l2 - kt
       const float g = w2 * kt;
       const float c = Vb[t] + w * kt * kt;
-      const float* br = BK + l1 * b2;
+      const float* br = BK + l1 * b2p;
       float s0 = 0.f, s1 = 0.f, s2 = 0.f;
       float lf = 0.f, d = -kt;
       for (int l2 = 0; l2 < b2; ++l2, lf += 1.f, d += 1.f) {

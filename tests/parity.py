@@ -81,4 +81,5 @@ CONFIGS = {
     # configs[2]: 256x256, s = 4, eps sweep
     "cfg3_gm_eps2": lambda: make_problem("gm", 256, 4, eps_factor=2.0, theta_deg=5, seed=0),
     "cfg3_gm_eps4": lambda: make_problem("gm", 256, 4, eps_factor=4.0, theta_deg=5, seed=1),
+    "cfg3_gm_eps8": lambda: make_problem("gm", 256, 4, eps_factor=8.0, theta_deg=5, seed=2),
 }

@@ -13,8 +13,8 @@ gpu = pytest.mark.gpu
 
 
 @gpu
-@pytest.mark.parametrize("cfg", ["cfg1_gm", "cfg1_gm1", "cfg1_bumps_small_eps", "cfg2_gm", "cfg2_bumps"])
-@pytest.mark.parametrize("part", ["A", "B"])
+@pytest.mark.parametrize("cfg,part", [(c, p) for c in ["cfg1_gm", "cfg1_gm1", "cfg1_bumps_small_eps", "cfg2_gm",
+                                                       "cfg2_bumps"] for p in "AB"])
 def test_first_sweep_parity_fixed_iterations(cfg, part):
     """One sweep from the generated coupling (identical inputs: nu_I^0 exact,
     alpha = 0), exactly K Sinkhorn passes per cell on both sides: boxes
@@ -78,6 +78,35 @@ def test_pure_domdec_trajectory_parity(cfg, sweeps):
         assert abs(ex - oex) < 1e-6 and abs(ey - oey) < 1e-6, (k, ex, oex, ey, oey)
     cmp = compare_states(dd.boxes(), st.boxes)
     assert cmp["unexplained"] == 0, cmp
+
+
+@gpu
+@pytest.mark.parametrize("cfg,part", [("cfg3_gm_eps2", "B"), ("cfg3_gm_eps4", "A"), ("cfg3_gm_eps8", "A"),
+                                      ("cfg3_gm_eps8", "B")])
+def test_first_sweep_eps_sweep_sampled(cfg, part):
+    """Config 3's eps sweep ((2h)^2, (4h)^2, (8h)^2 at 256^2, s = 4; the large
+    eps routes cells through the M / L / X size classes): the GPU sweeps all
+    composite cells with exactly K passes, the oracle recomputes a sample of
+    cells on identical inputs; boxes bit-exact outside the guard band, values
+    within the fp32 tolerance."""
+    p = CONFIGS[cfg]()
+    K = 25
+    st = oracle_state(p)
+    comp = O.composite_partition(st.n1, st.n2, part)
+    rng = np.random.default_rng(3)
+    sample = sorted(set([0, len(comp) - 1] + list(rng.choice(len(comp), 14, replace=False))))
+    res = O.domdec_sweep(st, part, fixed_iter=K, cells=sample)
+    dd = gpu_ctx(p, fixed_iter=K)
+    gst = dd.sweep(part, stats=True)
+    assert gst["overflow"] == 0 and gst["iters_total"] == K * len(comp)
+    gb = dd.boxes()
+    rb, rt = rel_tols(p.eps_prime)
+    for k in sample:
+        for i, ob in res[k]["boxes"].items():
+            c = compare_cell(gb[i], ob)
+            assert c["box_equal"] or c["guard_ok"], (k, i, c)
+            assert c["rel_bulk"] < rb and c["rel_tail"] < rt, (k, i, c)
+    dd.close()
 
 
 def _check_integer_instance(cbar_o, q, C):
