@@ -27,6 +27,7 @@
 #include "ctx.cuh"
 
 namespace dd {
+long long* mcf_info_ptr(void* ws, int I);
 namespace {
 
 // out (N1/2 x N2/2) = 2x2 block sums of a (R23)
@@ -498,32 +499,63 @@ dd_status dd_multiscale_solve(const dd_problem* P, const dd_options* O, const dd
     S.N[l] = Q.N1;
     int cyc = 0;
     double emax = INFINITY;
+    // one host read-back per cycle (device-resident sweep totals and flow
+    // result, one synchronisation), flow updates timed with CUDA events
+    cudaEvent_t ef0 = nullptr, ef1 = nullptr;
+    cudaEventCreate(&ef0);
+    cudaEventCreate(&ef1);
+    auto fail = [&](const char* what, dd_status st) {
+      set_global_error(std::string(what) + dd_last_error(c));
+      cudaEventDestroy(ef0);
+      cudaEventDestroy(ef1);
+      domdec_destroy(c);
+      return st;
+    };
     for (cyc = 0; cyc < ms->max_cycles; ++cyc) {
-      dd_sweep_stats a{}, b{};
-      if ((r = domdec_sweep(c, DD_PART_A, &a)) != DD_OK || (r = domdec_sweep(c, DD_PART_B, &b)) != DD_OK) {
-        set_global_error(std::string("multiscale sweep: ") + dd_last_error(c));
-        domdec_destroy(c);
-        return r;
+      if ((r = domdec_sweep(c, DD_PART_A, nullptr)) != DD_OK || (r = domdec_sweep(c, DD_PART_B, nullptr)) != DD_OK)
+        return fail("multiscale sweep: ", r);
+      const bool doflow = ms->flow_every > 0 && (cyc % ms->flow_every) == ms->flow_every - 1;
+      if (doflow) {
+        cudaEventRecord(ef0, c->stream);
+        if ((r = flow_update(c, nullptr)) != DD_OK) return fail("multiscale flow update: ", r);
+        cudaEventRecord(ef1, c->stream);
       }
-      if (ms->flow_every > 0 && (cyc % ms->flow_every) == ms->flow_every - 1) {
-        dd_flow_stats fs{};
-        const auto tf = clk::now();
-        r = flow_update(c, &fs);
-        S.flow_seconds[l] += std::chrono::duration<double>(clk::now() - tf).count();
-        if (r != DD_OK) {
-          set_global_error(std::string("multiscale flow update: ") + dd_last_error(c));
-          domdec_destroy(c);
-          return r;
+      SweepTotals ta{}, tb{};
+      long long info[16] = {0};
+      unsigned long long fcnt[2] = {0, 0};
+      cudaMemcpyAsync(&ta, c->d_totals[0], sizeof(ta), cudaMemcpyDeviceToHost, c->stream);
+      cudaMemcpyAsync(&tb, c->d_totals[1], sizeof(tb), cudaMemcpyDeviceToHost, c->stream);
+      if (doflow) {
+        cudaMemcpyAsync(info, mcf_info_ptr(c->d_mcf, c->I), sizeof(info), cudaMemcpyDeviceToHost, c->stream);
+        cudaMemcpyAsync(fcnt, c->d_flow_info, sizeof(fcnt), cudaMemcpyDeviceToHost, c->stream);
+      }
+      if (cudaStreamSynchronize(c->stream) != cudaSuccess) {
+        c->err = cudaGetErrorString(cudaGetLastError());
+        return fail("multiscale cycle: ", DD_ERR_CUDA);
+      }
+      if (ta.overflow || tb.overflow) {
+        c->err = "box capacity exceeded or pool exhausted";
+        return fail("multiscale sweep: ", DD_ERR_NUMERIC);
+      }
+      if (doflow) {
+        float ms_f = 0.f;
+        cudaEventElapsedTime(&ms_f, ef0, ef1);
+        S.flow_seconds[l] += 1e-3 * ms_f;
+        if (info[6] || fcnt[1]) {
+          c->err = info[6] ? "min-cost flow did not converge" : "flow apply: pool exhausted";
+          return fail("multiscale flow update: ", DD_ERR_NUMERIC);
         }
-        S.flows[l] += fs.stationary ? 0 : 1;
+        S.flows[l] += info[1] ? 0 : 1;
       }
-      emax = std::max(a.l1x_entry, b.l1x_entry) / smu;
+      emax = std::max(ta.e0, tb.e0) / smu;
       if (emax <= ms->conv) {
         S.converged[l] = 1;
         ++cyc;
         break;
       }
     }
+    cudaEventDestroy(ef0);
+    cudaEventDestroy(ef1);
     S.cycles[l] = cyc;
     S.entry_error[l] = emax;
     S.seconds[l] = std::chrono::duration<double>(clk::now() - t0).count();

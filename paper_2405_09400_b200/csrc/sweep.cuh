@@ -508,13 +508,13 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
         Ub[o] = U;
         UK[o] = U - w * (float)(k1 * k1);
       };
-      for (int o = tid, k1 = tid / b2, l2 = tid % b2; o < NX * b2;
-           o += T, k1 += T / b2, l2 += T % b2, (l2 >= b2 ? (l2 -= b2, ++k1) : 0))
-        y1_out(o, k1, l2, first);
-      if (bad) {   // cold path: this thread's outputs again with a true max shift
+      // pass 1 (cold, flagged threads only): the outputs again with a true
+      // max shift; one call site keeps the stage's code compact (i-cache)
+      for (int pass = 0; pass < 2 && (pass == 0 || bad); ++pass) {
+        const bool mp = first || pass == 1;
         for (int o = tid, k1 = tid / b2, l2 = tid % b2; o < NX * b2;
              o += T, k1 += T / b2, l2 += T % b2, (l2 >= b2 ? (l2 -= b2, ++k1) : 0))
-          y1_out(o, k1, l2, true);
+          y1_out(o, k1, l2, mp);
       }
     }
     __syncthreads();
@@ -559,14 +559,13 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
           BK[l1 * b2p + l2] = Bv + P1[o];   // P1 = log2 nu_J - w l2^2
         }
       };
-      if (b2 <= T) {
-        if (y2_rg < RG) y2_column(y2_col, y2_rg, RG, first);
-        if (bad) y2_column(y2_col, y2_rg, RG, true);
-      } else {   // hull wider than the CTA
-        for (int l2 = tid; l2 < b2; l2 += T) y2_column(l2, 0, 1, first);
-        if (bad)
-          for (int l2 = tid; l2 < b2; l2 += T) y2_column(l2, 0, 1, true);
-      }
+      // columns in chunks of T when the hull is wider than the CTA; pass 1
+      // (cold, flagged threads only) with a true max shift; one call site
+      const int c0 = b2 <= T ? y2_col : tid, cstep = b2 <= T ? b2 : T;
+      const int r0 = b2 <= T ? y2_rg : 0, rstep = b2 <= T ? RG : 1;
+      if (b2 > T || y2_rg < RG)
+        for (int pass = 0; pass < 2 && (pass == 0 || bad); ++pass)
+          for (int l2 = c0; l2 < b2; l2 += cstep) y2_column(l2, r0, rstep, first || pass == 1);
     }
     __syncthreads();
     // X-half stage 1: V(l1, k2) = LSE_l2 [B + log2 nu_J - w (k2 - l2~)^2],
@@ -592,12 +591,7 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
           lf = __fadd2_rn(lf, make_float2(2.f, 2.f));
         }
       };
-      if (maxpass) {
-        maxshift();
-      } else {
-        ca = Vb[l1 * NX + qa] + w * kta * kta;
-        cb = Vb[l1 * NX + qb] + w * ktb * ktb;
-      }
+      ca = cb = 0.f;
       auto sums = [&](float2& sa, float2& sb) {
         const float2 nca = make_float2(-ca, -ca), ncb = make_float2(-cb, -cb);
         const float2 g2a = make_float2(ga, ga), g2b = make_float2(gb, gb);
@@ -615,13 +609,18 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
         }
       };
       float2 s2a, s2b;
-      sums(s2a, s2b);
-      float sa = s2a.x + s2a.y, sb = s2b.x + s2b.y;
-      if (!(sa > 0x1p-60f && sa < 0x1p60f) || !(sb > 0x1p-60f && sb < 0x1p60f)) {   // once per 2 x b2 terms
-        maxshift();
+      float sa = 0.f, sb = 0.f;
+      for (int pass = 0; pass < 2; ++pass) {   // pass 1: max shift after an out-of-range sum
+        if (maxpass || pass == 1) {
+          maxshift();
+        } else {
+          ca = Vb[l1 * NX + qa] + w * kta * kta;
+          cb = Vb[l1 * NX + qb] + w * ktb * ktb;
+        }
         sums(s2a, s2b);
         sa = s2a.x + s2a.y;
         sb = s2b.x + s2b.y;
+        if ((sa > 0x1p-60f && sa < 0x1p60f) && (sb > 0x1p-60f && sb < 0x1p60f)) break;
       }
       const float Va = ca + lg2f(sa) - w * kta * kta;
       const float Vbv = cb + lg2f(sb) - w * ktb * ktb;
