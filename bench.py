@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--s", type=int, default=CFG["s"])
     ap.add_argument("--no-ttc", action="store_true", help="skip the time-to-1e-4 runs")
     ap.add_argument("--ttc-cycles", type=int, default=6000)
-    ap.add_argument("--ttc-seconds", type=float, default=90.0)
+    ap.add_argument("--ttc-seconds", type=float, default=45.0)
     ap.add_argument("--ttc-flow-every", type=int, default=8,
                     help="flow period k of the single-scale 1024^2 time-to-1e-4 run (PAPER.md:750)")
     ap.add_argument("--no-extra", action="store_true", help="skip the eps-sweep / config-5 keys")
@@ -498,7 +498,8 @@ def run_ours(a, parallelism):
                     nfl += 1
                 t_sw += t2 - t1
                 t_fl += time.perf_counter() - t2
-                conv = allmax(max(sa_["l1x_entry"], sb_["l1x_entry"]))
+                ea_, eb_ = sa_["l1x_entry"], sb_["l1x_entry"]
+                conv = allmax(max(ea_, eb_) if np.isfinite(ea_) and np.isfinite(eb_) else float("inf"))
                 if conv <= 1e-4:
                     torch.cuda.synchronize()
                     res = {"seconds": allmax(time.perf_counter() - t0), "cycles": c + 1, "sweeps": 2 * (c + 1),

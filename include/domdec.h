@@ -144,9 +144,14 @@ dd_status domdec_init(const dd_problem *problem, const dd_options *options, dd_c
  * reading R7).  Per-cell stopping rule (readings R6/R6'):
  * sum_x mu |r - 2^(A - A')| <= err mu(X_J) after the Y-update, with
  * r = ||nu_J|| / mu(X_J) (1 unless truncation removed mass).  Cells that hit
- * max_iter are counted in stats->nonconverged, not an error.  Cells that
- * cannot be written (pool exhausted, annihilated box) keep their previous
- * marginals and make a stats call return DD_ERR_NUMERIC.  stats may be NULL
+ * max_iter are counted in stats->nonconverged, not an error.  A cell whose
+ * truncation would annihilate a member keeps its previous marginals (counted
+ * in stats->overflow; a stats call returns DD_ERR_NUMERIC).  If the marginal
+ * pool is exhausted the state is invalid: the sweep's stats call and every
+ * later synchronising call (marginal_error, domdec_counters) return
+ * DD_ERR_NUMERIC.  Cells are processed in size classes by hull side (one
+ * fused kernel per class); the result of a cell
+ * depends only on its inputs and its class.  stats may be NULL
  * (asynchronous). */
 dd_status domdec_sweep(dd_ctx *ctx, dd_partition part, dd_sweep_stats *stats);
 

@@ -16,6 +16,22 @@ namespace dd {
 void set_global_error(const std::string& m) { g_last_error = m; }
 }  // namespace dd
 
+// Context memory comes from the device's stream-ordered pool (cudaMallocAsync,
+// freed with cudaFreeAsync): multiscale layers and tests create and destroy
+// contexts of several GB, and the pool keeps freed memory mapped (release
+// threshold raised once per device) so that the next context does not pay
+// for page mapping again.
+void keep_device_pool(int dev) {
+  static bool done[256] = {};
+  if (dev < 0 || dev >= 256 || done[dev]) return;
+  cudaMemPool_t mp;
+  if (cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
 namespace {
 
 __global__ void k_init_mu(const double* __restrict__ mu, float* __restrict__ muf, float* __restrict__ l2,
@@ -216,7 +232,8 @@ std::vector<CompCell> build_partition(int n1, int n2, int s, int kind) {
 
 template <class T>
 dd_status dalloc(dd_ctx* c, T** p, size_t n) {
-  cudaError_t e = cudaMalloc((void**)p, n * sizeof(T) + 16);
+  keep_device_pool(c->device);
+  cudaError_t e = cudaMallocAsync((void**)p, n * sizeof(T) + 16, c->stream);
   if (e != cudaSuccess) {
     c->err = std::string("cudaMalloc: ") + cudaGetErrorString(e);
     return e == cudaErrorMemoryAllocation ? DD_ERR_OOM : DD_ERR_CUDA;
@@ -228,13 +245,19 @@ void free_ctx(dd_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  void* ptrs[] = {c->d_pos[0], c->d_pos[1], c->d_poolctr, c->d_scratch_huge,
-                  c->d_mu, c->d_log2mu, c->d_nu, c->d_m, c->d_q, c->d_pool[0], c->d_pool[1], c->d_off[0],
-                  c->d_off[1], c->d_ext[0], c->d_ext[1], c->d_cells[0], c->d_cells[1], c->d_alpha[0],
-                  c->d_alpha[1], c->d_gauge[0], c->d_gauge[1], c->d_stats[0], c->d_stats[1], c->d_totals[0],
-                  c->d_totals[1], c->d_mom, c->d_xbar, c->d_var, c->d_cbar, c->d_C, c->d_w, c->d_mcf,
-                  c->d_flow_info, c->d_scratch, c->d_red, c->d_cls, c->d_cum, c->d_pxm, c->d_gam, c->d_mu64, c->d_ecell, c->d_pd, c->d_halo};
-  for (void* p : ptrs)
+  // dalloc'd (stream-ordered pool) and cudaMalloc'd (flow / solver / diagnostics) memory
+  void* pooled[] = {c->d_pos[0], c->d_pos[1], c->d_poolctr, c->d_scratch_huge, c->d_mu, c->d_log2mu, c->d_nu,
+                    c->d_m, c->d_q, c->d_pool[0], c->d_pool[1], c->d_off[0], c->d_off[1], c->d_ext[0], c->d_ext[1],
+                    c->d_cells[0], c->d_cells[1], c->d_alpha[0], c->d_alpha[1], c->d_gauge[0], c->d_gauge[1],
+                    c->d_stats[0], c->d_stats[1], c->d_totals[0], c->d_totals[1], c->d_mom, c->d_scratch, c->d_red,
+                    c->d_cls, c->d_cum, c->d_mu64, c->d_ecell, c->d_halo};
+  void* plain[] = {c->d_xbar, c->d_var, c->d_cbar, c->d_C, c->d_w, c->d_mcf, c->d_flow_info, c->d_pxm, c->d_gam,
+                   c->d_pd};
+  for (void* p : pooled)
+    if (p) cudaFreeAsync(p, c->stream);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  else cudaDeviceSynchronize();
+  for (void* p : plain)
     if (p) cudaFree(p);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   if (c->aux) cudaStreamDestroy(c->aux);
@@ -442,7 +465,7 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c, 
     }
     if (c->opt.comp_cap > 0)   // testing knob: route larger hulls to the global-scratch class
       for (int k = 0; k < kClasses - 1; ++k) c->cls.ccap[k] = std::min(c->cls.ccap[k], c->opt.comp_cap);
-    TRY(dalloc(c, &c->d_scratch_huge, 16 * c->scratch_stride));
+    TRY(dalloc(c, &c->d_scratch_huge, (size_t)c->cls.grid[kClasses - 1] * c->scratch_stride));
     DD_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
     DD_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     DD_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));

@@ -26,6 +26,7 @@
 
 #include "ctx.cuh"
 
+void keep_device_pool(int dev);   // api.cu
 namespace dd {
 long long* mcf_info_ptr(void* ws, int I);
 namespace {
@@ -180,6 +181,12 @@ __global__ void k_alpha_refine(const float* __restrict__ alpha_c, const int* __r
   }
 }
 
+void keep_device_pool_ms() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  keep_device_pool(dev);
+}
+
 std::string cuda_msg(const char* what, cudaError_t e) { return std::string(what) + ": " + cudaGetErrorString(e); }
 
 // Device buffers of one device-made initial coupling.
@@ -190,13 +197,17 @@ struct Staging {
   int* ext = nullptr;
   unsigned long long* ctr = nullptr;   // [0] used, [1] fail
   double* dropped = nullptr;
+  cudaStream_t st = nullptr;            // the pool is stream-ordered (cudaMallocAsync)
   ~Staging() {
-    for (void* p : {(void*)pool, (void*)pos, (void*)off, (void*)ext, (void*)ctr, (void*)dropped})
+    if (pool) cudaFreeAsync(pool, st);
+    for (void* p : {(void*)pos, (void*)off, (void*)ext, (void*)ctr, (void*)dropped})
       if (p) cudaFree(p);
   }
-  cudaError_t alloc(int I, long long cap) {
+  cudaError_t alloc(int I, long long cap, cudaStream_t stream) {
     cudaError_t e;
-    if ((e = cudaMalloc(&pool, (size_t)cap * 8)) != cudaSuccess) return e;
+    st = stream;
+    keep_device_pool_ms();
+    if ((e = cudaMallocAsync(&pool, (size_t)cap * 8, st)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&pos, (size_t)I * 8)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&off, (size_t)I * 8)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&ext, (size_t)I * 8)) != cudaSuccess) return e;
@@ -269,7 +280,7 @@ static dd_status product_ctx(const dd_problem* P, const dd_options* O, dd_ctx** 
   const long long cap = (long long)I * B1 * B2;
   Staging S;
   double *dnu = nullptr, *dm = nullptr;
-  cudaError_t e = S.alloc(I, cap);
+  cudaError_t e = S.alloc(I, cap, st);
   if (e == cudaSuccess) e = cudaMalloc(&dnu, (size_t)N1 * N2 * 8);
   if (e == cudaSuccess) e = cudaMalloc(&dm, (size_t)I * 8);
   if (e == cudaSuccess) e = cudaMemcpyAsync(dnu, P->nu, (size_t)N1 * N2 * 8, cudaMemcpyHostToDevice, st);
@@ -334,7 +345,7 @@ static dd_status refine_ctx(dd_ctx* c, const dd_problem* P, const dd_options* O,
   for (int i = 0; i < Ic; ++i) cap += 16LL * cext[2 * i] * cext[2 * i + 1];
   Staging S;
   double *dnuf = nullptr, *dnuc = nullptr, *dry = nullptr, *dmf = nullptr, *dl1 = nullptr;
-  e = S.alloc(If, cap);
+  e = S.alloc(If, cap, st);
   if (e == cudaSuccess) e = cudaMalloc(&dnuf, NNf * 8);
   if (e == cudaSuccess) e = cudaMalloc(&dnuc, NNc * 8);
   if (e == cudaSuccess) e = cudaMalloc(&dry, NNf * 8);
@@ -547,7 +558,8 @@ dd_status dd_multiscale_solve(const dd_problem* P, const dd_options* O, const dd
         }
         S.flows[l] += info[1] ? 0 : 1;
       }
-      emax = std::max(ta.e0, tb.e0) / smu;
+      // a non-finite error never counts as converged
+      emax = (std::isfinite(ta.e0) && std::isfinite(tb.e0)) ? std::max(ta.e0, tb.e0) / smu : INFINITY;
       if (emax <= ms->conv) {
         S.converged[l] = 1;
         ++cyc;

@@ -16,7 +16,7 @@
 //   M  256 threads, 3 CTAs/SM
 //   L  512 threads, 2 CTAs/SM
 //   X  512 threads, 1 CTA/SM    (largest hull that fits 227 KB)
-//   H  512 threads, 16 CTAs on global-memory scratch (any hull; rare)
+//   H  512 threads, one CTA per SM on global-memory scratch (hull <= 1024; rare)
 // The large classes run on an auxiliary stream concurrently with S (fork /
 // join events), so their few long cells overlap the bulk instead of forming a
 // serial tail.  No host synchronisation inside a sweep.
@@ -98,11 +98,14 @@ cudaError_t sweep_classes(int s, int N, int nsm, int ncells, SweepClasses* out, 
     out->grid[C] = (int)(g > 0 ? g : 1);
     prev = cap;
   }
-  out->ccap[4] = N;
+  // H: any hull up to 1024 px on global-memory scratch (24 B per entry,
+  // 25 MB per CTA at 1024); one CTA per SM so that the few huge cells of a
+  // refined multiscale layer run side by side instead of in waves of 16
+  out->ccap[4] = N < 1024 ? N : 1024;
   out->threads[4] = kThreads[4];
   out->smem[4] = 0;
-  out->grid[4] = 16;
-  *scratch_stride = ((size_t)cell_layout(N, s, kThreads[4]).total + 255) & ~size_t(255);
+  out->grid[4] = nsm;
+  *scratch_stride = ((size_t)cell_layout(out->ccap[4], s, kThreads[4]).total + 255) & ~size_t(255);
   return cudaSuccess;
 }
 

@@ -713,8 +713,10 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
         A2n[oa] = ana;
         A2n[ob] = anb;
         // L1 X-marginal error of the plan (A, B): sum mu |r - 2^(A - A')| (R6')
+        // (padded pixels of ragged B cells carry mu = 0 and would give 0 * inf)
         const float rm1 = X[5 * NXX];   // (A2/A2n swap; X itself is fixed)
-        epart += MU[oa] * fabsf(exp2m1f(A2[oa] - ana) - rm1) + MU[ob] * fabsf(exp2m1f(A2[ob] - anb) - rm1);
+        if (MU[oa] > 0.f) epart += MU[oa] * fabsf(exp2m1f(A2[oa] - ana) - rm1);
+        if (MU[ob] > 0.f) epart += MU[ob] * fabsf(exp2m1f(A2[ob] - anb) - rm1);
         AL[oa] = ana + LM[oa] - wk2;   // AK of the next pass
         AL[ob] = anb + LM[ob] - wk2;
       }
