@@ -7,6 +7,15 @@ namespace dd {
 
 constexpr float kNeg = -1.0e30f;     // log of zero weight (reading R19), never NaN
 constexpr int kClasses = 5;          // size classes of the sweep (S, M, L, X, H)
+// Threads and target CTAs per SM of each size class.  Cells of s <= 2
+// (NX <= 4) carry a quarter of the work of s = 4 cells with the same per-cell
+// overheads, so their classes use half the threads and twice the CTAs.
+__host__ __device__ constexpr int class_threads(int NX, int C) {
+  return NX <= 4 ? (C == 0 ? 64 : C == 1 ? 128 : C == 2 ? 256 : 512) : (C == 0 ? 128 : C == 1 ? 256 : 512);
+}
+__host__ __device__ constexpr int class_min_blocks(int NX, int C) {
+  return NX <= 4 ? (C == 0 ? 14 : C == 1 ? 7 : C == 2 ? 3 : 1) : (C == 0 ? 7 : C == 1 ? 3 : C == 2 ? 2 : 1);
+}
 
 // One composite cell (Def. partitions).
 struct CompCell {

@@ -134,7 +134,7 @@ __device__ __forceinline__ long long floor_div(long long a, long long b) {   // 
 //     every node) along residual arcs v -> u with l = c_p + epsT;
 //   mode 2 (certificate): one node per cell, d(j) over the 4-neighbour arcs
 //     i -> j with the integer costs C (no negative cycle <=> converges).
-constexpr int TH = 16, TW = 32, TP = TW + 2, kSweeps = 32;
+constexpr int TH = 16, TW = 32, TP = TW + 2, kSweeps = 16;   // (sweeps per grid round: tuned on the bench trajectory, tools/mcf_knobs.py)
 
 __device__ __noinline__ bool tiled_bf(const McfArgs& A, cg::grid_group& grid, const int mode, const int par, const long long eps,
                          const int cap, long long gt, long long gs, int* rounds_used) {
@@ -933,7 +933,7 @@ dd_status mcf_solve_device(int n1, int n2, const int64_t* d_q, const int64_t* d_
   A.gu_every = 50;
   A.tiled = 1;
   A.tile_rounds = 16;
-  A.gu_tiled = 16;
+  A.gu_tiled = 8;
   A.alpha = 16;
   A.bf_sweeps = kSweeps;
   A.pr_cap = 0;

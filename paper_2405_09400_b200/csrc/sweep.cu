@@ -16,6 +16,7 @@
 //   M  256 threads, 3 CTAs/SM
 //   L  512 threads, 2 CTAs/SM
 //   X  512 threads, 1 CTA/SM    (largest hull that fits 227 KB)
+// (s <= 2: S 64 x 14, M 128 x 7, L 256 x 3, X 512 x 1; internal.cuh)
 //   H  512 threads, one CTA per SM on global-memory scratch (hull <= 1024; rare)
 // The large classes run on an auxiliary stream concurrently with S (fork /
 // join events), so their few long cells overlap the bulk instead of forming a
@@ -31,8 +32,6 @@ int sweep_occupancy_nx(int C, size_t smem);
 
 namespace {
 
-constexpr int kThreads[kClasses] = {128, 256, 512, 512, 512};
-constexpr int kMinBlocks[kClasses] = {7, 3, 2, 1, 1};
 
 // Bin every composite cell by the side of its hull (warp-aggregated atomics).
 __global__ void k_bin(const SweepParams p, const int4 caps) {
@@ -81,13 +80,14 @@ cudaError_t sweep_classes(int s, int N, int nsm, int ncells, SweepClasses* out, 
   const size_t per_sm = 228 * 1024, max_cta = 227 * 1024;
   int prev = 0;
   for (int C = 0; C < kClasses - 1; ++C) {
-    size_t budget = per_sm / kMinBlocks[C] - 1024;
+    const int nt = class_threads(2 * s, C);
+    size_t budget = per_sm / class_min_blocks(2 * s, C) - 1024;
     if (budget > max_cta) budget = max_cta;
     int cap = prev;
-    while (cap < N && cell_layout(cap + 1, s, kThreads[C]).total <= budget) ++cap;
+    while (cap < N && cell_layout(cap + 1, s, nt).total <= budget) ++cap;
     out->ccap[C] = cap;
-    out->threads[C] = kThreads[C];
-    out->smem[C] = cell_layout(cap > 0 ? cap : 1, s, kThreads[C]).total;
+    out->threads[C] = nt;
+    out->smem[C] = cell_layout(cap > 0 ? cap : 1, s, nt).total;
     int occ = 1;
     if (cap > 0) {
       occ = occupancy_s(s, C, out->smem[C]);
@@ -102,10 +102,10 @@ cudaError_t sweep_classes(int s, int N, int nsm, int ncells, SweepClasses* out, 
   // 25 MB per CTA at 1024); one CTA per SM so that the few huge cells of a
   // refined multiscale layer run side by side instead of in waves of 16
   out->ccap[4] = N < 1024 ? N : 1024;
-  out->threads[4] = kThreads[4];
+  out->threads[4] = class_threads(2 * s, 4);
   out->smem[4] = 0;
   out->grid[4] = nsm;
-  *scratch_stride = ((size_t)cell_layout(out->ccap[4], s, kThreads[4]).total + 255) & ~size_t(255);
+  *scratch_stride = ((size_t)cell_layout(out->ccap[4], s, out->threads[4]).total + 255) & ~size_t(255);
   return cudaSuccess;
 }
 

@@ -6,18 +6,15 @@
 
 namespace dd {
 
-constexpr int kClassThreads[kClasses] = {128, 256, 512, 512, 512};
-constexpr int kClassMinBlocks[kClasses] = {7, 3, 2, 1, 1};
-
 template <int NX, int C, bool PR>
 cudaError_t launch_class(const SweepParams& p, const SweepClasses& cls, cudaStream_t st) {
   constexpr bool GS = C == 4;
-  auto kern = sweep_kernel<NX, kClassThreads[C], kClassMinBlocks[C], PR, GS>;
+  auto kern = sweep_kernel<NX, class_threads(NX, C), class_min_blocks(NX, C), PR, GS>;
   if (cls.smem[C] > 48 * 1024) {   // per-device attribute: set on every launch (cheap)
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cls.smem[C]);
     if (e != cudaSuccess) return e;
   }
-  kern<<<cls.grid[C], kClassThreads[C], cls.smem[C], st>>>(p, C, cls.ccap[C]);
+  kern<<<cls.grid[C], class_threads(NX, C), cls.smem[C], st>>>(p, C, cls.ccap[C]);
   return cudaGetLastError();
 }
 
@@ -39,12 +36,13 @@ cudaError_t launch_sweep_nx(const SweepParams& p, const SweepClasses& cls, cudaS
 
 template <int NX, int C>
 int occupancy_of(size_t smem) {
-  auto kern = sweep_kernel<NX, kClassThreads[C], kClassMinBlocks[C], false, false>;
+  auto kern = sweep_kernel<NX, class_threads(NX, C), class_min_blocks(NX, C), false, false>;
   if (smem > 48 * 1024 &&   // the query counts 0 CTAs above the opt-in limit
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return -1;
   int per = 0;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kClassThreads[C], smem) == cudaSuccess ? per : -1;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, class_threads(NX, C), smem) == cudaSuccess ? per
+                                                                                                          : -1;
 }
 
 template <int NX>

@@ -542,8 +542,16 @@ def _lockstep_hybrid(p, cycles, on_sweep=None, **kw):
             if on_sweep is not None and on_sweep(cyc, part, st, ost, dd, gst):
                 return st, dd
         _, C, q = dd.edge_costs()
-        # the oracle's own a7 + R11 integer instance agrees with the GPU's
-        _check_integer_instance(O.edge_costs(st), q, C)
+        # the oracle's own a7 + R11 integer instance agrees with the GPU's: up
+        # to rounding-boundary arcs in parity mode; in tolerance mode the two
+        # sides may stop a cell's Sinkhorn one pass apart, so the costs agree
+        # to the Sinkhorn tolerance (1e-4 relative) instead
+        if "fixed_iter" in kw:
+            _check_integer_instance(O.edge_costs(st), q, C)
+        else:
+            oC, oq = O.integer_instance(O.edge_costs(st), q)
+            assert np.array_equal(oq, q)
+            assert np.all(np.abs(C - oC) <= 1 + 1e-4 * np.abs(oC)), np.abs(C - oC).max()
         w, obj, _ = mincost_flow(p.n, p.n, q, C)
         _, oobj = O.min_cost_flow(q, C, p.n, p.n)
         assert obj == min(oobj, 0), (cyc, obj, oobj)
