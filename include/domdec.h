@@ -167,6 +167,26 @@ dd_status domdec_sweep(dd_ctx *ctx, dd_partition part, dd_sweep_stats *stats);
  * stats may be NULL (asynchronous). */
 dd_status flow_update(dd_ctx *ctx, dd_flow_stats *stats);
 
+/* The hybrid iteration (Alg. 3) run to convergence on the
+ * device: cycles of sweep(A), sweep(B) and, every flow_every-th cycle, a
+ * flow update (flow_every = 0: plain DomDec, Alg. 2).
+ * Stops at the first cycle whose sweep-entry errors of both partitions,
+ * divided by ||mu||, are <= conv (reading R14), or after max_cycles.
+ * The cycles are launched as CUDA-graph units of G = 2 (flow_every = 0) or
+ * 2 flow_every cycles (an even number of pool flips, so one captured graph
+ * replays; the first unit runs eagerly and allocates), with one 32 G-byte
+ * device-to-host read of the per-cycle errors per unit; the state is
+ * therefore advanced to the end of the unit, up to G - 1 cycles past the
+ * converged one, and up to G - 1 past max_cycles.  Falls back to eager
+ * launches of the same unit when capture is unavailable.
+ * Outputs (each may be NULL): cycles = cycles executed; entry_error = the
+ * error of the first converged cycle, else of the last one; moved_flows =
+ * flow updates that changed the coupling (non-stationary).  Same results as
+ * the equivalent sequence of domdec_sweep / flow_update calls.  Not in
+ * stripe mode (DD_ERR_ARG).  Synchronises once per unit. */
+dd_status domdec_run_cycles(dd_ctx *ctx, int32_t max_cycles, int32_t flow_every, double conv, int32_t *cycles,
+                            double *entry_error, int32_t *moved_flows);
+
 /* L1 marginal errors (Table rows), fp64:
  * l1_x = sum_x |P_X pi(x) - mu(x)| of the last sweep's plans,
  * l1_y = sum_y |sum_i nu_i(y) - nu(y)| of the stored basic-cell marginals.

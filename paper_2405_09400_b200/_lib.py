@@ -130,6 +130,9 @@ def lib():
             L.domdec_refine.argtypes = [vp, C.POINTER(_Problem), C.POINTER(_Options), C.POINTER(vp)]
             L.dd_multiscale_solve.argtypes = [C.POINTER(_Problem), C.POINTER(_Options), C.POINTER(MsOptions),
                                               C.POINTER(vp), C.POINTER(MsStats)]
+        if hasattr(L, "domdec_run_cycles"):
+            L.domdec_run_cycles.argtypes = [vp, C.c_int32, C.c_int32, C.c_double, C.POINTER(C.c_int32),
+                                            C.POINTER(C.c_double), C.POINTER(C.c_int32)]
         L.domdec_counters.argtypes = [vp, C.POINTER(Counters)]
         L.domdec_reset_counters.argtypes = [vp]
         L.dd_mufu_peak.argtypes = [C.c_int32, C.POINTER(C.c_double)]
@@ -142,7 +145,7 @@ def lib():
                    "domdec_reset_counters", "dd_mufu_peak", "domdec_halo_pack", "domdec_halo_unpack",
                    "dd_sinkhorn_global", "domdec_init_product", "domdec_refine", "dd_multiscale_solve",
                    "domdec_export_cell_stats", "flow_edge_costs_device", "flow_solve", "flow_apply_device",
-                   "domdec_halo_capacity", "flow_set_candidate"):
+                   "domdec_halo_capacity", "flow_set_candidate", "domdec_run_cycles"):
             if hasattr(L, fn):
                 getattr(L, fn).restype = C.c_int
         _lib = L
@@ -155,7 +158,7 @@ EXPORTED = ("domdec_init", "domdec_sweep", "flow_update", "marginal_error", "pri
             "dd_last_error", "dd_version", "domdec_counters", "domdec_reset_counters", "dd_mufu_peak",
             "domdec_halo_pack", "domdec_halo_unpack", "dd_sinkhorn_global", "domdec_init_product",
             "domdec_refine", "dd_multiscale_solve", "flow_edge_costs_device", "flow_solve",
-            "flow_apply_device", "domdec_halo_capacity", "flow_set_candidate")
+            "flow_apply_device", "domdec_halo_capacity", "flow_set_candidate", "domdec_run_cycles")
 
 
 def _problem(mu, nu, s, eps, h, E, off=None, ext=None, pos=None, data=None):
@@ -266,6 +269,14 @@ class DomDec:
         st = FlowStats() if stats else None
         _check(lib().flow_update(self._ctx, C.byref(st) if st is not None else None), self._ctx)
         return st.as_dict() if st is not None else None
+
+    def run_cycles(self, max_cycles, flow_every=1, conv=1e-4):
+        """Hybrid cycles to convergence on the device (CUDA-graph units):
+        returns (cycles executed, entry error, non-stationary flow updates)."""
+        n, e, mv = C.c_int32(), C.c_double(), C.c_int32()
+        _check(lib().domdec_run_cycles(self._ctx, int(max_cycles), int(flow_every), float(conv), C.byref(n),
+                                       C.byref(e), C.byref(mv)), self._ctx)
+        return n.value, e.value, mv.value
 
     def marginal_error(self):
         x, y = C.c_double(), C.c_double()

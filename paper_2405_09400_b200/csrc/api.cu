@@ -252,7 +252,8 @@ void free_ctx(dd_ctx* c) {
                     c->d_stats[0], c->d_stats[1], c->d_totals[0], c->d_totals[1], c->d_mom, c->d_scratch, c->d_red,
                     c->d_cls, c->d_cum, c->d_mu64, c->d_ecell, c->d_halo};
   void* plain[] = {c->d_xbar, c->d_var, c->d_cbar, c->d_C, c->d_w, c->d_mcf, c->d_flow_info, c->d_pxm, c->d_gam,
-                   c->d_pd};
+                   c->d_pd, c->d_hist};
+  if (c->cyc_exec) cudaGraphExecDestroy(c->cyc_exec);
   for (void* p : pooled)
     if (p) cudaFreeAsync(p, c->stream);
   if (c->stream) cudaStreamSynchronize(c->stream);
@@ -798,6 +799,164 @@ dd_status domdec_export_plan_cost(dd_ctx* c, double* Qm) {
   // <c, pi_i> = sum_y nu_i^pre(y) E[|x - y|^2 | y] = G0 - 2 G1 + M2 (centred moments)
   for (int i = 0; i < c->I; ++i) Qm[i] = mom[6 * i + 3] - 2.0 * mom[6 * i + 4] + mom[6 * i + 5];
   return DD_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// One cycle's record: the sweep-entry errors of A and B, 1 if the cycle's
+// flow update moved mass (solver info[1] = stationary flag), and a failure
+// flag (box overflow in a sweep, min-cost flow round cap, pool exhausted in
+// the flow apply).  info / fcnt are null when the cycle has no flow update.
+__global__ void k_record_cycle(const SweepTotals* __restrict__ ta, const SweepTotals* __restrict__ tb,
+                               const long long* __restrict__ info, const unsigned long long* __restrict__ fcnt,
+                               double* __restrict__ dst) {
+  dst[0] = ta->e0;
+  dst[1] = tb->e0;
+  dst[2] = info && !info[1] ? 1.0 : 0.0;
+  dst[3] = (ta->overflow || tb->overflow || (info && info[6]) || (fcnt && fcnt[1])) ? 1.0 : 0.0;
+}
+
+// One unit of G hybrid cycles on the ctx stream (recording the entry errors);
+// host bookkeeping is done by the caller.
+dd_status enqueue_cycles(dd_ctx* c, int G, int flow_every, int* flows) {
+  *flows = 0;
+  for (int k = 0; k < G; ++k) {
+    for (int b = 0; b < 2; ++b) {
+      dd_status s = domdec_sweep(c, (dd_partition)b, nullptr);
+      if (s) return s;
+    }
+    const bool doflow = flow_every > 0 && k % flow_every == flow_every - 1;
+    if (doflow) {
+      dd_status s = flow_update_impl(c, nullptr);
+      if (s) return s;
+      ++*flows;
+    }
+    k_record_cycle<<<1, 1, 0, c->stream>>>(c->d_totals[0], c->d_totals[1],
+                                           doflow ? mcf_info_ptr(c->d_mcf, c->I) : nullptr,
+                                           doflow ? (const unsigned long long*)c->d_flow_info : nullptr,
+                                           c->d_hist + 4 * k);
+    DD_CUDA(cudaGetLastError());
+  }
+  return DD_OK;
+}
+}  // namespace
+
+extern "C" {
+
+dd_status domdec_run_cycles(dd_ctx* c, int32_t max_cycles, int32_t flow_every, double conv, int32_t* cycles,
+                            double* entry_error, int32_t* moved_flows) {
+  if (!c || max_cycles < 1 || flow_every < 0) return DD_ERR_ARG;
+  if (c->stripe) {
+    c->err = "stripe mode: use the cycle program of stripes.py";
+    return DD_ERR_ARG;
+  }
+  DD_CUDA(cudaSetDevice(c->device));
+  // graph unit: G cycles with an even number of pool flips (each sweep and
+  // each flow update flips the double-buffered pool), so every replay starts
+  // from the same buffers: 2G sweeps + G / flow_every updates
+  const int G = flow_every == 0 ? 2 : 2 * flow_every;
+  if (!c->d_hist || G > c->cyc_G) {
+    if (c->d_hist) cudaFree(c->d_hist);
+    c->d_hist = nullptr;
+    DD_CUDA(cudaMalloc(&c->d_hist, (size_t)4 * G * sizeof(double)));
+  }
+  double smu = 0.0;
+  {
+    std::vector<double> hm(c->I);
+    DD_CUDA(cudaMemcpyAsync(hm.data(), c->d_m, (size_t)c->I * 8, cudaMemcpyDeviceToHost, c->stream));
+    DD_CUDA(cudaStreamSynchronize(c->stream));
+    for (double v : hm) smu += v;
+  }
+  int done = 0, moved = 0;
+  double emax = INFINITY;
+  std::vector<double> hist(4 * (size_t)G);
+  // read the unit's history back (one D2H per unit) and scan it: converged
+  // once a cycle meets conv (emax = that cycle's error; the rest of its unit
+  // has run as well)
+  bool converged = false;
+  auto fetch = [&]() -> dd_status {
+    unsigned long long invalid = 0;
+    DD_CUDA(cudaMemcpyAsync(hist.data(), c->d_hist, hist.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+    DD_CUDA(cudaMemcpyAsync(&invalid, &c->d_cum->invalid, 8, cudaMemcpyDeviceToHost, c->stream));
+    DD_CUDA(cudaStreamSynchronize(c->stream));
+    if (invalid) {
+      c->err = "marginal pool exhausted in a sweep: the state is invalid";
+      return DD_ERR_NUMERIC;
+    }
+    for (int k = 0; k < G; ++k) {
+      if (hist[4 * k + 3] != 0.0) {
+        c->err = "box capacity exceeded, min-cost flow round cap or flow-apply pool exhausted";
+        return DD_ERR_NUMERIC;
+      }
+    }
+    for (int k = 0; k < G; ++k) {
+      const double a = hist[4 * k], b = hist[4 * k + 1];
+      moved += hist[4 * k + 2] > 0.5 ? 1 : 0;
+      ++done;
+      if (converged) continue;   // keep the error of the first converged cycle
+      emax = (std::isfinite(a) && std::isfinite(b)) ? std::max(a, b) / smu : INFINITY;
+      converged = emax <= conv;
+    }
+    return DD_OK;
+  };
+  auto finish = [&]() {
+    if (cycles) *cycles = done;
+    if (entry_error) *entry_error = emax;
+    if (moved_flows) *moved_flows = moved;
+    return DD_OK;
+  };
+  // warm-up unit, uncaptured: both partitions swept, the flow workspace
+  // allocated (nothing may allocate inside a capture)
+  const bool need_warm = c->swept != 3 || (flow_every > 0 && !c->d_mcf) || c->cyc_flow_every != flow_every ||
+                         c->cyc_G != G || !c->cyc_exec;
+  if (need_warm) {
+    int fl = 0;
+    dd_status s = enqueue_cycles(c, G, flow_every, &fl);
+    if (s) return s;
+    if ((s = fetch())) return s;
+    if (converged || done >= max_cycles) return finish();
+    // capture one unit; host state is saved and restored around the capture
+    if (c->cyc_exec) cudaGraphExecDestroy(c->cyc_exec);
+    c->cyc_exec = nullptr;
+    const int cur0 = c->cur, last0 = c->last_part, swept0 = c->swept;
+    const long long ns0 = c->n_sweeps, nf0 = c->n_flows;
+    const bool pv0 = c->primal_valid;
+    cudaGraph_t g = nullptr;
+    bool ok = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+      dd_status es = enqueue_cycles(c, G, flow_every, &fl);
+      ok = cudaStreamEndCapture(c->stream, &g) == cudaSuccess && es == DD_OK;
+      if (ok) ok = cudaGraphInstantiate(&c->cyc_exec, g, 0) == cudaSuccess;
+      if (g) cudaGraphDestroy(g);
+    }
+    cudaGetLastError();   // a failed capture leaves a sticky-free error state
+    c->cur = cur0; c->last_part = last0; c->swept = swept0;
+    c->n_sweeps = ns0; c->n_flows = nf0; c->primal_valid = pv0;
+    c->cyc_G = G;
+    c->cyc_flow_every = flow_every;
+    c->cyc_flows = fl;
+    if (!ok) {
+      if (c->cyc_exec) cudaGraphExecDestroy(c->cyc_exec);
+      c->cyc_exec = nullptr;
+    }
+  }
+  while (done < max_cycles) {
+    int fl = c->cyc_flows;
+    if (c->cyc_exec) {
+      DD_CUDA(cudaGraphLaunch(c->cyc_exec, c->stream));
+      c->n_sweeps += 2 * G;
+      c->n_flows += fl;
+      c->last_part = 1;
+    } else {   // capture unsupported here: the same unit, launched eagerly
+      dd_status s = enqueue_cycles(c, G, flow_every, &fl);
+      if (s) return s;
+    }
+    dd_status s = fetch();
+    if (s) return s;
+    if (converged) break;
+  }
+  return finish();
 }
 
 dd_status flow_update(dd_ctx* c, dd_flow_stats* stats) {

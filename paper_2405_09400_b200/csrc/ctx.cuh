@@ -52,6 +52,11 @@ struct dd_ctx {
   bool stripe = false;
   long long* d_halo = nullptr; // [3 * n2] halo pack/unpack metadata
   bool primal_valid = false;   // the last sweep recorded d_ecell
+  // domdec_run_cycles: a CUDA graph of G hybrid cycles and the per-sweep
+  // entry errors it records on the device
+  cudaGraphExec_t cyc_exec = nullptr;
+  int cyc_G = 0, cyc_flow_every = -1, cyc_flows = 0;
+  double* d_hist = nullptr;    // [2 G] sweep-entry errors of the last graph replay
   double* d_mom = nullptr;   // [I][6] plan moments of the last sweep (R13)
   // gluing edge candidates (flow_set_candidate)
   int candidate = 0;           // 0 = product (R12), 1 = glued with entropic gamma_ij
@@ -93,6 +98,7 @@ dd_status flow_apply_impl(dd_ctx* c);
 dd_status mcf_solve_device(int n1, int n2, const int64_t* d_q, const int64_t* d_C, int64_t* d_w,
                            void** d_ws, size_t* ws_bytes, int warm, cudaStream_t st, std::string& err);
 dd_status flow_init_static(dd_ctx* c);
+long long* mcf_info_ptr(void* ws, int I);
 dd_status pd_gap_impl(dd_ctx* c, double* primal, double* dual, double* rel_gap, double* transport);
 void set_global_error(const std::string& m);   // dd_last_error(NULL)
 }  // namespace dd
