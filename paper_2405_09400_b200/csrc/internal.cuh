@@ -102,6 +102,10 @@ struct SweepClasses {
   int threads[kClasses];
   int grid[kClasses];      // persistent CTAs per class
   size_t smem[kClasses];   // dynamic shared memory per CTA (0 for H: global scratch)
+  // H on thread-block clusters (sweep_cluster.cuh): cl_size CTAs per cell,
+  // cl_grid CTAs, cl_smem bytes of dynamic shared memory each; 0 = off
+  int cl_size, cl_grid;
+  size_t cl_smem;
 };
 cudaError_t sweep_classes(int s, int N, int nsm, int ncells, SweepClasses* out, size_t* scratch_stride);
 cudaError_t launch_sweep(const SweepParams& p, const SweepClasses& cls, cudaStream_t st, cudaStream_t aux,

@@ -22,6 +22,7 @@
 // join events), so their few long cells overlap the bulk instead of forming a
 // serial tail.  No host synchronisation inside a sweep.
 #include "sweep.cuh"
+#include <cstdlib>
 
 namespace dd {
 
@@ -29,6 +30,8 @@ template <int NX>
 cudaError_t launch_sweep_nx(const SweepParams& p, const SweepClasses& cls, cudaStream_t st, cudaStream_t aux);
 template <int NX>
 int sweep_occupancy_nx(int C, size_t smem);
+template <int NX>
+int cluster_capacity_nx(int KC, size_t smem);
 
 namespace {
 
@@ -72,6 +75,15 @@ int occupancy_s(int s, int C, size_t smem) {
   }
 }
 
+int cluster_capacity_s(int s, int KC, size_t smem) {
+  switch (s) {
+    case 1: return cluster_capacity_nx<2>(KC, smem);
+    case 2: return cluster_capacity_nx<4>(KC, smem);
+    case 4: return cluster_capacity_nx<8>(KC, smem);
+    default: return cluster_capacity_nx<16>(KC, smem);
+  }
+}
+
 }  // namespace
 
 cudaError_t sweep_classes(int s, int N, int nsm, int ncells, SweepClasses* out, size_t* scratch_stride) {
@@ -106,6 +118,26 @@ cudaError_t sweep_classes(int s, int N, int nsm, int ncells, SweepClasses* out, 
   out->smem[4] = 0;
   out->grid[4] = nsm;
   *scratch_stride = ((size_t)cell_layout(out->ccap[4], s, out->threads[4]).total + 255) & ~size_t(255);
+  // H on clusters of 8 CTAs (one per SM, 160 KB of shared memory each for the
+  // rows of the cell; sweep_cluster.cuh), a cluster per 8 SMs.  Test knobs:
+  // DD_H_CLUSTER = cluster size (0: the single-CTA path), DD_H_CLUSTER_KB =
+  // shared memory per CTA (a small value sends every cell to the leader-only
+  // fallback).
+  out->cl_size = 0;
+  out->cl_grid = 0;
+  out->cl_smem = 0;
+  const char* env = getenv("DD_H_CLUSTER");
+  const char* envkb = getenv("DD_H_CLUSTER_KB");
+  const int KC = env ? atoi(env) : 8;
+  if (KC == 2 || KC == 4 || KC == 8) {
+    const size_t sm = (size_t)(envkb && atoi(envkb) > 0 ? atoi(envkb) : 160) * 1024;
+    if (cluster_capacity_s(s, KC, sm) > 0) {
+      out->cl_size = KC;
+      out->cl_grid = (nsm / KC) * KC;
+      out->cl_smem = sm;
+    }
+    cudaGetLastError();   // a failed capacity query is not an error of the caller
+  }
   return cudaSuccess;
 }
 

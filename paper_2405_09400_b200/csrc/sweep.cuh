@@ -135,7 +135,7 @@ __device__ __forceinline__ float block_sum_f(float v, float* scratch, int parity
 struct CellLayout {
   unsigned nuJ, R2, U, V, X, fred, ints, red, total;
 };
-__host__ __device__ inline unsigned red_doubles(int s, int nt) {
+__host__ __device__ constexpr unsigned red_doubles(int s, int nt) {
   const unsigned NXX = 4u * (unsigned)s * (unsigned)s, nw = (unsigned)nt / 32u;
   const unsigned a = 6u * NXX, b = 16u * nw + 16u;
   return (a > b ? a : b) + 64u;
@@ -343,13 +343,24 @@ __device__ __forceinline__ void primal_terms(const SweepParams& p, const CompCel
   __syncthreads();
 }
 
+}  // namespace dd
+#include "sweep_cluster.cuh"
+namespace dd {
+
 // ===========================================================================
 // The fused cell routine.  NX = 2 s (X-block side), NT = threads per CTA,
 // PR = record the primal score, GS = the working set lives in global scratch
 // (huge class; a separate instantiation so that the shared-memory classes see
-// a pointer derived from the __shared__ array and compile to LDS/STS).
-template <int NX, int NT, bool PR, bool GS>
-__device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, const int ccap, unsigned char* smem) {
+// a pointer derived from the __shared__ array and compile to LDS/STS),
+// CL = the huge class on a thread-block cluster: every CTA of the cluster
+// calls this routine for the same cell; the leader (rank 0) runs the setup
+// and the epilogue on the global scratch, the Sinkhorn passes run on all KC
+// CTAs (sweep_cluster.cuh).  loc = the CTA's own small shared buffers (ints,
+// reductions), csm / cbudget = its shared-memory working set for the solve.
+template <int NX, int NT, bool PR, bool GS, bool CL = false>
+__device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, const int ccap, unsigned char* smem,
+                                           unsigned char* loc = nullptr, float* csm = nullptr, int cbudget = 0,
+                                           int rank = 0, int KC = 1) {
   const int tid = threadIdx.x;
   constexpr int T = NT;
   const CellLayout Ls = cell_layout(ccap, NX / 2, NT);
@@ -358,11 +369,12 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
   const CompCell cc = p.cells[J];
   const int nmem = cc.nmem, n1 = cc.n1, n2 = cc.n2;
   const float w = p.w;
-  int* ints = (int*)(smem + Ls.ints);
+  int* ints = CL ? (int*)loc : (int*)(smem + Ls.ints);
+  const bool lead = !CL || rank == 0;
   const int4 hull = cell_hull(p, cc, ints);
   const int L1 = hull.x, L2 = hull.y, b1 = hull.z, b2 = hull.w, BB = b1 * b2;
   const int b2p = b2 + (b2 & 1);        // even row stride of BK (8-byte aligned pairs)
-  float* P1 = P0 + BB;                  // log2 nu_J - w l2^2
+  float* P1 = P0 + BB;                  // log2 nu_J - w lc2^2 (lc = l - o: centred hull column)
   float* P2 = P0 + 2 * BB;              // BK [b1][b2p] (may extend into the 4th R2 array)
   float* Ub = (float*)(smem + Ls.U);
   float* Rb = Ub + NX * ccap;           // UK
@@ -373,25 +385,28 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
   float* LM = X + 2 * NX * NX;
   float* MU = X + 3 * NX * NX;
   float* AL = X + 4 * NX * NX;
-  float* fred = (float*)(smem + Ls.fred);
-  double* red = (double*)(smem + Ls.red);
+  float* fred = CL ? (float*)(loc + 256) : (float*)(smem + Ls.fred);
+  double* red = CL ? (double*)(loc + 512) : (double*)(smem + Ls.red);
   // gauge origin G = L + o, o = floor((b - n)/2)
   const int o1 = (b1 - n1) >> 1, o2 = (b2 - n2) >> 1;
   const int G1 = L1 + o1, G2 = L2 + o2;
   if (b1 > ccap || b2 > ccap) {   // cannot happen after binning (see copy_unchanged)
-    copy_unchanged(p, cc, J, ints, 1);
+    if (lead) copy_unchanged(p, cc, J, ints, 1);
     return;
   }
+  double muXJ = 0.0;
+  for (int q = 0; q < nmem; ++q) muXJ += p.m[cc.mem[q]];
+  const int NN = n1 * n2;
+  constexpr int NXX = NX * NX;
+  if (lead) {   // setup (a cluster's leader: on the global scratch)
   assemble(p, cc, ints, L1, L2, b2, BB, nuJ);
   double nsum = 0.0;
   for (int t = tid; t < BB; t += T) {
     const double v = nuJ[t];
     nsum += v;
-    const int l2 = t % b2;   // LNK = log2 nu_J - w l2^2 (zeros -> kNeg, R19)
-    P1[t] = v > 0.0 ? lg2f((float)v) - w * (float)(l2 * l2) : kNeg;
+    const float lc = (float)(t % b2 - o2);   // LNK = log2 nu_J - w lc^2 (zeros -> kNeg, R19)
+    P1[t] = v > 0.0 ? lg2f((float)v) - w * lc * lc : kNeg;
   }
-  double muXJ = 0.0;
-  for (int q = 0; q < nmem; ++q) muXJ += p.m[cc.mem[q]];
   {
     // mass defect of the cell problem (truncation ledger, reading R9): after
     // a Y-update the plan has mass ||nu_J||, so its X-marginal is compared
@@ -402,8 +417,6 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
   // ---- X-block data, warm start (R7) and re-gauge ------------------------
   // The X-block is padded to NX x NX (ragged B cells have n = s on an axis);
   // padded pixels carry log2 mu = kNeg, so their terms vanish.
-  const int NN = n1 * n2;
-  constexpr int NXX = NX * NX;
   float amax = kNeg;
   for (int t = tid; t < NXX; t += T) {
     const int k1 = t / NX, k2 = t % NX;
@@ -430,6 +443,7 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
     A2[t] -= amax;
     AL[t] = A2[t] + LM[t] - w * (float)((t % NX) * (t % NX));   // AK of the first pass
   }
+  }   // setup
   const float tolJ = (float)(p.tol * muXJ);
   __syncthreads();
 
@@ -449,11 +463,12 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
   float* UK = Rb;                     // [NX][b2]  U - w k1^2
   float* VK = Vb + NX * ccap;         // [b1][NX]  V - w l1^2
   float* BK = P2;                     // [b1][b2p] B + log2 nu_J - w l2^2
-  if (b2 & 1)                         // padding column: a zero-weight term for X1's pairs
-    for (int l1 = tid; l1 < b1; l1 += T) BK[l1 * b2p + b2] = kNeg;
   const float w2 = 2.f * w;
   const float fo1 = (float)o1, fo2 = (float)o2;
   constexpr int HX = NX / 2;
+  auto single_loop = [&]() {
+  if (b2 & 1)                         // padding column: a zero-weight term for X1's pairs
+    for (int l1 = tid; l1 < b1; l1 += T) BK[l1 * b2p + b2] = kNeg;
   // Y2 mapping: thread -> (column l2, row group rg of RG)
   // (a hull wider than the CTA: columns in chunks of T)
   const int RG = max(1, T / b2);
@@ -493,7 +508,9 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
           s0 = c - w * x * x;
         } else {
           s0 = Ub[o];               // previous U: the shift is U_old + w x^2
-          c = fmaf(w * x, x, s0);
+          const float K = __fmul_rn(__fmul_rn(w, x), x);   // see Y2: s0 <- (s0 + K) - K
+          c = __fadd_rn(s0, K);
+          s0 = __fsub_rn(c, K);
         }
         const float2 nc = make_float2(-c, -c);
         float2 acc = make_float2(0.f, 0.f);
@@ -543,7 +560,11 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
             s0 = c - w * x * x;
           } else {
             s0 = -P0[o];            // previous B: the shift is -B_old + w x^2
-            c = fmaf(w * x, x, s0);
+            // shift c = s0 + K; s0 <- c - K (exact) carries the rounding of
+            // the shift into the output (the output is c + lg2 sum - K)
+            const float K = __fmul_rn(__fmul_rn(w, x), x);
+            c = __fadd_rn(s0, K);
+            s0 = __fsub_rn(c, K);
           }
           const float2 nc = make_float2(-c, -c);
           float2 acc = make_float2(0.f, 0.f);
@@ -556,7 +577,7 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
           bad |= !(sum > 0x1p-60f && sum < 0x1p60f);
           const float Bv = -(s0 + lg2f(sum));
           P0[o] = Bv;
-          BK[l1 * b2p + l2] = Bv + P1[o];   // P1 = log2 nu_J - w l2^2
+          BK[l1 * b2p + l2] = Bv + P1[o];   // P1 = log2 nu_J - w lc2^2
         }
       };
       // columns in chunks of T when the hull is wider than the CTA; pass 1
@@ -568,13 +589,17 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
           for (int l2 = c0; l2 < b2; l2 += cstep) y2_column(l2, r0, rstep, first || pass == 1);
     }
     __syncthreads();
-    // X-half stage 1: V(l1, k2) = LSE_l2 [B + log2 nu_J - w (k2 - l2~)^2],
+    // X-half stage 1: V(l1, k2) = LSE_l2 [B + log2 nu_J - w (k2 - lc2)^2],
     // two outputs (k2 = qa, qa + HX) per thread sharing every loaded BK pair
-    // (LDS.64 of {l2, l2+1}, FFMA2 / FADD2 on the pair).
+    // (LDS.64 of {l2, l2+1}, FFMA2 / FADD2 on the pair).  Hull coordinates
+    // are centred on the X-block (lc = l - o): the expanded terms
+    // BK + 2 w k2 lc then stay O(w b k2) instead of O(w b^2), which keeps
+    // fp32 exponents of wide hulls accurate.
     for (int t = tid; t < b1 * HX; t += T) {
       const int l1 = t / HX, qa = t % HX, qb = qa + HX;
-      const float kta = (float)qa + fo2, ktb = (float)qb + fo2;   // k2 - l2~ = kt - l2
+      const float kta = (float)qa, ktb = (float)qb;
       const float ga = w2 * kta, gb = w2 * ktb;
+      const float Ka = __fmul_rn(__fmul_rn(w, kta), kta), Kb = __fmul_rn(__fmul_rn(w, ktb), ktb);
       const float2* br = reinterpret_cast<const float2*>(BK + l1 * b2p);
       const int np = b2p >> 1;
       float ca, cb;
@@ -582,7 +607,7 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
       auto maxshift = [&]() {
         ca = kNeg;
         cb = kNeg;
-        float2 lf = make_float2(0.f, 1.f);
+        float2 lf = make_float2(-fo2, 1.f - fo2);
         for (int k = 0; k < np; ++k) {
           const float2 bk = br[k];
           const float2 za = __ffma2_rn(make_float2(ga, ga), lf, bk), zb = __ffma2_rn(make_float2(gb, gb), lf, bk);
@@ -597,7 +622,7 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
         const float2 g2a = make_float2(ga, ga), g2b = make_float2(gb, gb);
         sa = make_float2(0.f, 0.f);
         sb = make_float2(0.f, 0.f);
-        float2 lf = make_float2(0.f, 1.f);
+        float2 lf = make_float2(-fo2, 1.f - fo2);
 #pragma unroll 2
         for (int k = 0; k < np; ++k) {
           const float2 bk = br[k];
@@ -614,36 +639,41 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
         if (maxpass || pass == 1) {
           maxshift();
         } else {
-          ca = Vb[l1 * NX + qa] + w * kta * kta;
-          cb = Vb[l1 * NX + qb] + w * ktb * ktb;
+          ca = __fadd_rn(Vb[l1 * NX + qa], Ka);
+          cb = __fadd_rn(Vb[l1 * NX + qb], Kb);
         }
         sums(s2a, s2b);
         sa = s2a.x + s2a.y;
         sb = s2b.x + s2b.y;
         if ((sa > 0x1p-60f && sa < 0x1p60f) && (sb > 0x1p-60f && sb < 0x1p60f)) break;
       }
-      const float Va = ca + lg2f(sa) - w * kta * kta;
-      const float Vbv = cb + lg2f(sb) - w * ktb * ktb;
-      const float wl1 = w * (float)(l1 * l1);
+      // (c - K) + lg2 sum: c - K is exact, so the output carries no rounding
+      // of the large shift K = w kt^2 (wide hulls)
+      const float Va = __fsub_rn(ca, Ka) + lg2f(sa);
+      const float Vbv = __fsub_rn(cb, Kb) + lg2f(sb);
+      const float lc1 = (float)l1 - fo1;
+      const float wl1 = w * lc1 * lc1;
       Vb[l1 * NX + qa] = Va;
       Vb[l1 * NX + qb] = Vbv;
       VK[l1 * NX + qa] = Va - wl1;
       VK[l1 * NX + qb] = Vbv - wl1;
     }
     __syncthreads();
-    // X-half stage 2: A'(k1, k2) = -LSE_l1 [V(l1, k2) - w (k1 - l1~)^2],
+    // X-half stage 2: A'(k1, k2) = -LSE_l1 [V(l1, k2) - w (k1 - lc1)^2],
     // two outputs (k1 = qa, qa + HX) per thread, terms split over SX lanes
+    // (centred rows, as in X1)
     float epart = 0.f;
     {
       const int qa = x2_qa, qb = qa + HX, k2 = x2_k2;
-      const float kta = (float)qa + fo1, ktb = (float)qb + fo1;
+      const float kta = (float)qa, ktb = (float)qb;
       const float ga = w2 * kta, gb = w2 * ktb;
+      const float Ka = __fmul_rn(__fmul_rn(w, kta), kta), Kb = __fmul_rn(__fmul_rn(w, ktb), ktb);
       float ca = 0.f, cb = 0.f;
       if (first) {
         ca = kNeg;
         cb = kNeg;
         if (x2_valid) {
-          float lf = (float)x2_h;
+          float lf = (float)x2_h - fo1;
           for (int l1 = x2_h; l1 < b1; l1 += SX, lf += (float)SX) {
             const float vk = VK[l1 * NX + k2];
             ca = fmaxf(ca, fmaf(ga, lf, vk));
@@ -656,12 +686,12 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
           cb = fmaxf(cb, __shfl_xor_sync(0xffffffffu, cb, off));
         }
       } else if (x2_valid) {
-        ca = -A2[qa * NX + k2] + w * kta * kta;
-        cb = -A2[qb * NX + k2] + w * ktb * ktb;
+        ca = __fadd_rn(-A2[qa * NX + k2], Ka);
+        cb = __fadd_rn(-A2[qb * NX + k2], Kb);
       }
       float sa = 0.f, sb = 0.f;
       if (x2_valid) {
-        float lf = (float)x2_h;
+        float lf = (float)x2_h - fo1;
         for (int l1 = x2_h; l1 < b1; l1 += SX, lf += (float)SX) {
           const float vk = VK[l1 * NX + k2];
           sa += ex2f(fmaf(ga, lf, vk) - ca);
@@ -677,7 +707,7 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
       if (__any_sync(0xffffffffu, bad)) {
         float ma = kNeg, mb = kNeg;
         if (x2_valid) {
-          float lf = (float)x2_h;
+          float lf = (float)x2_h - fo1;
           for (int l1 = x2_h; l1 < b1; l1 += SX, lf += (float)SX) {
             const float vk = VK[l1 * NX + k2];
             ma = fmaxf(ma, fmaf(ga, lf, vk));
@@ -691,7 +721,7 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
         }
         float ta = 0.f, tb = 0.f;
         if (x2_valid) {
-          float lf = (float)x2_h;
+          float lf = (float)x2_h - fo1;
           for (int l1 = x2_h; l1 < b1; l1 += SX, lf += (float)SX) {
             const float vk = VK[l1 * NX + k2];
             ta += ex2f(fmaf(ga, lf, vk) - ma);
@@ -708,8 +738,8 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
       if (x2_valid && x2_h == 0) {
         const float wk2 = w * (float)(k2 * k2);
         const int oa = qa * NX + k2, ob = qb * NX + k2;
-        const float ana = -(ca + lg2f(sa) - w * kta * kta);
-        const float anb = -(cb + lg2f(sb) - w * ktb * ktb);
+        const float ana = -(__fsub_rn(ca, Ka) + lg2f(sa));   // (c - K) exact, as in X1
+        const float anb = -(__fsub_rn(cb, Kb) + lg2f(sb));
         A2n[oa] = ana;
         A2n[ob] = anb;
         // L1 X-marginal error of the plan (A, B): sum mu |r - 2^(A - A')| (R6')
@@ -728,6 +758,25 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
     if (stop) break;
     float* tmp = A2; A2 = A2n; A2n = tmp;   // A <- A'
     first = false;
+  }
+  };   // single_loop
+  if constexpr (CL) {
+    cluster_sync_all();   // the leader's setup is in the global scratch
+    if (cluster_floats(b1, b2, NX, KC) * 4u <= (unsigned)cbudget) {
+      const ClusterSolveOut co =
+          cluster_solve<NX, NT>(p, b1, b2, w, fo1, fo2, tolJ, P1, P0, BK, Vb, VK, X, csm, fred, rank, KC);
+      it = co.it;
+      e0 = co.e0;
+      e = co.e;
+      A2 = X;
+      A2n = X + NXX;
+    } else if (lead) {   // too large for the cluster's shared memory: the leader alone
+      single_loop();
+    }
+    cluster_sync_all();
+    if (!lead) return;
+  } else {
+    single_loop();
   }
   __syncthreads();
   if (PR) primal_terms<NX>(p, cc, J, b1, b2, L1, L2, o1, o2, G1, G2, A2, A2n, MU, P0, nuJ, red);
@@ -782,11 +831,11 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
     for (int t = tid; t < b1 * NX; t += T) {
       const int l1 = t / NX, k2 = t % NX;
       const float kt = (float)k2 + fo2;   // lt2 - k2 = l2 - kt
-      const float g = w2 * kt;
-      const float c = Vb[t] + w * kt * kt;
+      const float g = w2 * (float)k2;     // centred columns (X1)
+      const float c = Vb[t] + w * (float)(k2 * k2);
       const float* br = BK + l1 * b2p;
       float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-      float lf = 0.f, d = -kt;
+      float lf = -fo2, d = -kt;
       for (int l2 = 0; l2 < b2; ++l2, lf += 1.f, d += 1.f) {
         const float ev = ex2f(fmaf(g, lf, br[l2]) - c);
         s0 += ev;
@@ -805,10 +854,10 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
       double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
       if (k1 < n1 && k2 < n2) {
         const float kt = (float)k1 + fo1;
-        const float g = w2 * kt;
-        const float c = -A2n[t] + w * kt * kt;
+        const float g = w2 * (float)k1;   // centred rows (X2)
+        const float c = -A2n[t] + w * (float)(k1 * k1);
         float t0 = 0.f, t1 = 0.f, t2 = 0.f, u1 = 0.f, u2 = 0.f;
-        float lf = 0.f, d = -kt;
+        float lf = -fo1, d = -kt;
         for (int l1 = 0; l1 < b1; ++l1, lf += 1.f, d += 1.f) {
           const float ev = ex2f(fmaf(g, lf, VK[l1 * NX + k2]) - c);
           t0 += ev;
@@ -1204,6 +1253,31 @@ __global__ void __launch_bounds__(NT, MINB) sweep_kernel(SweepParams p, const in
     __syncthreads();
     if (k >= n) break;
     sweep_cell<NX, NT, PR, GS>(p, list[k], ccap, base);
+    __syncthreads();
+  }
+}
+
+// The huge class on thread-block clusters: each cluster fetches one cell at
+// a time (the leader's fetch is read by all CTAs through DSMEM) and solves it
+// with sweep_cell<..., CL> on the cluster's slot of the global scratch.
+template <int NX, int NT, bool PR>
+__global__ void __launch_bounds__(NT, 1) sweep_kernel_cl(SweepParams p, const int cls, const int ccap,
+                                                         const int cbudget) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ __align__(16) unsigned char loc[512 + 8 * red_doubles(NX / 2, NT)];
+  __shared__ int job;
+  cgc::cluster_group cl = cgc::this_cluster();
+  const int rank = (int)cl.block_rank(), KC = (int)cl.num_blocks();
+  unsigned char* base = p.scratch + (size_t)(blockIdx.x / KC) * p.scratch_stride;
+  const int n = p.cls_count[cls];
+  const int* list = p.cls_list + (size_t)cls * p.ncells;
+  for (;;) {
+    if (rank == 0 && threadIdx.x == 0) job = atomicAdd(&p.cls_fetch[cls], 1);
+    cl.sync();
+    const int k = *cl.map_shared_rank(&job, 0);
+    cl.sync();   // every CTA has read the job before the leader fetches again
+    if (k >= n) break;
+    sweep_cell<NX, NT, PR, true, true>(p, list[k], ccap, base, loc, (float*)smem, cbudget, rank, KC);
     __syncthreads();
   }
 }

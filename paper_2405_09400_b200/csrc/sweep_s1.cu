@@ -4,4 +4,5 @@
 namespace dd {
 template cudaError_t launch_sweep_nx<2>(const SweepParams&, const SweepClasses&, cudaStream_t, cudaStream_t);
 template int sweep_occupancy_nx<2>(int, size_t);
+template int cluster_capacity_nx<2>(int, size_t);
 }  // namespace dd
