@@ -71,6 +71,11 @@ def dist_env():
     return world, rank, local
 
 
+def ms_levels(N, s):
+    """Multiscale layers down to the coarsest grid of 2 x 2 basic cells."""
+    return int(np.log2(N // (2 * s))) + 1
+
+
 def make(seed, N, s, theta=None, eps_factor=None):
     from synth import make_problem
     return make_problem("gm", N, s, eps_factor=CFG["eps_factor"] if eps_factor is None else eps_factor,
@@ -521,18 +526,26 @@ def run_ours(a, parallelism):
             dd3.close()
             return res
 
-        def ttc_multiscale(N, s, theta, levels):
+        def ttc_multiscale(N, s, theta, levels=None, reps=3):
+            # the first solve of a process also loads the multiscale kernels
+            # (lazy module loading): reported as cold_seconds; seconds = the
+            # median of the next reps solves (the same problem)
+            levels = ms_levels(N, s) if levels is None else levels
             q = make(rank, N, s, theta=theta)
-            barrier()
-            t0 = time.perf_counter()
-            dd4, st = multiscale_solve(q.mu, q.nu, s, q.eps, q.E, levels=levels, conv=1e-4, max_cycles=3000,
-                                       flow_every=1, stream=stream.cuda_stream, device=local)
-            torch.cuda.synchronize()
-            sec = allmax(time.perf_counter() - t0)
-            ex4, ey4 = dd4.marginal_error()
-            dd4.close()
+            times = []
+            for r in range(reps + 1):
+                barrier()
+                t0 = time.perf_counter()
+                dd4, st = multiscale_solve(q.mu, q.nu, s, q.eps, q.E, levels=levels, conv=1e-4, max_cycles=3000,
+                                           flow_every=1, stream=stream.cuda_stream, device=local)
+                torch.cuda.synchronize()
+                times.append(allmax(time.perf_counter() - t0))
+                ex4, ey4 = dd4.marginal_error()
+                dd4.close()
             ok = all(st["converged"])
-            return {"seconds": sec if ok else None, "reached": ok, "levels": st,
+            sec = float(np.median(times[1:]))
+            return {"seconds": sec if ok else None, "reached": ok, "cold_seconds": times[0],
+                    "solve_seconds": times[1:], "levels": st,
                     "l1_x": ex4, "l1_y": ey4, "nonstationary_flows": int(sum(st["flows"])),
                     "workload": (f"GM(rank) {N}^2 s={s} eps=(2h)^2 theta={theta:g}deg (the same mu, nu pair), "
                                  f"multiscale (SURVEY 8(f) f3, readings R23-R25): {levels} layers from "
@@ -550,9 +563,9 @@ def run_ours(a, parallelism):
                   "seconds": ms_sg / 1e3, "iterations": it_sg, "l1_x": e_sg, "ms_per_iteration": ms_sg / it_sg,
                   "note": "device time (CUDA events), host copies excluded; fp64 potentials"}
         if not a.no_ttc:
-            ttc = {f"cfg4_{a.N}_multiscale": ttc_multiscale(a.N, a.s, CFG["theta"], 5),
-                   f"cfg4_{a.N}_multiscale_theta5": ttc_multiscale(a.N, a.s, 5.0, 5),
-                   "cfg3_256_multiscale": ttc_multiscale(256, 4, 5.0, 3),
+            ttc = {f"cfg4_{a.N}_multiscale": ttc_multiscale(a.N, a.s, CFG["theta"]),
+                   f"cfg4_{a.N}_multiscale_theta5": ttc_multiscale(a.N, a.s, 5.0),
+                   "cfg3_256_multiscale": ttc_multiscale(256, 4, 5.0),
                    "cfg3_256": ttc_single(256, 4, 5.0, a.ttc_seconds, a.ttc_cycles, 1),
                    f"cfg4_{a.N}": ttc_single(a.N, a.s, 5.0, a.ttc_seconds, a.ttc_cycles, a.ttc_flow_every)}
         if rank == 0 and not a.no_extra:
@@ -649,15 +662,19 @@ def extra_configs(stream, local, mp):
         out["cfg3_eps_sweep"][f"({f:g}h)^2"] = sweeps(make(0, 256, 4, theta=5.0, eps_factor=f))
     p5 = make(0, 2048, 2)
     out["cfg5_2048_s2"] = sweeps(p5, 2, 4)
-    t0 = time.perf_counter()
-    dd5, st = multiscale_solve(p5.mu, p5.nu, 2, p5.eps, p5.E, levels=5, conv=1e-4, max_cycles=3000, flow_every=1,
-                               stream=stream.cuda_stream, device=local)
-    torch.cuda.synchronize()
-    sec = time.perf_counter() - t0
-    dd5.close()
-    out["cfg5_2048_s2"]["ttc_multiscale"] = {"seconds": sec if all(st["converged"]) else None, "levels": st,
-                                             "workload": "GM(0)+T_20 2048^2 s=2 eps=(2h)^2, 5 layers from 128^2, "
-                                                         "flow update every cycle"}
+    L5 = ms_levels(2048, 2)
+    times = []
+    for r in range(2):   # the second solve is reported (the first also loads kernels / grows the pool)
+        t0 = time.perf_counter()
+        dd5, st = multiscale_solve(p5.mu, p5.nu, 2, p5.eps, p5.E, levels=L5, conv=1e-4, max_cycles=3000,
+                                   flow_every=1, stream=stream.cuda_stream, device=local)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+        dd5.close()
+    out["cfg5_2048_s2"]["ttc_multiscale"] = {"seconds": times[1] if all(st["converged"]) else None,
+                                             "cold_seconds": times[0], "levels": st,
+                                             "workload": f"GM(0)+T_20 2048^2 s=2 eps=(2h)^2, {L5} layers from "
+                                                         f"{2048 >> (L5 - 1)}^2, flow update every cycle"}
     return out
 
 

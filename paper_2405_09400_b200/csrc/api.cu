@@ -18,19 +18,39 @@ void set_global_error(const std::string& m) { g_last_error = m; }
 
 // Context memory comes from the device's stream-ordered pool (cudaMallocAsync,
 // freed with cudaFreeAsync): multiscale layers and tests create and destroy
-// contexts of several GB, and the pool keeps freed memory mapped (release
-// threshold raised once per device) so that the next context does not pay
-// for page mapping again.
+// contexts of several GB.  The library allocates device memory from the device's stream-ordered pool
+// only (cudaMallocAsync).  The pool keeps what it has mapped (release
+// threshold = max) and is pre-grown once per process (DD_POOL_RESERVE_GB,
+// default min(48 GB, free / 3)): growing a pool maps physical memory, and
+// growth in the middle of a multiscale solve cost 0.1-1 s per layer
+// (profiles/r02_pool_timers.txt).
+namespace dd {
 void keep_device_pool(int dev) {
   static bool done[256] = {};
   if (dev < 0 || dev >= 256 || done[dev]) return;
-  cudaMemPool_t mp;
-  if (cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
   done[dev] = true;
+  cudaMemPool_t mp;
+  if (cudaDeviceGetDefaultMemPool(&mp, dev) != cudaSuccess) return;
+  uint64_t thr = UINT64_MAX;
+  cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
+  size_t fr = 0, tot = 0;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != dev) cudaSetDevice(dev);
+  double gb = 48.0;
+  if (const char* env = getenv("DD_POOL_RESERVE_GB")) gb = atof(env);
+  if (gb > 0 && cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+    size_t want = std::min((size_t)(gb * (1ull << 30)), fr / 3);
+    void* p = nullptr;
+    if (want > 0 && cudaMallocAsync(&p, want, 0) == cudaSuccess) {
+      cudaFreeAsync(p, 0);
+      cudaStreamSynchronize(0);
+    }
+    cudaGetLastError();   // a reservation that does not fit is not an error
+  }
+  if (cur != dev) cudaSetDevice(cur);
 }
+}  // namespace dd
 
 namespace {
 
@@ -250,16 +270,13 @@ void free_ctx(dd_ctx* c) {
                     c->d_m, c->d_q, c->d_pool[0], c->d_pool[1], c->d_off[0], c->d_off[1], c->d_ext[0], c->d_ext[1],
                     c->d_cells[0], c->d_cells[1], c->d_alpha[0], c->d_alpha[1], c->d_gauge[0], c->d_gauge[1],
                     c->d_stats[0], c->d_stats[1], c->d_totals[0], c->d_totals[1], c->d_mom, c->d_scratch, c->d_red,
-                    c->d_cls, c->d_cum, c->d_mu64, c->d_ecell, c->d_halo};
-  void* plain[] = {c->d_xbar, c->d_var, c->d_cbar, c->d_C, c->d_w, c->d_mcf, c->d_flow_info, c->d_pxm, c->d_gam,
-                   c->d_pd, c->d_hist};
+                    c->d_cls, c->d_cum, c->d_mu64, c->d_ecell, c->d_halo, c->d_xbar, c->d_var, c->d_cbar,
+                    c->d_C, c->d_w, c->d_mcf, c->d_flow_info, c->d_pxm, c->d_gam, c->d_pd, c->d_hist};
   if (c->cyc_exec) cudaGraphExecDestroy(c->cyc_exec);
   for (void* p : pooled)
     if (p) cudaFreeAsync(p, c->stream);
   if (c->stream) cudaStreamSynchronize(c->stream);
   else cudaDeviceSynchronize();
-  for (void* p : plain)
-    if (p) cudaFree(p);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   if (c->aux) cudaStreamDestroy(c->aux);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
@@ -357,6 +374,7 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c, 
   c->stripe = !(c->rb == 0 && c->re == c->n1);
   const long long NN = (long long)c->N1 * c->N2;
   const int I = c->I, s = c->s;
+  DevTimer tm;
   // ---- host validation (PAPER.md:233 m_i > 0; feasibility of pi^0) ----------
   std::vector<double> m(I, 0.0);
   double smu = 0, snu = 0;
@@ -442,6 +460,7 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c, 
   DD_CUDA(cudaSetDevice(c->device));
   c->stream = (cudaStream_t)c->opt.stream;   // NULL = legacy default stream
   cudaStream_t st = c->stream;
+  tm.mark("init: host validation");
   TRY(dalloc(c, &c->d_mu, NN));
   TRY(dalloc(c, &c->d_log2mu, NN));
   TRY(dalloc(c, &c->d_nu, NN));
@@ -466,11 +485,14 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c, 
     }
     if (c->opt.comp_cap > 0)   // testing knob: route larger hulls to the global-scratch class
       for (int k = 0; k < kClasses - 1; ++k) c->cls.ccap[k] = std::min(c->cls.ccap[k], c->opt.comp_cap);
-    TRY(dalloc(c, &c->d_scratch_huge, (size_t)c->cls.grid[kClasses - 1] * c->scratch_stride));
+    // one global-scratch slot per huge-class CTA, or per cluster (the leader's)
+    const int slots = c->cls.cl_size > 1 ? c->cls.cl_grid / c->cls.cl_size : c->cls.grid[kClasses - 1];
+    TRY(dalloc(c, &c->d_scratch_huge, (size_t)slots * c->scratch_stride));
     DD_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
     DD_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     DD_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   }
+  tm.mark("init: classes + scratch");
   DD_CUDA(cudaMemsetAsync(c->d_cum, 0, sizeof(SweepTotals), c->stream));
   for (int b = 0; b < 2; ++b) {
     TRY(dalloc(c, &c->d_pool[b], (size_t)c->pool_cap));
@@ -501,6 +523,7 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c, 
     DD_CUDA(cudaMemsetAsync(c->d_totals[b], 0, sizeof(SweepTotals), st));
     DD_CUDA(cudaMemsetAsync(c->d_stats[b], 0, sizeof(CellStats) * c->ncells[b], st));
   }
+  tm.mark("init: pools + cells");
   // mu / nu / masses / supplies
   DD_CUDA(cudaMemcpyAsync(c->d_nu, P->nu, NN * 8, cudaMemcpyHostToDevice, st));
   DD_CUDA(cudaMemcpyAsync(c->d_scratch, P->mu, NN * 8, cudaMemcpyHostToDevice, st));
@@ -564,9 +587,11 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c, 
     DD_CUDA(cudaMemcpyAsync(c->d_ext[0], P->init_ext, I * 8, cudaMemcpyHostToDevice, st));
     DD_CUDA(cudaStreamSynchronize(st));   // host staging buffer goes out of scope
   }
+  tm.mark("init: initial coupling");
   c->cur = 0;
   TRY(flow_init_static(c));
   DD_CUDA(cudaStreamSynchronize(st));
+  tm.mark("init: flow static");
   return DD_OK;
 }
 
@@ -857,9 +882,9 @@ dd_status domdec_run_cycles(dd_ctx* c, int32_t max_cycles, int32_t flow_every, d
   // from the same buffers: 2G sweeps + G / flow_every updates
   const int G = flow_every == 0 ? 2 : 2 * flow_every;
   if (!c->d_hist || G > c->cyc_G) {
-    if (c->d_hist) cudaFree(c->d_hist);
+    if (c->d_hist) cudaFreeAsync(c->d_hist, c->stream);
     c->d_hist = nullptr;
-    DD_CUDA(cudaMalloc(&c->d_hist, (size_t)4 * G * sizeof(double)));
+    DD_CUDA(cudaMallocAsync(&c->d_hist, (size_t)4 * G * sizeof(double), c->stream));
   }
   double smu = 0.0;
   {

@@ -99,6 +99,7 @@ dd_status mcf_solve_device(int n1, int n2, const int64_t* d_q, const int64_t* d_
                            void** d_ws, size_t* ws_bytes, int warm, cudaStream_t st, std::string& err);
 dd_status flow_init_static(dd_ctx* c);
 long long* mcf_info_ptr(void* ws, int I);
+void keep_device_pool(int dev);   // api.cu: stream-ordered pool, pre-grown once
 dd_status pd_gap_impl(dd_ctx* c, double* primal, double* dual, double* rel_gap, double* transport);
 void set_global_error(const std::string& m);   // dd_last_error(NULL)
 }  // namespace dd

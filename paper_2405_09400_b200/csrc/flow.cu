@@ -391,7 +391,8 @@ __global__ void k_check_flow(const long long* __restrict__ w, const long long* _
 dd_status flow_init_static(dd_ctx* c) {
   const int I = c->I;
   auto alloc = [&](void** p, size_t bytes) -> dd_status {
-    cudaError_t e = cudaMalloc(p, bytes + 16);
+    keep_device_pool(c->device);
+    cudaError_t e = cudaMallocAsync(p, bytes + 16, c->stream);
     if (e != cudaSuccess) {
       c->err = std::string("cudaMalloc: ") + cudaGetErrorString(e);
       return DD_ERR_OOM;
@@ -540,11 +541,11 @@ dd_status flow_set_candidate(dd_ctx* c, int32_t candidate, double eps_gamma_p) {
   const long long NN = (long long)c->N1 * c->N2;
   const int P = c->s * c->s;
   if (!c->d_pxm) {
-    DD_CUDA(cudaMalloc(&c->d_pxm, NN * 24));
+    DD_CUDA(cudaMallocAsync(&c->d_pxm, NN * 24, c->stream));
     DD_CUDA(cudaMemsetAsync(c->d_pxm, 0, NN * 24, c->stream));
   }
   if (!c->d_gam || c->eps_gamma_p != eps_gamma_p) {
-    if (!c->d_gam) DD_CUDA(cudaMalloc(&c->d_gam, (size_t)c->I * 4 * P * 3 * 8));
+    if (!c->d_gam) DD_CUDA(cudaMallocAsync(&c->d_gam, (size_t)c->I * 4 * P * 3 * 8, c->stream));
     c->eps_gamma_p = eps_gamma_p;
     if (P > 64) {
       c->err = "gluing candidates need cell_size <= 8";
@@ -630,7 +631,8 @@ dd_status dd_mincost_flow(int32_t n1, int32_t n2, const int64_t* q, const int64_
   size_t wsb = 0;
   std::string err;
   dd_status s = DD_OK;
-  if (cudaMalloc(&dq, I * 8) || cudaMalloc(&dC, I * 40) || cudaMalloc(&dw, I * 40)) {
+  keep_device_pool(device);
+  if (cudaMallocAsync(&dq, I * 8, st) || cudaMallocAsync(&dC, I * 40, st) || cudaMallocAsync(&dw, I * 40, st)) {
     s = DD_ERR_OOM;
   } else {
     cudaMemcpyAsync(dq, q, I * 8, cudaMemcpyHostToDevice, st);
@@ -661,10 +663,11 @@ dd_status dd_mincost_flow(int32_t n1, int32_t n2, const int64_t* q, const int64_
       }
     }
   }
-  if (dq) cudaFree(dq);
-  if (dC) cudaFree(dC);
-  if (dw) cudaFree(dw);
-  if (ws) cudaFree(ws);
+  if (dq) cudaFreeAsync(dq, st);
+  if (dC) cudaFreeAsync(dC, st);
+  if (dw) cudaFreeAsync(dw, st);
+  if (ws) cudaFreeAsync(ws, st);
+  cudaStreamSynchronize(st);
   if (s != DD_OK) {
     if (err.empty()) err = s == DD_ERR_NUMERIC ? "min-cost flow did not finish within the round cap"
                                                 : std::string("CUDA: ") + cudaGetErrorString(cudaGetLastError());

@@ -3,7 +3,25 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 namespace dd {
+
+// Development timers (DD_MS_TIMERS=1): host time between checkpoints, with a
+// device synchronisation at each checkpoint; no effect otherwise.
+struct DevTimer {
+  bool on = getenv("DD_MS_TIMERS") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    cudaDeviceSynchronize();
+    const auto n = std::chrono::steady_clock::now();
+    fprintf(stderr, "[dd timer] %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
 
 constexpr float kNeg = -1.0e30f;     // log of zero weight (reading R19), never NaN
 constexpr int kClasses = 5;          // size classes of the sweep (S, M, L, X, H)

@@ -880,9 +880,9 @@ dd_status mcf_solve_device(int n1, int n2, const int64_t* d_q, const int64_t* d_
   const int I = n1 * n2;
   const size_t need = ws_size(I);
   if (*ws_bytes < need) {
-    if (*d_ws) cudaFree(*d_ws);
+    if (*d_ws) cudaFreeAsync(*d_ws, st);
     *d_ws = nullptr;
-    if (cudaMalloc(d_ws, need) != cudaSuccess) {
+    if (cudaMallocAsync(d_ws, need, st) != cudaSuccess) {
       err = "mcf workspace allocation failed";
       return DD_ERR_OOM;
     }

@@ -26,7 +26,6 @@
 
 #include "ctx.cuh"
 
-void keep_device_pool(int dev);   // api.cu
 namespace dd {
 long long* mcf_info_ptr(void* ws, int I);
 namespace {
@@ -199,20 +198,19 @@ struct Staging {
   double* dropped = nullptr;
   cudaStream_t st = nullptr;            // the pool is stream-ordered (cudaMallocAsync)
   ~Staging() {
-    if (pool) cudaFreeAsync(pool, st);
-    for (void* p : {(void*)pos, (void*)off, (void*)ext, (void*)ctr, (void*)dropped})
-      if (p) cudaFree(p);
+    for (void* p : {(void*)pool, (void*)pos, (void*)off, (void*)ext, (void*)ctr, (void*)dropped})
+      if (p) cudaFreeAsync(p, st);
   }
   cudaError_t alloc(int I, long long cap, cudaStream_t stream) {
     cudaError_t e;
     st = stream;
     keep_device_pool_ms();
     if ((e = cudaMallocAsync(&pool, (size_t)cap * 8, st)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&pos, (size_t)I * 8)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&off, (size_t)I * 8)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&ext, (size_t)I * 8)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&ctr, 16)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&dropped, 8)) != cudaSuccess) return e;
+    if ((e = cudaMallocAsync(&pos, (size_t)I * 8, st)) != cudaSuccess) return e;
+    if ((e = cudaMallocAsync(&off, (size_t)I * 8, st)) != cudaSuccess) return e;
+    if ((e = cudaMallocAsync(&ext, (size_t)I * 8, st)) != cudaSuccess) return e;
+    if ((e = cudaMallocAsync(&ctr, 16, st)) != cudaSuccess) return e;
+    if ((e = cudaMallocAsync(&dropped, 8, st)) != cudaSuccess) return e;
     return cudaSuccess;
   }
 };
@@ -281,8 +279,8 @@ static dd_status product_ctx(const dd_problem* P, const dd_options* O, dd_ctx** 
   Staging S;
   double *dnu = nullptr, *dm = nullptr;
   cudaError_t e = S.alloc(I, cap, st);
-  if (e == cudaSuccess) e = cudaMalloc(&dnu, (size_t)N1 * N2 * 8);
-  if (e == cudaSuccess) e = cudaMalloc(&dm, (size_t)I * 8);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dnu, (size_t)N1 * N2 * 8, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dm, (size_t)I * 8, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(dnu, P->nu, (size_t)N1 * N2 * 8, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(dm, m.data(), (size_t)I * 8, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(S.ctr, 0, 16, st);
@@ -301,8 +299,8 @@ static dd_status product_ctx(const dd_problem* P, const dd_options* O, dd_ctx** 
     res = finish_staging(S, I, P, O, st, out, err);
   }
   cudaStreamSynchronize(st);
-  if (dnu) cudaFree(dnu);
-  if (dm) cudaFree(dm);
+  if (dnu) cudaFreeAsync(dnu, st);
+  if (dm) cudaFreeAsync(dm, st);
   return res;
 }
 
@@ -320,6 +318,7 @@ static dd_status refine_ctx(dd_ctx* c, const dd_problem* P, const dd_options* O,
   const int n1f = N1 / s, n2f = N2 / s, If = n1f * n2f, Ic = c->I;
   const long long NNf = (long long)N1 * N2, NNc = (long long)c->N1 * c->N2;
   // masses of the fine cells; their 2x2 sums must be the coarse masses (R23)
+  DevTimer tm;
   const std::vector<double> mf = basic_masses(P->mu, N1, N2, s);
   std::vector<double> mc(Ic);
   std::vector<int> coff(2 * (size_t)Ic), cext(2 * (size_t)Ic);
@@ -343,14 +342,15 @@ static dd_status refine_ctx(dd_ctx* c, const dd_problem* P, const dd_options* O,
   }
   long long cap = 0;
   for (int i = 0; i < Ic; ++i) cap += 16LL * cext[2 * i] * cext[2 * i + 1];
+  tm.mark("refine: coarse readback");
   Staging S;
   double *dnuf = nullptr, *dnuc = nullptr, *dry = nullptr, *dmf = nullptr, *dl1 = nullptr;
   e = S.alloc(If, cap, st);
-  if (e == cudaSuccess) e = cudaMalloc(&dnuf, NNf * 8);
-  if (e == cudaSuccess) e = cudaMalloc(&dnuc, NNc * 8);
-  if (e == cudaSuccess) e = cudaMalloc(&dry, NNf * 8);
-  if (e == cudaSuccess) e = cudaMalloc(&dmf, (size_t)If * 8);
-  if (e == cudaSuccess) e = cudaMalloc(&dl1, 8);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dnuf, NNf * 8, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dnuc, NNc * 8, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dry, NNf * 8, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dmf, (size_t)If * 8, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dl1, 8, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(dnuf, P->nu, NNf * 8, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(dmf, mf.data(), (size_t)If * 8, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(S.ctr, 0, 16, st);
@@ -365,6 +365,7 @@ static dd_status refine_ctx(dd_ctx* c, const dd_problem* P, const dd_options* O,
                                  S.ctr + 1);
     e = cudaGetLastError();
   }
+  tm.mark("refine: staging + kernels");
   if (e == cudaSuccess) {
     // the fine nu must coarsen to the coarse one (R23), exactly for dyadic data
     std::vector<double> hc((size_t)NNc), hn((size_t)NNc);
@@ -384,7 +385,9 @@ static dd_status refine_ctx(dd_ctx* c, const dd_problem* P, const dd_options* O,
     err = cuda_msg("refine", e);
     res = e == cudaErrorMemoryAllocation ? DD_ERR_OOM : DD_ERR_CUDA;
   } else if (res == DD_OK) {
+    tm.mark("refine: nu check");
     res = finish_staging(S, If, P, O, st, out, err);
+    tm.mark("refine: finish staging (init)");
     if (res == DD_OK && c->alpha_valid[0] && !c->stripe && !(*out)->stripe) {
       dd_ctx* f = *out;
       k_alpha_refine<<<f->ncells[0], 64, 0, f->stream>>>(c->d_alpha[0], c->d_gauge[0], c->N2, s, f->d_cells[0], N2,
@@ -400,7 +403,8 @@ static dd_status refine_ctx(dd_ctx* c, const dd_problem* P, const dd_options* O,
   }
   cudaStreamSynchronize(st);
   for (void* p : {(void*)dnuf, (void*)dnuc, (void*)dry, (void*)dmf, (void*)dl1})
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, st);
+  tm.mark("refine: alpha + frees");
   return res;
 }
 
@@ -455,8 +459,9 @@ dd_status dd_multiscale_solve(const dd_problem* P, const dd_options* O, const dd
   {
     const long long NN = (long long)P->N1 * P->N2;
     double *da = nullptr, *db = nullptr;
-    cudaError_t e = cudaMalloc(&da, NN * 8);
-    if (e == cudaSuccess) e = cudaMalloc(&db, NN * 8);
+    keep_device_pool_ms();
+    cudaError_t e = cudaMallocAsync(&da, NN * 8, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&db, NN * 8, st);
     for (int which = 0; which < 2 && e == cudaSuccess; ++which) {
       std::vector<std::vector<double>>& dst = which ? nus : mus;
       const double* src = which ? P->nu : P->mu;
@@ -473,8 +478,9 @@ dd_status dd_multiscale_solve(const dd_problem* P, const dd_options* O, const dd
       }
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (da) cudaFree(da);
-    if (db) cudaFree(db);
+    if (da) cudaFreeAsync(da, st);
+    if (db) cudaFreeAsync(db, st);
+    cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
       set_global_error(cuda_msg("multiscale layers", e));
       return DD_ERR_CUDA;
@@ -498,7 +504,9 @@ dd_status dd_multiscale_solve(const dd_problem* P, const dd_options* O, const dd
     Q.init_off = nullptr; Q.init_ext = nullptr; Q.init_pos = nullptr; Q.init_data = nullptr;
     dd_ctx* next = nullptr;
     dd_status r = l == 0 ? product_ctx(&Q, O, &next, err) : refine_ctx(c, &Q, O, &next, err);
+    DevTimer tmd;
     if (c) domdec_destroy(c);
+    tmd.mark("multiscale: destroy coarse");
     c = next;
     if (r != DD_OK) {
       set_global_error(err);

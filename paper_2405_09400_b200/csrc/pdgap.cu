@@ -217,7 +217,7 @@ dd_status pd_gap_impl(dd_ctx* c, double* primal, double* dual, double* rel_gap, 
   const int nparts = 256;
   // scratch: aA, aB (later g, T), inc [na1 na2], partial sums 2 x [2 nparts], out [8]
   const size_t need = 2 * (size_t)NN + (size_t)na1 * na2 + 4 * nparts + 8;
-  if (!c->d_pd) DD_CUDA(cudaMalloc(&c->d_pd, need * sizeof(double)));
+  if (!c->d_pd) DD_CUDA(cudaMallocAsync(&c->d_pd, need * sizeof(double), c->stream));
   double* aA = c->d_pd;
   double* aB = aA + NN;
   double* inc = aB + NN;

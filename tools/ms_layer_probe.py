@@ -11,7 +11,7 @@ from oracle.multiscale import layers   # input preparation only (2x2 sums), not 
 from synth import make_problem
 
 N = int(os.environ.get("N", "1024")); L = int(os.environ.get("LEVELS", "5"))
-p = make_problem("gm", N, 4, eps_factor=2.0, theta_deg=20, seed=0)
+p = make_problem("gm", N, 4, eps_factor=2.0, theta_deg=float(os.environ.get("THETA_DEG", "20")), seed=0)
 lay = layers(p.mu, p.nu, L)
 dd = None
 for lv, (mu, nu) in enumerate(lay):

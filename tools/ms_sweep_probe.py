@@ -11,18 +11,23 @@ import torch
 from paper_2405_09400_b200 import DomDec, multiscale_solve
 from synth import make_problem
 
-out = {"h_cluster": os.environ.get("DD_H_CLUSTER", "8")}
+out = {"h_cluster": os.environ.get("DD_H_CLUSTER", "8"), "levels": os.environ.get("LEVELS", "5")}
 for th in (20.0, 5.0):
     p = make_problem("gm", 1024, 4, eps_factor=2.0, theta_deg=th, seed=0)
-    for rep in range(2):
+    reps = []
+    for rep in range(int(os.environ.get("REPS", "2"))):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        dd, st = multiscale_solve(p.mu, p.nu, 4, p.eps, p.E, levels=5, conv=1e-4, max_cycles=3000, flow_every=1)
+        dd, st = multiscale_solve(p.mu, p.nu, 4, p.eps, p.E, levels=int(os.environ.get("LEVELS", "5")), conv=1e-4, max_cycles=3000, flow_every=1)
         torch.cuda.synchronize()
         sec = time.perf_counter() - t0
         ex, ey = dd.marginal_error()
         dd.close()
-    out[f"ms_T{th:g}"] = {"seconds": sec, "cycles": st["cycles"], "layer_s": [round(x, 3) for x in st["seconds"]],
+        reps.append((round(sec, 3), [round(x, 3) for x in st["seconds"]], [round(x, 3) for x in st["init_seconds"]]))
+    out[f"ms_T{th:g}"] = {"seconds": sec, "reps": reps, "cycles": st["cycles"],
+                          "layer_s": [round(x, 3) for x in st["seconds"]],
+                          "init_s": [round(x, 3) for x in st["init_seconds"]],
+                          "flow_s": [round(x, 3) for x in st["flow_seconds"]],
                           "l1x": ex, "l1y": ey, "converged": all(st["converged"])}
 p = make_problem("gm", 1024, 4, eps_factor=2.0, theta_deg=20, seed=0)
 dd = DomDec.from_problem(p)
