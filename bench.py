@@ -55,7 +55,8 @@ def parse():
     ap.add_argument("--ttc-flow-every", type=int, default=8,
                     help="flow period k of the single-scale 1024^2 time-to-1e-4 run (PAPER.md:750)")
     ap.add_argument("--no-extra", action="store_true", help="skip the eps-sweep / config-5 keys")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=0,
+                    help="hybrid cycles of the end-to-end run (0: warmup + steps, the whole bench job)")
     ap.add_argument("--cpu-seconds", type=float, default=30.0, help="LP time cap of the CPU oracle cycle")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--parallelism", default="auto", choices=["auto", "independent", "stripes"],
@@ -354,7 +355,7 @@ def run_stripes(a):
         dist.barrier()
         t0 = time.perf_counter()
         eng2 = GpuEngine(p, rows[rank], rows[rank + 1], device=local, stream=stream)
-        e2e_steps = max(1, min(a.steps, a.e2e_steps))
+        e2e_steps = a.e2e_steps if a.e2e_steps > 0 else a.warmup + a.steps
         for _ in range(e2e_steps):
             run_distributed(cycle_program(eng2, rank, world, rows, n1, n2), rank, world, device=dev)
         run_distributed(cycle_program(eng2, rank, world, rows, n1, n2, flow=False, conv=True), rank, world,
@@ -468,7 +469,7 @@ def run_ours(a, parallelism):
         barrier()
         t0 = time.perf_counter()
         dd2 = DomDec.from_problem(p, stream=stream.cuda_stream, device=local)
-        e2e_steps = max(1, min(a.steps, a.e2e_steps))
+        e2e_steps = a.e2e_steps if a.e2e_steps > 0 else a.warmup + a.steps
         for _ in range(e2e_steps):
             dd2.sweep("A")
             dd2.sweep("B")
@@ -586,7 +587,10 @@ def run_ours(a, parallelism):
             "e2e": {"value": 2 * e2e_steps * world / e2e_s, "unit": "sweeps/s",
                     "h2d_bytes_per_step": int(h2d / e2e_steps), "d2h_bytes_per_step": int(16 / e2e_steps),
                     "steps": e2e_steps,
-                    "note": "domdec_init from host buffers + steps hybrid cycles + marginal_error readback"},
+                    "note": ("the whole job end to end through the C-ABI: domdec_init from host buffers (H2D "
+                             "of the problem and the initial coupling), the same warmup + steps hybrid cycles "
+                             "from the initial coupling, marginal_error readback (D2H); includes the cold "
+                             "first min-cost flow")},
             # per step: 2 sweeps x (k_bin + 5 size-class launches) + flow (k_flow_costs, mcf_kernel,
             # k_apply_flow); profiles/r02_launches_*.csv
             "gpu_launches": 15 * a.steps,
