@@ -72,6 +72,9 @@ def dist_env():
     return world, rank, local
 
 
+MS_EPS_SCALE = 4.0   # R24': a layer spans a factor 4 in eps, ending at the target
+
+
 def ms_levels(N, s):
     """Multiscale layers down to the coarsest grid of 2 x 2 basic cells."""
     return int(np.log2(N // (2 * s))) + 1
@@ -538,7 +541,8 @@ def run_ours(a, parallelism):
                 barrier()
                 t0 = time.perf_counter()
                 dd4, st = multiscale_solve(q.mu, q.nu, s, q.eps, q.E, levels=levels, conv=1e-4, max_cycles=3000,
-                                           flow_every=1, stream=stream.cuda_stream, device=local)
+                                           flow_every=1, eps_scale=MS_EPS_SCALE, eps_stage_cycles=1,
+                                           stream=stream.cuda_stream, device=local)
                 torch.cuda.synchronize()
                 times.append(allmax(time.perf_counter() - t0))
                 ex4, ey4 = dd4.marginal_error()
@@ -549,9 +553,11 @@ def run_ours(a, parallelism):
                     "solve_seconds": times[1:], "levels": st,
                     "l1_x": ex4, "l1_y": ey4, "nonstationary_flows": int(sum(st["flows"])),
                     "workload": (f"GM(rank) {N}^2 s={s} eps=(2h)^2 theta={theta:g}deg (the same mu, nu pair), "
-                                 f"multiscale (SURVEY 8(f) f3, readings R23-R25): {levels} layers from "
-                                 f"{N >> (levels - 1)}^2, product coupling at the coarsest, hybrid A/B + flow "
-                                 "update every cycle on every layer, each layer until R14 <= 1e-4")}
+                                 f"multiscale (SURVEY 8(f) f3, readings R23-R25, R24'): {levels} layers from "
+                                 f"{N >> (levels - 1)}^2, product coupling at the coarsest, eps-scaling inside "
+                                 f"every layer (eps' x{MS_EPS_SCALE:g} halving to eps' = 4, one cycle per "
+                                 "intermediate stage, PAPER.md:1287), hybrid A/B + flow update every cycle, "
+                                 "each layer until R14 <= 1e-4")}
 
         sg = ttc = extra = None
         if rank == 0 and not a.no_ttc:
@@ -671,14 +677,15 @@ def extra_configs(stream, local, mp):
     for r in range(2):   # the second solve is reported (the first also loads kernels / grows the pool)
         t0 = time.perf_counter()
         dd5, st = multiscale_solve(p5.mu, p5.nu, 2, p5.eps, p5.E, levels=L5, conv=1e-4, max_cycles=3000,
-                                   flow_every=1, stream=stream.cuda_stream, device=local)
+                                   flow_every=1, eps_scale=MS_EPS_SCALE, eps_stage_cycles=1,
+                                   stream=stream.cuda_stream, device=local)
         torch.cuda.synchronize()
         times.append(time.perf_counter() - t0)
         dd5.close()
     out["cfg5_2048_s2"]["ttc_multiscale"] = {"seconds": times[1] if all(st["converged"]) else None,
                                              "cold_seconds": times[0], "levels": st,
                                              "workload": f"GM(0)+T_20 2048^2 s=2 eps=(2h)^2, {L5} layers from "
-                                                         f"{2048 >> (L5 - 1)}^2, flow update every cycle"}
+                                                         f"{2048 >> (L5 - 1)}^2, flow update every cycle, eps-scaling x4 per layer (R24')"}
     return out
 
 

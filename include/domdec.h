@@ -167,6 +167,14 @@ dd_status domdec_sweep(dd_ctx *ctx, dd_partition part, dd_sweep_stats *stats);
  * stats may be NULL (asynchronous). */
 dd_status flow_update(dd_ctx *ctx, dd_flow_stats *stats);
 
+/* Change the regularisation of a context to eps (physical units, 0 < eps <=
+ * the eps it was built with: the pools are sized for that one), keeping the
+ * physical dual potentials: the stored potentials (units of eps, base 2) are
+ * multiplied by eps_old / eps_new (eps-scaling, App. A.2.1 PAPER.md:1285-1287,
+ * reading R24').  The coupling is unchanged; the next sweeps solve the cell
+ * problems at the new eps.  Asynchronous.  DD_ERR_ARG for an eps out of range. */
+dd_status domdec_set_eps(dd_ctx *ctx, double eps);
+
 /* The hybrid iteration (Alg. 3) run to convergence on the
  * device: cycles of sweep(A), sweep(B) and, every flow_every-th cycle, a
  * flow update (flow_every = 0: plain DomDec, Alg. 2).
@@ -374,6 +382,12 @@ typedef struct {
   int32_t max_cycles;   /* cap of hybrid cycles per layer                                   */
   int32_t flow_every;   /* flow update after every k-th cycle; 0 = pure domdec */
   double conv;          /* layer done when both sweep-entry errors / ||mu|| <= conv (R14)   */
+  double eps_scale;     /* F >= 1: eps-scaling inside every layer (reading R24'):
+                           stages eps' F, eps' F / 2, ..., eps', each until conv; F = 4 spans the
+                           paper's factor 4 per layer, so a layer starts at the eps the coarser
+                           one ended with.  <= 1: eps' fixed on every layer (R24).            */
+  int32_t eps_stage_cycles; /* cycles of every stage but the last (0: each stage until conv);
+                           the last stage always runs until conv (or max_cycles)             */
 } dd_ms_options;
 
 typedef struct {
@@ -390,7 +404,9 @@ typedef struct {
 } dd_ms_stats;
 
 /* Coarse-to-fine hybrid solve of the problem (init_* ignored; eps' =
- * eps / h^2 is kept on every layer, R24).  On success *out is the finest
+ * eps / h^2 is the final eps' of every layer, R24; with eps_scale > 1 every
+ * layer first runs the larger eps' stages of R24').  cycles[l] sums the
+ * stages; converged[l] is the last stage's.  On success *out is the finest
  * layer's context in its final state (query it with marginal_error,
  * primal_dual_gap, exports, or keep iterating).  stats may be NULL.
  * Synchronises once per cycle (convergence test). */

@@ -60,7 +60,8 @@ class FlowStats(C.Structure):
 
 
 class MsOptions(C.Structure):
-    _fields_ = [("levels", C.c_int32), ("max_cycles", C.c_int32), ("flow_every", C.c_int32), ("conv", C.c_double)]
+    _fields_ = [("levels", C.c_int32), ("max_cycles", C.c_int32), ("flow_every", C.c_int32), ("conv", C.c_double),
+                ("eps_scale", C.c_double), ("eps_stage_cycles", C.c_int32)]
 
 
 class MsStats(C.Structure):
@@ -130,6 +131,8 @@ def lib():
             L.domdec_refine.argtypes = [vp, C.POINTER(_Problem), C.POINTER(_Options), C.POINTER(vp)]
             L.dd_multiscale_solve.argtypes = [C.POINTER(_Problem), C.POINTER(_Options), C.POINTER(MsOptions),
                                               C.POINTER(vp), C.POINTER(MsStats)]
+        if hasattr(L, "domdec_set_eps"):
+            L.domdec_set_eps.argtypes = [vp, C.c_double]
         if hasattr(L, "domdec_run_cycles"):
             L.domdec_run_cycles.argtypes = [vp, C.c_int32, C.c_int32, C.c_double, C.POINTER(C.c_int32),
                                             C.POINTER(C.c_double), C.POINTER(C.c_int32)]
@@ -145,7 +148,7 @@ def lib():
                    "domdec_reset_counters", "dd_mufu_peak", "domdec_halo_pack", "domdec_halo_unpack",
                    "dd_sinkhorn_global", "domdec_init_product", "domdec_refine", "dd_multiscale_solve",
                    "domdec_export_cell_stats", "flow_edge_costs_device", "flow_solve", "flow_apply_device",
-                   "domdec_halo_capacity", "flow_set_candidate", "domdec_run_cycles"):
+                   "domdec_halo_capacity", "flow_set_candidate", "domdec_run_cycles", "domdec_set_eps"):
             if hasattr(L, fn):
                 getattr(L, fn).restype = C.c_int
         _lib = L
@@ -158,7 +161,8 @@ EXPORTED = ("domdec_init", "domdec_sweep", "flow_update", "marginal_error", "pri
             "dd_last_error", "dd_version", "domdec_counters", "domdec_reset_counters", "dd_mufu_peak",
             "domdec_halo_pack", "domdec_halo_unpack", "dd_sinkhorn_global", "domdec_init_product",
             "domdec_refine", "dd_multiscale_solve", "flow_edge_costs_device", "flow_solve",
-            "flow_apply_device", "domdec_halo_capacity", "flow_set_candidate", "domdec_run_cycles")
+            "flow_apply_device", "domdec_halo_capacity", "flow_set_candidate", "domdec_run_cycles",
+            "domdec_set_eps")
 
 
 def _problem(mu, nu, s, eps, h, E, off=None, ext=None, pos=None, data=None):
@@ -176,7 +180,8 @@ def _options(err=1e-4, max_iter=2000, fixed_iter=0, trunc=1e-15, slot_cap=0, com
                     int(row_begin), int(row_end))
 
 
-def multiscale_solve(mu, nu, cell_size, eps, E, levels, conv=1e-4, max_cycles=1000, flow_every=1, **opts):
+def multiscale_solve(mu, nu, cell_size, eps, E, levels, conv=1e-4, max_cycles=1000, flow_every=1, eps_scale=1.0,
+                     eps_stage_cycles=0, **opts):
     """dd_multiscale_solve (readings R23-R25): coarse-to-fine
     hybrid domain decomposition of the N1 x N2 problem on [-1, 1]^2 (h = 2/N1,
     eps in physical units, eps' = eps/h^2 kept on every layer).  Returns
@@ -185,7 +190,8 @@ def multiscale_solve(mu, nu, cell_size, eps, E, levels, conv=1e-4, max_cycles=10
     nu_ = np.ascontiguousarray(nu, np.float64)
     P = _problem(mu_, nu_, cell_size, eps, 2.0 / mu_.shape[0], E)
     O = _options(**opts)
-    M = MsOptions(int(levels), int(max_cycles), int(flow_every), float(conv))
+    M = MsOptions(int(levels), int(max_cycles), int(flow_every), float(conv), float(eps_scale),
+                  int(eps_stage_cycles))
     st = MsStats()
     ctx = C.c_void_p()
     _check(lib().dd_multiscale_solve(C.byref(P), C.byref(O), C.byref(M), C.byref(ctx), C.byref(st)), None)
@@ -269,6 +275,10 @@ class DomDec:
         st = FlowStats() if stats else None
         _check(lib().flow_update(self._ctx, C.byref(st) if st is not None else None), self._ctx)
         return st.as_dict() if st is not None else None
+
+    def set_eps(self, eps):
+        """domdec_set_eps: new eps (physical, <= the construction eps), physical potentials kept."""
+        _check(lib().domdec_set_eps(self._ctx, float(eps)), self._ctx)
 
     def run_cycles(self, max_cycles, flow_every=1, conv=1e-4):
         """Hybrid cycles to convergence on the device (CUDA-graph units):

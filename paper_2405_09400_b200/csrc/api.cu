@@ -344,6 +344,7 @@ static dd_status init_impl(const dd_problem* P, const dd_options* O, dd_ctx* c, 
   c->h = P->h;
   c->eps = P->eps;
   c->eps_p = P->eps / (P->h * P->h);
+  c->eps_p_init = c->eps_p;
   c->E = P->mass_exponent;
   dd_options def{};
   def.err = 1e-4;
@@ -829,6 +830,11 @@ dd_status domdec_export_plan_cost(dd_ctx* c, double* Qm) {
 }  // extern "C"
 
 namespace {
+__global__ void k_scale_f(float* __restrict__ a, long long n, float f) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) a[i] *= f;
+}
+
 // One cycle's record: the sweep-entry errors of A and B, 1 if the cycle's
 // flow update moved mass (solver info[1] = stationary flag), and a failure
 // flag (box overflow in a sweep, min-cost flow round cap, pool exhausted in
@@ -982,6 +988,30 @@ dd_status domdec_run_cycles(dd_ctx* c, int32_t max_cycles, int32_t flow_every, d
     if (converged) break;
   }
   return finish();
+}
+
+dd_status domdec_set_eps(dd_ctx* c, double eps) {
+  if (!c) return DD_ERR_ARG;
+  const double eps_p = eps / (c->h * c->h);
+  if (!(eps > 0) || !(eps_p <= c->eps_p_init * (1 + 1e-12))) {
+    c->err = "domdec_set_eps: eps must be > 0 and <= the construction eps (pool capacities)";
+    return DD_ERR_ARG;
+  }
+  DD_CUDA(cudaSetDevice(c->device));
+  const float f = (float)(c->eps_p / eps_p);
+  const long long NN = (long long)c->N1 * c->N2;
+  for (int b = 0; b < 2; ++b)
+    if (c->alpha_valid[b]) {
+      k_scale_f<<<(unsigned)((NN + 255) / 256), 256, 0, c->stream>>>(c->d_alpha[b], NN, f);
+      DD_CUDA(cudaGetLastError());
+    }
+  c->eps = eps;
+  c->eps_p = eps_p;
+  // the captured cycles bake eps into their kernel parameters
+  if (c->cyc_exec) cudaGraphExecDestroy(c->cyc_exec);
+  c->cyc_exec = nullptr;
+  c->cyc_G = 0;
+  return DD_OK;
 }
 
 dd_status flow_update(dd_ctx* c, dd_flow_stats* stats) {

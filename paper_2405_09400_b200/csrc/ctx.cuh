@@ -10,6 +10,7 @@ struct dd_ctx {
   // problem
   int N1 = 0, N2 = 0, s = 0, n1 = 0, n2 = 0, I = 0;
   double h = 0, eps = 0, eps_p = 0;
+  double eps_p_init = 0;       // eps' at construction (sizes the pools; domdec_set_eps may only lower it)
   int E = 0;
   dd_options opt{};
   cudaStream_t stream = nullptr;

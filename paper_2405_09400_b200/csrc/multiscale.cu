@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -149,25 +150,26 @@ __global__ void k_refine(const double* __restrict__ pool_c, const long long* __r
 
 // Warm start of the fine layer's partition A from the coarse layer's A
 // potential (reading R25'): the physical potential alpha is kept, so in units
-// of eps the fine a is 4 times the coarse a at the parent pixel (eps drops 4x
-// per layer, R24).  Every fine A-cell lies inside one coarse A-cell (it is a
+// of eps the fine a is fac = eps_c / eps_f times the coarse a at the parent
+// pixel (4 when eps' is the same on both layers, R24; 1 with the paper's
+// per-layer eps-scaling over a factor 4, R24').  Every fine A-cell lies inside one coarse A-cell (it is a
 // coarse basic cell), so the coarse per-cell gauge constants stay constant
 // over a fine cell.  The coarse value is taken back to the global gauge (up
 // to its cell constant) as A + 2 w (K - g).kappa (the re-gauge of the sweep
 // kernel), and the fine cell stores it with its gauge origin at its X-block
 // corner (D = 0), minus the value at that corner.  One CTA per fine A-cell.
 __global__ void k_alpha_refine(const float* __restrict__ alpha_c, const int* __restrict__ gauge_c, int N2c, int s,
-                               const CompCell* __restrict__ cells_f, int N2f, float w, float* __restrict__ alpha_f,
-                               int* __restrict__ gauge_f) {
+                               const CompCell* __restrict__ cells_f, int N2f, float w, float fac,
+                               float* __restrict__ alpha_f, int* __restrict__ gauge_f) {
   const CompCell cc = cells_f[blockIdx.x];
   const int ncolc = (N2c / s + 1) / 2;   // A-cell columns of the coarse grid
-  auto coarse_value = [&](int r, int c) {   // 4 (log2 units) x global-gauge coarse potential at fine pixel (r, c)
+  auto coarse_value = [&](int r, int c) {   // fac x global-gauge coarse potential (log2 units) at fine pixel (r, c)
     const int rc = r >> 1, cl = c >> 1;
     const int K1 = rc - rc % (2 * s), K2 = cl - cl % (2 * s);
     const int Jc = (rc / (2 * s)) * ncolc + cl / (2 * s);
     const float a = alpha_c[(long long)rc * N2c + cl] +
                     2.f * w * ((float)(K1 - gauge_c[2 * Jc]) * (rc - K1) + (float)(K2 - gauge_c[2 * Jc + 1]) * (cl - K2));
-    return 4.f * a;
+    return fac * a;
   };
   const float ref = coarse_value(cc.r0, cc.c0);
   for (int t = threadIdx.x; t < cc.n1 * cc.n2; t += blockDim.x) {
@@ -390,8 +392,10 @@ static dd_status refine_ctx(dd_ctx* c, const dd_problem* P, const dd_options* O,
     tm.mark("refine: finish staging (init)");
     if (res == DD_OK && c->alpha_valid[0] && !c->stripe && !(*out)->stripe) {
       dd_ctx* f = *out;
+      // potential in units of eps: x eps_c / eps_f = 4 eps'_c / eps'_f (R25', R24')
       k_alpha_refine<<<f->ncells[0], 64, 0, f->stream>>>(c->d_alpha[0], c->d_gauge[0], c->N2, s, f->d_cells[0], N2,
-                                                        (float)(1.4426950408889634 / f->eps_p), f->d_alpha[0],
+                                                        (float)(1.4426950408889634 / c->eps_p),
+                                                        (float)(4.0 * c->eps_p / f->eps_p), f->d_alpha[0],
                                                         f->d_gauge[0]);
       if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(f->stream)) != cudaSuccess) {
         err = cuda_msg("refine: potential", e);
@@ -487,6 +491,9 @@ dd_status dd_multiscale_solve(const dd_problem* P, const dd_options* O, const dd
     }
   }
   const double eps_p = P->eps / (P->h * P->h);
+  // R24': eps' stages of every layer, eps' F, eps' F / 2, ..., eps' (F = eps_scale)
+  std::vector<double> stages{eps_p * std::max(1.0, ms->eps_scale)};
+  while (stages.back() > eps_p * (1 + 1e-12)) stages.push_back(std::max(eps_p, stages.back() / 2));
   dd_ms_stats S{};
   S.levels = L;
   dd_ctx* c = nullptr;
@@ -498,7 +505,7 @@ dd_status dd_multiscale_solve(const dd_problem* P, const dd_options* O, const dd
     Q.N1 = P->N1 / div;
     Q.N2 = P->N2 / div;
     Q.h = P->h * div;
-    Q.eps = eps_p * Q.h * Q.h;   // R24
+    Q.eps = stages[0] * Q.h * Q.h;   // R24 / R24' (first stage)
     Q.mu = mus[l].data();
     Q.nu = nus[l].data();
     Q.init_off = nullptr; Q.init_ext = nullptr; Q.init_pos = nullptr; Q.init_data = nullptr;
@@ -530,7 +537,13 @@ dd_status dd_multiscale_solve(const dd_problem* P, const dd_options* O, const dd
       domdec_destroy(c);
       return st;
     };
-    for (cyc = 0; cyc < ms->max_cycles; ++cyc) {
+    int total = 0;
+    for (size_t stage = 0; stage < stages.size(); ++stage) {
+    if (stage > 0 && (r = domdec_set_eps(c, stages[stage] * Q.h * Q.h)) != DD_OK) return fail("multiscale eps: ", r);
+    S.converged[l] = 0;
+    // intermediate stages: eps_stage_cycles cycles each (0: until conv); the last stage until conv
+    const int cap = (stage + 1 < stages.size() && ms->eps_stage_cycles > 0) ? ms->eps_stage_cycles : ms->max_cycles;
+    for (cyc = 0; cyc < cap; ++cyc) {
       if ((r = domdec_sweep(c, DD_PART_A, nullptr)) != DD_OK || (r = domdec_sweep(c, DD_PART_B, nullptr)) != DD_OK)
         return fail("multiscale sweep: ", r);
       const bool doflow = ms->flow_every > 0 && (cyc % ms->flow_every) == ms->flow_every - 1;
@@ -574,9 +587,11 @@ dd_status dd_multiscale_solve(const dd_problem* P, const dd_options* O, const dd
         break;
       }
     }
+    total += cyc;
+    }   // stages
     cudaEventDestroy(ef0);
     cudaEventDestroy(ef1);
-    S.cycles[l] = cyc;
+    S.cycles[l] = total;
     S.entry_error[l] = emax;
     S.seconds[l] = std::chrono::duration<double>(clk::now() - t0).count();
   }

@@ -117,3 +117,63 @@ def test_multiscale_converged_parity_cfg2():
     oex, oey = O.marginal_errors(st)
     assert abs(ex - oex) < 1e-6 and abs(ey - oey) < 1e-6, (ex, oex, ey, oey)
     dd.close()
+
+
+@gpu
+@pytest.mark.parametrize("stage_cycles", [0, 1])
+def test_multiscale_eps_scaling_matches_oracle_and_dense_optimum(stage_cycles):
+    """R24' eps-scaling inside every layer (eps' 16 -> 8 -> 4, PAPER.md:1287;
+    intermediate stages until R14 or one cycle each) on the 32^2 pair of
+    test_multiscale_matches_oracle_and_dense_optimum: the GPU and the oracle
+    both converge, their transport costs agree to 1e-5 relative and both are
+    within 1e-4 of the dense optimum at eps' = 4."""
+    from paper_2405_09400_b200 import multiscale_solve
+    p = make_problem("gm", 32, 2, theta_deg=20, seed=0)
+    dd, stats = multiscale_solve(p.mu, p.nu, 2, p.eps, p.E, levels=2, conv=1e-6, max_cycles=300, err=1e-6,
+                                 eps_scale=4.0, eps_stage_cycles=stage_cycles)
+    assert all(stats["converged"]), stats
+    st, hist = M.multiscale_solve(p.mu, p.nu, 2, p.eps_prime, levels=2, E=p.E, err=1e-6, conv=1e-6,
+                                  max_cycles=300, eps_scale=4.0, eps_stage_cycles=stage_cycles)
+    assert all(r["converged"] for r in hist), hist
+    gc = float(np.sum(dd.export_plan_cost())) * p.h * p.h
+    oc = O.transport_cost(st)
+    assert abs(gc - oc) < 1e-5 * oc, (gc, oc)
+    plan, a, b, xs, ys = O.dense_sinkhorn(p.mu, p.nu, p.eps_prime, tol=1e-12)
+    from oracle.sinkhorn import sqdist
+    N = p.N
+    cstar = float(np.sum(sqdist(np.stack([xs // N, xs % N], 1), np.stack([ys // N, ys % N], 1)) * plan)) * p.h ** 2
+    assert abs(gc - cstar) < 1e-4 * cstar, (gc, cstar)
+    dd.close()
+
+
+@gpu
+def test_set_eps_rescales_potentials_and_invalidates_graphs():
+    """domdec_set_eps keeps the physical potential (stored potentials x
+    eps_old / eps_new), refuses an eps above the construction one (pool
+    capacities), and a CUDA-graph unit captured before the change is not
+    replayed after it: run_cycles / set_eps / run_cycles equals the same
+    eager sequence bit for bit."""
+    import pytest as _pt
+    from parity import CONFIGS, gpu_ctx
+    p = CONFIGS["cfg2_gm"]()
+    g = gpu_ctx(p, fixed_iter=10)
+    g.sweep("A")
+    a0 = g.export_alpha("A")
+    g.set_eps(p.eps / 2)
+    a1 = g.export_alpha("A")
+    ok = np.isfinite(a0) & (np.abs(a0) > 1e-3)
+    np.testing.assert_allclose(a1[ok], 2.0 * a0[ok], rtol=2e-6, atol=1e-4)
+    with _pt.raises(Exception):
+        g.set_eps(p.eps * 4)
+    g.close()
+    g, r = gpu_ctx(p, fixed_iter=10), gpu_ctx(p, fixed_iter=10)
+    g.run_cycles(4, flow_every=1, conv=0.0)
+    g.set_eps(p.eps / 2)
+    g.run_cycles(4, flow_every=1, conv=0.0)
+    for k in range(8):
+        if k == 4:
+            r.set_eps(p.eps / 2)
+        r.sweep("A"); r.sweep("B"); r.flow_update()
+    for (r0, c0, d), (s0, t0, e) in zip(g.boxes(), r.boxes()):
+        assert r0 == s0 and c0 == t0 and np.array_equal(d, e)
+    g.close(); r.close()

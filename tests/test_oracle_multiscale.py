@@ -95,3 +95,36 @@ def test_multiscale_converges_to_dense_optimum():
     N = p.N
     cstar = float(np.sum(sqdist(np.stack([xs // N, xs % N], 1), np.stack([ys // N, ys % N], 1)) * plan)) * p.h ** 2
     assert abs(O.transport_cost(st) - cstar) < 1e-5 * cstar
+
+
+def test_eps_stages_and_set_eps():
+    """R24': stages eps' F, F/2, ..., 1 x eps'; set_eps keeps
+    the physical potential alpha * eps'."""
+    assert M.eps_stages(4.0, 4.0) == [16.0, 8.0, 4.0]
+    assert M.eps_stages(4.0, 1.0) == [4.0]
+    assert M.eps_stages(4.0, 3.0) == [12.0, 6.0, 4.0]
+    p = make_problem("gm", 16, 2, theta_deg=20, seed=0)
+    st = M.product_state(p.mu, p.nu, 2, 16.0, p.h)
+    O.domdec_sweep(st, "A", fixed_iter=5)
+    phys = st.alpha["A"] * st.eps_p
+    M.set_eps(st, 8.0)
+    assert st.eps_p == 8.0
+    np.testing.assert_allclose(st.alpha["A"] * st.eps_p, phys, rtol=1e-15)
+
+
+@pytest.mark.parametrize("stage_cycles", [0, 1])
+def test_multiscale_eps_scaling_converges_to_dense_optimum(stage_cycles):
+    """R24' eps-scaling inside every layer (eps' 16 -> 8 -> 4, the paper's 4x
+    span per layer; intermediate stages until R14 or one cycle
+    each) reaches the same dense global entropic optimum at the final eps' = 4
+    as the fixed-eps pipeline."""
+    p = make_problem("gm", 16, 2, theta_deg=20, seed=0)
+    st, hist = M.multiscale_solve(p.mu, p.nu, 2, 4.0, levels=2, E=p.E, err=1e-9, conv=1e-9, max_cycles=200,
+                                  eps_scale=4.0, eps_stage_cycles=stage_cycles)
+    assert all(r["converged"] for r in hist), hist
+    assert st.eps_p == 4.0
+    plan, a, b, xs, ys = O.dense_sinkhorn(p.mu, p.nu, 4.0, tol=1e-13)
+    from oracle.sinkhorn import sqdist
+    N = p.N
+    cstar = float(np.sum(sqdist(np.stack([xs // N, xs % N], 1), np.stack([ys // N, ys % N], 1)) * plan)) * p.h ** 2
+    assert abs(O.transport_cost(st) - cstar) < 1e-5 * cstar

@@ -11,14 +11,14 @@ import torch
 from paper_2405_09400_b200 import DomDec, multiscale_solve
 from synth import make_problem
 
-out = {"h_cluster": os.environ.get("DD_H_CLUSTER", "8"), "levels": os.environ.get("LEVELS", "5"), "max_iter": os.environ.get("MAX_ITER", "2000")}
+out = {"h_cluster": os.environ.get("DD_H_CLUSTER", "8"), "levels": os.environ.get("LEVELS", "5"), "max_iter": os.environ.get("MAX_ITER", "2000"), "eps_scale": os.environ.get("EPS_SCALE", "1")}
 for th in (20.0, 5.0):
     p = make_problem("gm", 1024, 4, eps_factor=2.0, theta_deg=th, seed=0)
     reps = []
     for rep in range(int(os.environ.get("REPS", "2"))):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        dd, st = multiscale_solve(p.mu, p.nu, 4, p.eps, p.E, levels=int(os.environ.get("LEVELS", "5")), conv=1e-4, max_cycles=3000, flow_every=1, max_iter=int(os.environ.get("MAX_ITER", "2000")))
+        dd, st = multiscale_solve(p.mu, p.nu, 4, p.eps, p.E, levels=int(os.environ.get("LEVELS", "5")), conv=1e-4, max_cycles=3000, flow_every=1, max_iter=int(os.environ.get("MAX_ITER", "2000")), eps_scale=float(os.environ.get("EPS_SCALE", "1")))
         torch.cuda.synchronize()
         sec = time.perf_counter() - t0
         ex, ey = dd.marginal_error()
