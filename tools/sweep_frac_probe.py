@@ -23,7 +23,7 @@ def sweeps(dd, nwarm=4, nt=6):
     s = e0.elapsed_time(e1) / 1e3
     cnt = dd.counters()
     return {"sweep_ms": round(1e3 * s / nt, 3), "frac": round(cnt["mufu_ops"] / s / peak, 4),
-            "iters": round(cnt["iters"] / max(1, cnt["cells"]), 2)}
+            "iters": cnt["iters"] / max(1, cnt["cells"]), "cells": cnt["cells"], "iters_total": cnt["iters"]}
 
 out = {"lib": os.environ.get("DD_LIB_PATH", "current")[-24:]}
 dd = DomDec.from_problem(make_problem("gm", 2048, 2, eps_factor=2.0, theta_deg=20, seed=0))
