@@ -1,7 +1,7 @@
 """Debug aid: pure domdec parity trajectory on a config, report the first
 sweep/cell whose comparison with the oracle fails."""
 import sys, os
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np
 import oracle as O

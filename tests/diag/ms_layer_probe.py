@@ -2,8 +2,9 @@
 layers by hand through the C-ABI (product init, refine) and prints per sweep
 the device time, iterations per cell, max iterations and MUFU work."""
 import json, os, sys, time
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np
 import torch
 from paper_2405_09400_b200 import DomDec

@@ -1,8 +1,9 @@
 """Debug aid: find composite cells with non-finite sweep-entry errors in the
 multiscale layers (per-cell stats through the C-ABI)."""
 import json, os, sys
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np
 from paper_2405_09400_b200 import DomDec
 from oracle.multiscale import layers

@@ -2,7 +2,7 @@
 sweep vs the oracle for several configs, size-class settings and builds
 (DD_LIB_PATH selects the build; DD_H_CLUSTER the huge-class path)."""
 import json, os, sys
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 import oracle as O

@@ -2,7 +2,7 @@
 entry GPU vs oracle after one fixed-K A sweep; the composite cell, member,
 position relative to the X-block and the values; K = 1, 2, 5, 20."""
 import json, os, sys
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np
 import oracle as O

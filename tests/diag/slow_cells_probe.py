@@ -4,8 +4,9 @@ first cycles print per sweep the cells with the most Sinkhorn passes: their
 hull side, X-mass relative to the mean cell, entry error relative to the
 cell's budget and the member boxes."""
 import json, os, sys
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np
 import torch
 from paper_2405_09400_b200 import multiscale_solve

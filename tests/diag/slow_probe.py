@@ -1,8 +1,9 @@
 """Debug aid: per-sweep iteration distribution and the slowest cells of the
 multiscale layers (hull side, mass, iterations)."""
 import json, os, sys
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np
 import torch
 from paper_2405_09400_b200 import DomDec

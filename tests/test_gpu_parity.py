@@ -58,7 +58,7 @@ def test_pure_domdec_trajectory_parity(cfg, sweeps):
     bit-exact outside the guard band at the end.  The four-bumps / T0
     trajectory (pure curl) amplifies the fp32-vs-fp64
     rounding differences by ~3-10x per sweep from sweep 4 on (measured with
-    the round-1 and the round-2 kernels alike, tools/debug_traj2.py): its box
+    the round-1 and the round-2 kernels alike, tests/diag/debug_traj2.py): its box
     comparison is made after 4 sweeps, where the differences are still at
     the fp32 tolerance."""
     p = CONFIGS[cfg]()
