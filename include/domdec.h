@@ -224,6 +224,14 @@ dd_status domdec_export_cells(dd_ctx *ctx, int32_t *off, int32_t *ext, int64_t *
  * PAPER.md:216).  DD_ERR_PRECOND if the partition was never swept. */
 dd_status domdec_export_alpha(dd_ctx *ctx, dd_partition part, double *alpha);
 
+/* Checkpoint / resume: set the warm-start potential of a partition (reading
+ * R7) from host [N1*N2] in the format of domdec_export_alpha (a = alpha/eps,
+ * any constant per composite cell).  With a context built by domdec_init from
+ * the boxes of domdec_export_cells, this resumes a solve: the next sweeps
+ * start from the exported potentials instead of alpha = 0.  Synchronises.
+ * DD_ERR_ARG for a non-finite value on a pixel of a composite cell. */
+dd_status domdec_import_alpha(dd_ctx *ctx, dd_partition part, const double *alpha);
+
 /* Per basic cell plan cost of the last sweep, Q_i m_i = <c, pi_i> in pixel^2
  * units (reading R13), host [I].  Synchronises. */
 dd_status domdec_export_plan_cost(dd_ctx *ctx, double *Qm);

@@ -106,6 +106,8 @@ def lib():
                                           C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_int64)]
         L.domdec_export_alpha.argtypes = [vp, C.c_int, C.POINTER(C.c_double)]
         L.domdec_export_plan_cost.argtypes = [vp, C.POINTER(C.c_double)]
+        if hasattr(L, "domdec_import_alpha"):
+            L.domdec_import_alpha.argtypes = [vp, C.c_int, C.POINTER(C.c_double)]
         if hasattr(L, "domdec_export_cell_stats"):   # (absent from older development builds)
             L.domdec_export_cell_stats.argtypes = [vp, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_double),
                                                    C.POINTER(C.c_double), C.POINTER(C.c_int32)]
@@ -148,7 +150,8 @@ def lib():
                    "domdec_reset_counters", "dd_mufu_peak", "domdec_halo_pack", "domdec_halo_unpack",
                    "dd_sinkhorn_global", "domdec_init_product", "domdec_refine", "dd_multiscale_solve",
                    "domdec_export_cell_stats", "flow_edge_costs_device", "flow_solve", "flow_apply_device",
-                   "domdec_halo_capacity", "flow_set_candidate", "domdec_run_cycles", "domdec_set_eps"):
+                   "domdec_halo_capacity", "flow_set_candidate", "domdec_run_cycles", "domdec_set_eps",
+                   "domdec_import_alpha"):
             if hasattr(L, fn):
                 getattr(L, fn).restype = C.c_int
         _lib = L
@@ -162,7 +165,7 @@ EXPORTED = ("domdec_init", "domdec_sweep", "flow_update", "marginal_error", "pri
             "domdec_halo_pack", "domdec_halo_unpack", "dd_sinkhorn_global", "domdec_init_product",
             "domdec_refine", "dd_multiscale_solve", "flow_edge_costs_device", "flow_solve",
             "flow_apply_device", "domdec_halo_capacity", "flow_set_candidate", "domdec_run_cycles",
-            "domdec_set_eps")
+            "domdec_set_eps", "domdec_import_alpha")
 
 
 def _problem(mu, nu, s, eps, h, E, off=None, ext=None, pos=None, data=None):
@@ -366,6 +369,13 @@ class DomDec:
         _check(lib().domdec_export_alpha(self._ctx, PART_A if part in ("A", 0) else PART_B, _ptr(a, C.c_double)),
                self._ctx)
         return a
+
+    def import_alpha(self, part, alpha):
+        """domdec_import_alpha: warm-start potential in the export_alpha format (resume)."""
+        a = np.ascontiguousarray(alpha, np.float64)
+        assert a.shape == (self.N1, self.N2)
+        _check(lib().domdec_import_alpha(self._ctx, PART_A if part in ("A", 0) else PART_B, _ptr(a, C.c_double)),
+               self._ctx)
 
     def cell_stats(self, part):
         """Per composite cell (iters, e0, e) of the last sweep on a partition."""

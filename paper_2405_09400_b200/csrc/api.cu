@@ -816,6 +816,39 @@ dd_status domdec_export_alpha(dd_ctx* c, dd_partition part, double* alpha) {
   return DD_OK;
 }
 
+dd_status domdec_import_alpha(dd_ctx* c, dd_partition part, const double* alpha) {
+  if (!c || !alpha || (part != DD_PART_A && part != DD_PART_B)) return DD_ERR_ARG;
+  const int b = (int)part;
+  DD_CUDA(cudaSetDevice(c->device));
+  const long long NN = (long long)c->N1 * c->N2;
+  // every composite cell takes its gauge origin at its X-block corner (D = 0),
+  // where the stored base-2 potential is a / ln 2 (the inverse of the export)
+  std::vector<float> a(NN, 0.f);
+  std::vector<int> g(2 * (size_t)c->ncells[b]);
+  for (int J = 0; J < c->ncells[b]; ++J) {
+    const CompCell& cc = c->h_cells[b][J];
+    g[2 * J] = cc.r0;
+    g[2 * J + 1] = cc.c0;
+    for (int k1 = 0; k1 < cc.n1; ++k1)
+      for (int k2 = 0; k2 < cc.n2; ++k2) {
+        const long long pix = (long long)(cc.r0 + k1) * c->N2 + cc.c0 + k2;
+        if (!std::isfinite(alpha[pix])) {
+          c->err = "domdec_import_alpha: non-finite potential";
+          return DD_ERR_ARG;
+        }
+        a[pix] = (float)(alpha[pix] * 1.4426950408889634);
+      }
+  }
+  DD_CUDA(cudaMemcpyAsync(c->d_alpha[b], a.data(), NN * 4, cudaMemcpyHostToDevice, c->stream));
+  DD_CUDA(cudaMemcpyAsync(c->d_gauge[b], g.data(), g.size() * 4, cudaMemcpyHostToDevice, c->stream));
+  DD_CUDA(cudaStreamSynchronize(c->stream));   // host staging goes out of scope
+  c->alpha_valid[b] = 1;
+  if (c->cyc_exec) cudaGraphExecDestroy(c->cyc_exec);   // captured units baked alpha_valid
+  c->cyc_exec = nullptr;
+  c->cyc_G = 0;
+  return DD_OK;
+}
+
 dd_status domdec_export_plan_cost(dd_ctx* c, double* Qm) {
   if (!c || !Qm) return DD_ERR_ARG;
   DD_CUDA(cudaSetDevice(c->device));
