@@ -36,9 +36,12 @@ def test_resume_from_exported_state(mode):
         sa = a.sweep(part, stats=True)
         sr = r.sweep(part, stats=True)
         sc = cold.sweep(part, stats=True)
-        rb, rt = rel_tols(p.eps_prime)
-        cmp = compare_states(r.boxes(), a.boxes())
-        assert cmp["unexplained"] == 0 and cmp["rel_bulk"] < rb and cmp["rel_tail"] < rt, (part, cmp)
+        if mode == "fixed":   # same passes: entries agree to the fp32 parity bound
+            rb, rt = rel_tols(p.eps_prime)
+            cmp = compare_states(r.boxes(), a.boxes())
+            assert cmp["unexplained"] == 0 and cmp["rel_bulk"] < rb and cmp["rel_tail"] < rt, (part, cmp)
+        # (tolerance mode: a cell may stop one pass apart, so entries agree to the
+        # Sinkhorn tolerance only; the cost and the pass counts are compared)
         ca, cr = gpu_transport_cost(a, p.h), gpu_transport_cost(r, p.h)
         assert abs(ca - cr) < 1e-6 * ca, (part, ca, cr)
         if mode == "tolerance":
