@@ -568,9 +568,23 @@ __global__ void __launch_bounds__(512, 1) mcf_kernel(McfArgs A) {
   grid.sync();
   // The stationary flow (w_ii = q_i) is the result of every early exit: A.w
   // holds the warm flow at this point and must not be applied again.
-  auto stationary_exit = [&](int bf_rounds) {
-    for (long long i = gt; i < I; i += gs)
+  // The certificate's labels d (d_j <= d_i + C_ij on every 4-neighbour arc;
+  // d = 0 when no cost is negative) price the stationary flow optimally:
+  // with p_S = p_T = SC d every arc has reduced cost SC (C_ij + d_i - d_j) >= 0
+  // and the self arcs 0.  A warm context keeps that pair, so the next
+  // non-stationary update starts from the optimum of this instance instead
+  // of the last moving flow, however old.
+  auto stationary_exit = [&](int bf_rounds, const long long* labels) {
+    for (long long i = gt; i < I; i += gs) {
       for (int a = 0; a < 5; ++a) A.w[5 * i + a] = (a == 0) ? A.q[i] : 0;
+      if (A.warm) {
+        for (int a = 0; a < 5; ++a) A.wW[5 * i + a] = (a == 0) ? A.q[i] : 0;
+        const long long pr = labels ? labels[i] * SC : 0;
+        A.wpS[i] = pr;
+        A.wpT[i] = pr;
+      }
+    }
+    if (A.warm && gt == 0) *A.wvalid = 1;
     if (gt == 0) {
       A.info[0] = 0; A.info[1] = 1; A.info[2] = 1; A.info[3] = 0; A.info[4] = 0; A.info[5] = bf_rounds;
       A.info[6] = 0; A.info[12] = (long long)(gtimer() - tm_start);
@@ -580,7 +594,7 @@ __global__ void __launch_bounds__(512, 1) mcf_kernel(McfArgs A) {
   // no negative arc cost, or the last certificate's labels are still a
   // feasible potential: no negative cycle, the stationary flow is optimal
   if (!any_negative || (cwarm && A.ctr[2] == 0)) {
-    stationary_exit(0);
+    stationary_exit(0, any_negative ? A.certd : nullptr);
     return;
   }
   // ---- Bellman-Ford certificate on (I, 4-nbr arcs, C) -----------------------
@@ -598,7 +612,7 @@ __global__ void __launch_bounds__(512, 1) mcf_kernel(McfArgs A) {
       for (long long i = gt; i < I; i += gs) A.certd[i] = A.dist[0][i];
       if (gt == 0) *A.cvalid = 1;
     }
-    stationary_exit(rb);
+    stationary_exit(rb, A.warm ? A.certd : nullptr);
     return;
   }
   // ---- cost scaling -----------------------------------------------------------
