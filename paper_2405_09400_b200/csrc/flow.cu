@@ -448,9 +448,16 @@ dd_status flow_costs_impl(dd_ctx* c) {
 
 dd_status flow_update_impl(dd_ctx* c, dd_flow_stats* stats) {
   ++c->n_flows;
-  dd_status s = flow_costs_impl(c);
+  dd_status s;
+  {
+    NvtxRange nv("dd/flow edge costs");
+    s = flow_costs_impl(c);
+  }
   if (s) return s;
-  s = mcf_solve_device(c->n1, c->n2, c->d_q, c->d_C, c->d_w, &c->d_mcf, &c->mcf_bytes, 1, c->stream, c->err);
+  {
+    NvtxRange nv("dd/min-cost flow");
+    s = mcf_solve_device(c->n1, c->n2, c->d_q, c->d_C, c->d_w, &c->d_mcf, &c->mcf_bytes, 1, c->stream, c->err);
+  }
   if (s) return s;
   unsigned long long* ctr = (unsigned long long*)c->d_flow_info;   // [0] changed, [1] failed
   double* dropped = (double*)(c->d_flow_info + 8);

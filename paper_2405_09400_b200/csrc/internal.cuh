@@ -3,11 +3,22 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
 
 namespace dd {
+
+// NVTX range over a C-ABI call (tracing: `ncu --nvtx --nvtx-include "dd/..."`
+// selects the kernels a call launched; no cost without a tool attached).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Development timers (DD_MS_TIMERS=1): host time between checkpoints, with a
 // device synchronisation at each checkpoint; no effect otherwise.
