@@ -632,7 +632,7 @@ dd_status domdec_init(const dd_problem* problem, const dd_options* options, dd_c
 
 dd_status domdec_sweep(dd_ctx* c, dd_partition part, dd_sweep_stats* stats) {
   if (!c || (part != DD_PART_A && part != DD_PART_B)) return DD_ERR_ARG;
-  NvtxRange nv(part == DD_PART_A ? "dd/sweep A" : "dd/sweep B");
+  NvtxRange nv(part == DD_PART_A ? "dd:sweep A" : "dd:sweep B");
   DD_CUDA(cudaSetDevice(c->device));
   const int b = (int)part;
   SweepParams p{};
@@ -912,7 +912,7 @@ extern "C" {
 dd_status domdec_run_cycles(dd_ctx* c, int32_t max_cycles, int32_t flow_every, double conv, int32_t* cycles,
                             double* entry_error, int32_t* moved_flows) {
   if (!c || max_cycles < 1 || flow_every < 0) return DD_ERR_ARG;
-  NvtxRange nv("dd/run_cycles");
+  NvtxRange nv("dd:run_cycles");
   if (c->stripe) {
     c->err = "stripe mode: use the cycle program of stripes.py";
     return DD_ERR_ARG;
@@ -1051,7 +1051,7 @@ dd_status domdec_set_eps(dd_ctx* c, double eps) {
 
 dd_status flow_update(dd_ctx* c, dd_flow_stats* stats) {
   if (!c) return DD_ERR_ARG;
-  NvtxRange nv("dd/flow_update");
+  NvtxRange nv("dd:flow_update");
   if (c->last_part < 0) {
     c->err = "flow_update needs a previous sweep (plan costs, reading R13)";
     return DD_ERR_PRECOND;

@@ -450,12 +450,12 @@ dd_status flow_update_impl(dd_ctx* c, dd_flow_stats* stats) {
   ++c->n_flows;
   dd_status s;
   {
-    NvtxRange nv("dd/flow edge costs");
+    NvtxRange nv("dd:flow edge costs");
     s = flow_costs_impl(c);
   }
   if (s) return s;
   {
-    NvtxRange nv("dd/min-cost flow");
+    NvtxRange nv("dd:min-cost flow");
     s = mcf_solve_device(c->n1, c->n2, c->d_q, c->d_C, c->d_w, &c->d_mcf, &c->mcf_bytes, 1, c->stream, c->err);
   }
   if (s) return s;

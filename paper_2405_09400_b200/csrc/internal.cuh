@@ -11,7 +11,7 @@
 
 namespace dd {
 
-// NVTX range over a C-ABI call (tracing: `ncu --nvtx --nvtx-include "dd/..."`
+// NVTX range over a C-ABI call (tracing: `ncu --nvtx --nvtx-include "dd:flow_update/dd:min-cost flow/"`
 // selects the kernels a call launched; no cost without a tool attached).
 struct NvtxRange {
   explicit NvtxRange(const char* name) { nvtxRangePushA(name); }

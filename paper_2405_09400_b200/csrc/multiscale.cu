@@ -499,11 +499,11 @@ dd_status dd_multiscale_solve(const dd_problem* P, const dd_options* O, const dd
   S.levels = L;
   dd_ctx* c = nullptr;
   std::string err;
-  NvtxRange nv("dd/multiscale_solve");
+  NvtxRange nv("dd:multiscale_solve");
   for (int l = 0; l < L; ++l) {
     const auto t0 = clk::now();
     char lname[32];
-    snprintf(lname, sizeof(lname), "dd/layer %d", l);
+    snprintf(lname, sizeof(lname), "dd:layer %d", l);
     NvtxRange nvl(lname);
     dd_problem Q = *P;
     const int div = 1 << (L - 1 - l);
