@@ -331,16 +331,19 @@ def test_hybrid_flow_updates_move_mass_then_stop():
 
 
 @gpu
+@pytest.mark.parametrize("size", [(1024, 4), (2048, 2)])
 @pytest.mark.parametrize("part", ["A", "B"])
-def test_full_size_sampled_first_sweep(part):
-    """BASELINE.json configs[3] (1024^2, s = 4, eps = (2h)^2) in the launch
-    configuration bench.py times (tolerance mode, Err = 1e-4): the GPU sweeps
-    all composite cells; the oracle recomputes a sample of cells one by one on
+def test_full_size_sampled_first_sweep(part, size):
+    """BASELINE.json configs[3] (1024^2, s = 4, eps = (2h)^2; the bench's
+    launch configuration, tolerance mode, Err = 1e-4) and configs[4] (2048^2,
+    s = 2, the maximum size: 1,048,576 basic cells): the GPU sweeps all
+    composite cells; the oracle recomputes a sample of cells one by one on
     identical inputs with exactly the GPU's per-cell iteration count
     (iteration-matched), so every sampled cell is compared at the fp32
     tolerance of the small configs (rel_tols) with bit-exact boxes outside the
     guard band."""
-    p = make_problem("gm", 1024, 4, eps_factor=2.0, theta_deg=20, seed=0)
+    N, s = size
+    p = make_problem("gm", N, s, eps_factor=2.0, theta_deg=20, seed=0)
     st = oracle_state(p)
     comp = O.composite_partition(st.n1, st.n2, part)
     rng = np.random.default_rng(7)
