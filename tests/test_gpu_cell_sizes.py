@@ -1,4 +1,4 @@
-"""Cell sizes s = 1 and s = 8 (the library builds sweep kernels for s in
+"""Cell sizes s = 1 and s = 8, and the smallest grids of 2 x 2 basic cells (the library builds sweep kernels for s in
 {1, 2, 4, 8}; the other parity tests use s = 2 and 4): one sweep from the
 generated coupling with exactly K Sinkhorn passes per cell against the fp64
 oracle, in the automatic size classes and with every cell in the huge class
@@ -13,11 +13,14 @@ from synth import make_problem
 gpu = pytest.mark.gpu
 
 CASES = {"s1": lambda: make_problem("gm", 24, 1, eps_factor=2.0, theta_deg=20, seed=1),
-         "s8": lambda: make_problem("gm", 64, 8, eps_factor=2.0, theta_deg=20, seed=2)}
+         "s8": lambda: make_problem("gm", 64, 8, eps_factor=2.0, theta_deg=20, seed=2),
+         # the smallest grids: 2 x 2 basic cells (one A cell, B cells of 1 x 1, 1 x 2, 2 x 1)
+         "tiny_s2": lambda: make_problem("gm", 4, 2, eps_factor=2.0, theta_deg=20, seed=3),
+         "tiny_s4": lambda: make_problem("gm", 8, 4, eps_factor=2.0, theta_deg=20, seed=4)}
 
 
 @gpu
-@pytest.mark.parametrize("case", ["s1", "s8"])
+@pytest.mark.parametrize("case", ["s1", "s8", "tiny_s2", "tiny_s4"])
 @pytest.mark.parametrize("part", ["A", "B"])
 @pytest.mark.parametrize("comp_cap", [0, 8])
 def test_first_sweep_parity_other_cell_sizes(case, part, comp_cap):
@@ -29,7 +32,7 @@ def test_first_sweep_parity_other_cell_sizes(case, part, comp_cap):
     (DESIGN.md "Parity tolerances"); the transport cost still agrees
     (test_hybrid_trajectory_other_cell_sizes)."""
     p = CASES[case]()
-    K = 20 if case == "s1" else 5
+    K = 5 if case == "s8" else 20
     st = oracle_state(p)
     ost = O.domdec_sweep(st, part, fixed_iter=K)
     dd = gpu_ctx(p, fixed_iter=K, comp_cap=comp_cap)
@@ -49,7 +52,7 @@ def test_first_sweep_parity_other_cell_sizes(case, part, comp_cap):
 
 
 @gpu
-@pytest.mark.parametrize("case", ["s1", "s8"])
+@pytest.mark.parametrize("case", ["s1", "s8", "tiny_s2", "tiny_s4"])
 def test_hybrid_trajectory_other_cell_sizes(case):
     """Four hybrid cycles (fixed K, the GPU's optimal flow injected on both
     sides as in the lockstep protocol of test_gpu_parity): transport cost
