@@ -22,6 +22,7 @@
 // join events), so their few long cells overlap the bulk instead of forming a
 // serial tail.  No host synchronisation inside a sweep.
 #include "sweep.cuh"
+#include <algorithm>
 #include <cstdlib>
 
 namespace dd {
@@ -131,9 +132,10 @@ cudaError_t sweep_classes(int s, int N, int nsm, int ncells, SweepClasses* out, 
   const int KC = env ? atoi(env) : 8;
   if (KC == 2 || KC == 4 || KC == 8) {
     const size_t sm = (size_t)(envkb && atoi(envkb) > 0 ? atoi(envkb) : 160) * 1024;
-    if (cluster_capacity_s(s, KC, sm) > 0) {
+    const int active = cluster_capacity_s(s, KC, sm);   // co-resident clusters (placement limits)
+    if (active > 0) {
       out->cl_size = KC;
-      out->cl_grid = (nsm / KC) * KC;
+      out->cl_grid = std::min(nsm / KC, active) * KC;
       out->cl_smem = sm;
     }
     cudaGetLastError();   // a failed capacity query is not an error of the caller
