@@ -12,16 +12,17 @@
 //     keeps its rows of B, log2 nu_J and BK, and V of its rows, in its own
 //     shared memory for the whole solve;
 //   * the X-block data (A, A', log2 mu, mu: NX^2 values) is replicated;
-//   * Y-half stage 1 (U(k1, l2), no row dependence) is split by columns and
-//     each CTA stores its slice into the U buffer of every CTA of the cluster
-//     (DSMEM stores); cluster barrier;
+//   * Y-half stage 1 (U(k1, l2), no row dependence, NX^2 b2 terms) is
+//     computed for all columns by every CTA: a column split with a DSMEM
+//     exchange cost one more cluster barrier per pass and measured 15% slower
+//     (profiles/r02_ncu_cluster.txt);
 //   * Y-half stage 2 and X-half stage 1 are row-local;
 //   * X-half stage 2 (A' = -LSE over all rows) adds per-CTA partial sums of
 //     the same shift (the previous A', or the cluster-wide maximum on the
 //     first pass): partials in shared memory, cluster barrier, every CTA sums
 //     the KC partials in rank order, so all CTAs hold bit-identical A' and
 //     X-errors and take the same stopping decision.
-// Two cluster barriers per pass (three on the first).  The arithmetic of
+// One cluster barrier per pass (two on the first).  The arithmetic of
 // every term is the one of the single-CTA loop (sweep.cuh, "Shift trick");
 // only the fp32 summation order of the row sums differs.  On exit the CTAs
 // write their rows of B, BK, V back to the cell's global scratch, where the
@@ -50,9 +51,9 @@ __host__ __device__ inline unsigned cluster_floats(int b1, int b2, int NX, int K
          + Rm * b2p          // BK (8-byte aligned pairs)
          + 2 * Rm * b2       // B, log2 nu_J - w l2^2
          + 2 * Rm * NX       // V, VK
-         + (unsigned)NX * nc // U of the own columns (shifts)
+         + (unsigned)NX * b2 // U of every column (shifts; Y-stage 1 is replicated)
          + 5 * NXX + 4       // A, A', log2 mu, mu, AL, mass defect
-         + 3 * NXX + 4;      // shifts, partial sums, partial maxima
+         + 4 * NXX + 4;      // shifts, partial sums (two buffers), partial maxima
 }
 
 struct ClusterSolveOut {
@@ -76,7 +77,10 @@ __device__ ClusterSolveOut cluster_solve(const SweepParams& p, const int b1, con
   const int b2p = b2 + (b2 & 1);
   const int Rm = (b1 + KC - 1) / KC, ncm = (b2 + KC - 1) / KC;
   const int r0 = min(b1, rank * Rm), R = min(b1, r0 + Rm) - r0;   // own rows [r0, r0 + R)
-  const int c0 = min(b2, rank * ncm), nc = min(b2, c0 + ncm) - c0;   // own columns of Y-stage 1
+  // Y-stage 1 (NX^2 b2 terms) is computed by every CTA for all columns: cheaper
+  // than a DSMEM exchange and its cluster barrier on every pass
+  const int c0 = 0, nc = b2;
+  (void)ncm;
   // shared-memory carve-up (see cluster_floats)
   float* UKt = csm;                   // [b2][NX]
   float* BK = UKt + NX * b2;
@@ -84,16 +88,16 @@ __device__ ClusterSolveOut cluster_solve(const SweepParams& p, const int b1, con
   float* LN = B + Rm * b2;
   float* Vb = LN + Rm * b2;
   float* VK = Vb + Rm * NX;
-  float* Ub = VK + Rm * NX;           // [NX][nc] own columns
-  float* Xl = Ub + NX * ncm;
+  float* Ub = VK + Rm * NX;           // [NX][b2]
+  float* Xl = Ub + NX * b2;
   float* A2 = Xl;
   float* A2n = Xl + NXX;
   float* LM = Xl + 2 * NXX;
   float* MU = Xl + 3 * NXX;
   float* AL = Xl + 4 * NXX;
   float* csh = Xl + 5 * NXX + 4;      // per-output shift of X-stage 2
-  float* part = csh + NXX;            // partial sums (read remotely)
-  float* pmx = part + NXX;            // partial maxima (read remotely)
+  float* part2 = csh + NXX;           // partial sums, by pass parity (read remotely)
+  float* pmx = part2 + 2 * NXX;       // partial maxima (read remotely)
   for (int t = tid; t < R * b2; t += T) LN[t] = __ldcg(P1g + (size_t)r0 * b2 + t);
   for (int t = tid; t < 5 * NXX + 1; t += T) Xl[t] = __ldcg(Xg + t);
   if (b2 & 1)
@@ -111,7 +115,7 @@ __device__ ClusterSolveOut cluster_solve(const SweepParams& p, const int b1, con
   constexpr int SX2 = T / NXX >= 8 ? 8 : (T / NXX >= 1 ? T / NXX : 1);
   for (;;) {
     ++out.it;
-    // ---- Y-half stage 1 on the own columns, stored into every CTA ----------
+    // ---- Y-half stage 1 (every column, replicated in every CTA) ------------
     {
       bool bad = false;
       for (int pass = 0; pass < 2; ++pass) {
@@ -144,12 +148,11 @@ __device__ ClusterSolveOut cluster_solve(const SweepParams& p, const int b1, con
           bad |= !(sum > 0x1p-60f && sum < 0x1p60f);
           const float U = s0 + lg2f(sum);
           Ub[o] = U;
-          const float uk = U - w * (float)(k1 * k1);
-          for (int r = 0; r < KC; ++r) cl.map_shared_rank(UKt, r)[l2 * NX + k1] = uk;
+          UKt[l2 * NX + k1] = U - w * (float)(k1 * k1);
         }
       }
     }
-    cl.sync();
+    __syncthreads();
     // ---- Y-half stage 2 on the own rows: B(l1, l2) = -LSE_k1 [...] --------
     {
       bool bad = false;
@@ -276,6 +279,10 @@ __device__ ClusterSolveOut cluster_solve(const SweepParams& p, const int b1, con
     const bool ov = o2 < NXX;
     const int k1 = ov ? o2 / NX : 0, k2 = ov ? o2 % NX : 0;
     const float g = w2 * (float)k1;   // centred rows (sweep.cuh X2)
+    // One cluster barrier per pass (in partial_sum): a CTA may start the next
+    // pass's partial sums while another still reads this pass's, hence two
+    // buffers by pass parity.
+    float* part = part2 + (out.it & 1) * NXX;
     auto partial_max = [&]() {
       float m = kNeg;
       if (ov)
