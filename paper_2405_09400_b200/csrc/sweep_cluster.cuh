@@ -44,7 +44,7 @@ __device__ __forceinline__ void cluster_sync_all() {
 
 // Float count of a CTA's shared-memory working set for a b1 x b2 hull.
 __host__ __device__ inline unsigned cluster_floats(int b1, int b2, int NX, int KC) {
-  const unsigned Rm = (unsigned)((b1 + KC - 1) / KC), nc = (unsigned)((b2 + KC - 1) / KC);
+  const unsigned Rm = (unsigned)((b1 + KC - 1) / KC);
   const unsigned b2p = (unsigned)(b2 + (b2 & 1));
   const unsigned NXX = (unsigned)(NX * NX);
   return (unsigned)NX * b2   // UK of all columns, transposed [b2][NX] (first: float4 rows)
@@ -75,12 +75,10 @@ __device__ ClusterSolveOut cluster_solve(const SweepParams& p, const int b1, con
   const int tid = threadIdx.x;
   constexpr int T = NT, NXX = NX * NX, HX = NX / 2;
   const int b2p = b2 + (b2 & 1);
-  const int Rm = (b1 + KC - 1) / KC, ncm = (b2 + KC - 1) / KC;
+  const int Rm = (b1 + KC - 1) / KC;
   const int r0 = min(b1, rank * Rm), R = min(b1, r0 + Rm) - r0;   // own rows [r0, r0 + R)
   // Y-stage 1 (NX^2 b2 terms) is computed by every CTA for all columns: cheaper
   // than a DSMEM exchange and its cluster barrier on every pass
-  const int c0 = 0, nc = b2;
-  (void)ncm;
   // shared-memory carve-up (see cluster_floats)
   float* UKt = csm;                   // [b2][NX]
   float* BK = UKt + NX * b2;
@@ -121,8 +119,8 @@ __device__ ClusterSolveOut cluster_solve(const SweepParams& p, const int b1, con
       for (int pass = 0; pass < 2; ++pass) {
         if (pass == 1 && !bad) break;
         const bool mp = first || pass == 1;
-        for (int o = tid; o < NX * nc; o += T) {
-          const int k1 = o / nc, l2 = c0 + (o - (o / nc) * nc);
+        for (int o = tid; o < NX * b2; o += T) {
+          const int k1 = o / b2, l2 = o - (o / b2) * b2;
           const float x = (float)l2 - fo2;
           const float wx = w2 * x;
           float z[NX];
