@@ -495,6 +495,21 @@ dd_status dd_multiscale_solve(const dd_problem* P, const dd_options* O, const dd
   // R24': eps' stages of every layer, eps' F, eps' F / 2, ..., eps' (F = eps_scale)
   std::vector<double> stages{eps_p * std::max(1.0, ms->eps_scale)};
   while (stages.back() > eps_p * (1 + 1e-12)) stages.push_back(std::max(eps_p, stages.back() / 2));
+  // Marginal-pool slot size of every layer from the FINAL eps' (R24'): the
+  // larger eps' of the first stages only widens boxes for a cycle or two,
+  // which the 2x initial-data term of the capacity covers; sizing from the
+  // first stage's eps' doubled the pools at 2048^2 (~50 GB) and made layer
+  // construction grow the memory pool.
+  dd_options Os = O ? *O : dd_options{};
+  if (!O) {
+    Os.err = 1e-4;
+    Os.max_iter = 2000;
+    Os.trunc = 1e-15;
+  }
+  if (Os.slot_cap <= 0) {
+    const int typ = 2 * s + 2 * (int)std::ceil(std::sqrt(eps_p * std::log(1e10))) + 12;
+    Os.slot_cap = typ * typ;
+  }
   dd_ms_stats S{};
   S.levels = L;
   dd_ctx* c = nullptr;
@@ -515,7 +530,7 @@ dd_status dd_multiscale_solve(const dd_problem* P, const dd_options* O, const dd
     Q.nu = nus[l].data();
     Q.init_off = nullptr; Q.init_ext = nullptr; Q.init_pos = nullptr; Q.init_data = nullptr;
     dd_ctx* next = nullptr;
-    dd_status r = l == 0 ? product_ctx(&Q, O, &next, err) : refine_ctx(c, &Q, O, &next, err);
+    dd_status r = l == 0 ? product_ctx(&Q, &Os, &next, err) : refine_ctx(c, &Q, &Os, &next, err);
     DevTimer tmd;
     if (c) domdec_destroy(c);
     tmd.mark("multiscale: destroy coarse");

@@ -18,7 +18,7 @@ for th in (20.0, 5.0):
     for rep in range(int(os.environ.get("REPS", "2"))):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        dd, st = multiscale_solve(p.mu, p.nu, 4, p.eps, p.E, levels=int(os.environ.get("LEVELS", "5")), conv=1e-4, max_cycles=3000, flow_every=1, max_iter=int(os.environ.get("MAX_ITER", "2000")), eps_scale=float(os.environ.get("EPS_SCALE", "1")))
+        dd, st = multiscale_solve(p.mu, p.nu, 4, p.eps, p.E, levels=int(os.environ.get("LEVELS", "5")), conv=1e-4, max_cycles=3000, flow_every=1, max_iter=int(os.environ.get("MAX_ITER", "2000")), eps_scale=float(os.environ.get("EPS_SCALE", "1")), eps_stage_cycles=int(os.environ.get("STAGE_CYCLES", "0")))
         torch.cuda.synchronize()
         sec = time.perf_counter() - t0
         ex, ey = dd.marginal_error()
