@@ -84,3 +84,36 @@ def test_cluster_class_tolerance_mode_hybrid():
     (ex_c, _), qc = out["cluster"]
     assert abs(qa - qc) < 1e-4 * abs(qa)
     assert ex_c < 3e-4 and ex_a < 3e-4
+
+
+@gpu
+@pytest.mark.parametrize("part", ["A", "B"])
+def test_stale_potentials_exercise_fallbacks(part):
+    """A warm start far from the solution (potentials perturbed by +-60 log2
+    units per pixel, imported with domdec_import_alpha): from the second pass
+    on, the shifts (the previous outputs) are far from the new values, so
+    shifted sums can leave [2^-60, 2^60] and take the max-shift fallback
+    (single-CTA and cluster paths alike).  The result after K passes matches
+    the oracle started from the same potentials."""
+    import os
+    from test_gpu_resume import _resume
+    p = CONFIGS["cfg2_gm"]()
+    K = 20
+    rng = np.random.default_rng(11)
+    base = gpu_ctx(p, fixed_iter=5)
+    base.sweep("A"); base.sweep("B")
+    alpha = base.export_alpha(part) + rng.uniform(-60.0, 60.0, (p.N, p.N)) * np.log(2.0)
+    st = oracle_state(p)
+    # the oracle from the same coupling (the generated one) and the same potentials
+    st.alpha[part] = alpha.copy()
+    O.domdec_sweep(st, part, fixed_iter=K)
+    rb, rt = rel_tols(p.eps_prime)
+    for name, env in (("single", VARIANTS["single"]), ("cluster8", VARIANTS["cluster8"])):
+        dd = _ctx_with(env, p, fixed_iter=K, comp_cap=8)
+        dd.import_alpha(part, alpha)
+        gst = dd.sweep(part, stats=True)
+        assert gst["overflow"] == 0 and np.isfinite(gst["l1x_final"]), (name, gst)
+        cmp = compare_states(dd.boxes(), st.boxes)
+        assert cmp["unexplained"] == 0 and cmp["rel_bulk"] < rb and cmp["rel_tail"] < rt, (name, cmp)
+        dd.close()
+    base.close()
