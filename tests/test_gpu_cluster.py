@@ -95,8 +95,6 @@ def test_stale_potentials_exercise_fallbacks(part):
     shifted sums can leave [2^-60, 2^60] and take the max-shift fallback
     (single-CTA and cluster paths alike).  The result after K passes matches
     the oracle started from the same potentials."""
-    import os
-    from test_gpu_resume import _resume
     p = CONFIGS["cfg2_gm"]()
     K = 20
     rng = np.random.default_rng(11)
