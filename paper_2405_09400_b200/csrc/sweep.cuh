@@ -38,6 +38,16 @@ __device__ __forceinline__ float lg2f(float x) {
   return y;
 }
 
+// max(m, |v|), NaN-propagating (the Y stages' out-of-range flag: a shifted
+// sum outside (2^-kLgRange, 2^kLgRange), an infinite or a NaN sum all give
+// !(m < kLgRange))
+__device__ __forceinline__ float fmax_nan_abs(float m, float v) {
+  float y;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(y) : "f"(m), "f"(fabsf(v)));
+  return y;
+}
+constexpr float kLgRange = 60.f;
+
 // 2^x - 1 with relative accuracy near 0 (X-error of a nearly converged cell).
 __device__ __forceinline__ float exp2m1f(float x) {
   if (fabsf(x) < 0.0625f) {
@@ -466,6 +476,10 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
   const float w2 = 2.f * w;
   const float fo1 = (float)o1, fo2 = (float)o2;
   constexpr int HX = NX / 2;
+  // per-term slopes of the Y stages: z_q = x * (2 w) k_q + input, k_q = 2q, 2q+1
+  float2 gq[HX];
+#pragma unroll
+  for (int q = 0; q < HX; ++q) gq[q] = make_float2(w2 * (float)(2 * q), w2 * (float)(2 * q + 1));
   auto single_loop = [&]() {
   if (b2 & 1)                         // padding column: a zero-weight term for X1's pairs
     for (int l1 = tid; l1 < b1; l1 += T) BK[l1 * b2p + b2] = kNeg;
@@ -487,18 +501,19 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
     // [2^-60, 2^60] only sets a flag, and a thread with a flagged output
     // recomputes all its outputs of the stage with a max shift (cold path).
     {
-      bool bad = false;
+      // out-of-range flag: max over the thread's outputs of |lg2 sum| (NaN
+      // propagating), tested once per pass: one FMNMX per output
+      float lgmax = 0.f;
       auto y1_out = [&](const int o, const int k1, const int l2, const bool maxpass) {
         const float x = (float)l2 - fo2;
-        const float wx = w2 * x;
         const float2* ar = reinterpret_cast<const float2*>(AL + k1 * NX);
         float2 a[HX];
 #pragma unroll
         for (int q = 0; q < HX; ++q) a[q] = ar[q];
-        const float2 wx2 = make_float2(wx, wx);
+        const float2 x2 = make_float2(x, x);
         float2 z[HX];
 #pragma unroll
-        for (int q = 0; q < HX; ++q) z[q] = __ffma2_rn(make_float2((float)(2 * q), (float)(2 * q + 1)), wx2, a[q]);
+        for (int q = 0; q < HX; ++q) z[q] = __ffma2_rn(x2, gq[q], a[q]);
         float s0;   // U = s0 + lg2(sum) - w x^2 ... with c = s0' + w x^2 (see below)
         float c;
         if (maxpass) {
@@ -519,15 +534,15 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
           const float2 t = __fadd2_rn(z[q], nc);
           acc = __fadd2_rn(acc, make_float2(ex2f(t.x), ex2f(t.y)));
         }
-        const float sum = acc.x + acc.y;
-        bad |= !(sum > 0x1p-60f && sum < 0x1p60f);
-        const float U = s0 + lg2f(sum);
+        const float lg = lg2f(acc.x + acc.y);
+        lgmax = fmax_nan_abs(lgmax, lg);
+        const float U = s0 + lg;
         Ub[o] = U;
         UK[o] = U - w * (float)(k1 * k1);
       };
       // pass 1 (cold, flagged threads only): the outputs again with a true
       // max shift; one call site keeps the stage's code compact (i-cache)
-      for (int pass = 0; pass < 2 && (pass == 0 || bad); ++pass) {
+      for (int pass = 0; pass < 2 && (pass == 0 || !(lgmax < kLgRange)); ++pass) {
         const bool mp = first || pass == 1;
         for (int o = tid, k1 = tid / b2, l2 = tid % b2; o < NX * b2;
              o += T, k1 += T / b2, l2 += T % b2, (l2 >= b2 ? (l2 -= b2, ++k1) : 0))
@@ -539,19 +554,19 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
     // thread's column inputs stay in registers as pairs; BK rows have the
     // even stride b2p (row b2p-1 of an odd b2 holds kNeg for X1's pairs).
     {
-      bool bad = false;
+      float lgmax = 0.f;   // out-of-range flag as in Y1
       auto y2_column = [&](const int l2, const int l1_0, const int l1_step, const bool maxpass) {
         float2 u[HX];
 #pragma unroll
         for (int q = 0; q < HX; ++q) u[q] = make_float2(UK[(2 * q) * b2 + l2], UK[(2 * q + 1) * b2 + l2]);
-        for (int l1 = l1_0; l1 < b1; l1 += l1_step) {
+        float x = (float)l1_0 - fo1;
+        const float xstep = (float)l1_step;
+        for (int l1 = l1_0; l1 < b1; l1 += l1_step, x += xstep) {
           const int o = l1 * b2 + l2;
-          const float x = (float)l1 - fo1;
-          const float wx = w2 * x;
-          const float2 wx2 = make_float2(wx, wx);
+          const float2 x2 = make_float2(x, x);
           float2 z[HX];
 #pragma unroll
-          for (int q = 0; q < HX; ++q) z[q] = __ffma2_rn(make_float2((float)(2 * q), (float)(2 * q + 1)), wx2, u[q]);
+          for (int q = 0; q < HX; ++q) z[q] = __ffma2_rn(x2, gq[q], u[q]);
           float s0, c;
           if (maxpass) {
             c = kNeg;
@@ -573,9 +588,9 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
             const float2 t = __fadd2_rn(z[q], nc);
             acc = __fadd2_rn(acc, make_float2(ex2f(t.x), ex2f(t.y)));
           }
-          const float sum = acc.x + acc.y;
-          bad |= !(sum > 0x1p-60f && sum < 0x1p60f);
-          const float Bv = -(s0 + lg2f(sum));
+          const float lg = lg2f(acc.x + acc.y);
+          lgmax = fmax_nan_abs(lgmax, lg);
+          const float Bv = -s0 - lg;
           P0[o] = Bv;
           BK[l1 * b2p + l2] = Bv + P1[o];   // P1 = log2 nu_J - w lc2^2
         }
@@ -585,7 +600,7 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
       const int c0 = b2 <= T ? y2_col : tid, cstep = b2 <= T ? b2 : T;
       const int r0 = b2 <= T ? y2_rg : 0, rstep = b2 <= T ? RG : 1;
       if (b2 > T || y2_rg < RG)
-        for (int pass = 0; pass < 2 && (pass == 0 || bad); ++pass)
+        for (int pass = 0; pass < 2 && (pass == 0 || !(lgmax < kLgRange)); ++pass)
           for (int l2 = c0; l2 < b2; l2 += cstep) y2_column(l2, r0, rstep, first || pass == 1);
     }
     __syncthreads();

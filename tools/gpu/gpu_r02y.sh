@@ -1,9 +1,11 @@
 #!/bin/bash
-cd "$GRAFT_REPO_ROOT" || exit 1
+# Y-stage instruction trim: A/B of the pure sweep (old build vs new), then the sweep parity tests
 mkdir -p gpurun_out
-for c in 0 8; do
-  echo "cluster=$c" >> gpurun_out/r02y_layers.jsonl
-  DD_H_CLUSTER=$c timeout 600 python tests/diag/ms_layer_probe.py >> gpurun_out/r02y_layers.jsonl 2>> gpurun_out/r02y.err
+for lib in new old new old; do
+  if [ $lib = old ]; then export DD_LIB_PATH=$PWD/abtmp/old.so; else unset DD_LIB_PATH; fi
+  timeout 300 python tools/sweep_frac_probe.py >> gpurun_out/r02y_ab.jsonl 2>&1
 done
-DD_H_CLUSTER=8 DD_H_CLUSTER_KB=64 timeout 600 python tools/ms_sweep_probe.py >> gpurun_out/r02y_probe.jsonl 2>> gpurun_out/r02y.err
-echo done
+unset DD_LIB_PATH
+timeout 1500 python -m pytest -x -q -m gpu tests/test_gpu_parity.py tests/test_gpu_cell_sizes.py tests/test_gpu_cluster.py tests/test_gpu_rectangular.py > gpurun_out/r02y_pytest.txt 2>&1; echo "rc=$?" >> gpurun_out/r02y_pytest.txt
+tail -3 gpurun_out/r02y_pytest.txt
+cat gpurun_out/r02y_ab.jsonl
