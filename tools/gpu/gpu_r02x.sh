@@ -1,8 +1,11 @@
 #!/bin/bash
-cd "$GRAFT_REPO_ROOT" || exit 1
+# X1 lane split: A/B of the pure sweep (previous build y.so vs new), then the sweep parity tests
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_cluster.py tests/test_gpu_parity.py -k "cluster or hull_wider or size_classes" -q -x > gpurun_out/r02x_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/r02x_pytest.log
-for c in 0 8; do
-  DD_H_CLUSTER=$c timeout 600 python tools/ms_sweep_probe.py >> gpurun_out/r02x_probe.jsonl 2>> gpurun_out/r02x_probe.err
+for lib in new y new y; do
+  if [ $lib = y ]; then export DD_LIB_PATH=$PWD/abtmp/y.so; else unset DD_LIB_PATH; fi
+  timeout 300 python tools/sweep_frac_probe.py >> gpurun_out/r02x_ab.jsonl 2>&1
 done
-echo done
+unset DD_LIB_PATH
+timeout 1500 python -m pytest -x -q -m gpu tests/test_gpu_parity.py tests/test_gpu_cell_sizes.py tests/test_gpu_cluster.py tests/test_gpu_rectangular.py > gpurun_out/r02x_pytest.txt 2>&1; echo "rc=$?" >> gpurun_out/r02x_pytest.txt
+tail -3 gpurun_out/r02x_pytest.txt
+cat gpurun_out/r02x_ab.jsonl
