@@ -21,7 +21,8 @@ void set_global_error(const std::string& m) { g_last_error = m; }
 // contexts of several GB.  The library allocates device memory from the device's stream-ordered pool
 // only (cudaMallocAsync).  The pool keeps what it has mapped (release
 // threshold = max) and is pre-grown once per process (DD_POOL_RESERVE_GB,
-// default min(48 GB, free / 3)): growing a pool maps physical memory, and
+// default min(80 GB, free / 2): the 2048^2 multiscale solve peaks at
+// ~67 GB): growing a pool maps physical memory, and
 // growth in the middle of a multiscale solve cost 0.1-1 s per layer
 // (profiles/r02_pool_timers.txt).
 namespace dd {
@@ -37,10 +38,10 @@ void keep_device_pool(int dev) {
   int cur = 0;
   cudaGetDevice(&cur);
   if (cur != dev) cudaSetDevice(dev);
-  double gb = 48.0;
+  double gb = 80.0;
   if (const char* env = getenv("DD_POOL_RESERVE_GB")) gb = atof(env);
   if (gb > 0 && cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
-    size_t want = std::min((size_t)(gb * (1ull << 30)), fr / 3);
+    size_t want = std::min((size_t)(gb * (1ull << 30)), fr / 2);
     void* p = nullptr;
     if (want > 0 && cudaMallocAsync(&p, want, 0) == cudaSuccess) {
       cudaFreeAsync(p, 0);
