@@ -684,8 +684,8 @@ def extra_configs(stream, local, mp):
         dd5.close()
     out["cfg5_2048_s2"]["ttc_multiscale"] = {"seconds": float(np.median(times[1:])) if all(st["converged"]) else None,
                                              "cold_seconds": times[0], "solve_seconds": times[1:], "levels": st,
-                                             "note": "layer-context construction at 2048^2 varies by 0.1-3 s "
-                                                     "between solves (pool allocation), hence the median",
+                                             "note": "median of solves 2-4; the solve peaks at ~67 GB of device "
+                                                     "memory (the library's pool is pre-grown to min(80 GB, free/2))",
                                              "workload": f"GM(0)+T_20 2048^2 s=2 eps=(2h)^2, {L5} layers from "
                                                          f"{2048 >> (L5 - 1)}^2, flow update every cycle, eps-scaling x4 per layer (R24')"}
     return out
