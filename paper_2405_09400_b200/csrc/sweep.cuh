@@ -705,13 +705,18 @@ __device__ __forceinline__ void sweep_cell(const SweepParams& p, const int J, co
         cb = __fadd_rn(-A2[qb * NX + k2], Kb);
       }
       float sa = 0.f, sb = 0.f;
-      if (x2_valid) {
+      if (x2_valid) {   // the two outputs as a pair (FFMA2 / FADD2)
+        const float2 g2 = make_float2(ga, gb), nc2 = make_float2(-ca, -cb);
+        float2 s2 = make_float2(0.f, 0.f);
         float lf = (float)x2_h - fo1;
+#pragma unroll 4
         for (int l1 = x2_h; l1 < b1; l1 += SX, lf += (float)SX) {
           const float vk = VK[l1 * NX + k2];
-          sa += ex2f(fmaf(ga, lf, vk) - ca);
-          sb += ex2f(fmaf(gb, lf, vk) - cb);
+          const float2 z = __fadd2_rn(__ffma2_rn(make_float2(lf, lf), g2, make_float2(vk, vk)), nc2);
+          s2 = __fadd2_rn(s2, make_float2(ex2f(z.x), ex2f(z.y)));
         }
+        sa = s2.x;
+        sb = s2.y;
       }
 #pragma unroll
       for (int off = SX >> 1; off > 0; off >>= 1) {
