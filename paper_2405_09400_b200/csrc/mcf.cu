@@ -134,7 +134,14 @@ __device__ __forceinline__ long long floor_div(long long a, long long b) {   // 
 //     every node) along residual arcs v -> u with l = c_p + epsT;
 //   mode 2 (certificate): one node per cell, d(j) over the 4-neighbour arcs
 //     i -> j with the integer costs C (no negative cycle <=> converges).
-constexpr int TH = 16, TW = 32, TP = TW + 2, kSweeps = 16;   // (sweeps per grid round: tuned on the bench trajectory, tools/mcf_knobs.py)
+// tile height: 8 x 32 cells per CTA (at 1024^2: 256 tiles, 128 working per
+// checkerboard phase on 148 SMs) — 4.5% faster warm solves than 16 x 32
+// (128 tiles, 64 working per phase) and 16% faster than 4 x 32 on the bench
+// trajectory (profiles/r02_mcf_experiments.txt)
+#ifndef DD_MCF_TH
+#define DD_MCF_TH 8
+#endif
+constexpr int TH = DD_MCF_TH, TW = 32, TP = TW + 2, kSweeps = 16;   // (sweeps per grid round: tuned on the bench trajectory, tools/mcf_knobs.py)
 
 __device__ __noinline__ bool tiled_bf(const McfArgs& A, cg::grid_group& grid, const int mode, const int par, const long long eps,
                          const int cap, long long gt, long long gs, int* rounds_used) {
@@ -965,15 +972,16 @@ dd_status mcf_solve_device(int n1, int n2, const int64_t* d_q, const int64_t* d_
   cudaGetDevice(&dev);
   int nsm = 0, per = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  // one CTA per SM at most: grid barriers get cheaper with fewer CTAs
-  const int threads = 512;
+  // one CTA per tile (TH x TW cells, one thread per cell), at most the
+  // co-resident CTAs of the device
+  const int threads = TH * TW;
   // per-device function attribute: set on every launch (cheap)
   e = cudaFuncSetAttribute(mcf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmemBytes);
   if (e != cudaSuccess) { err = std::string("mcf smem: ") + cudaGetErrorString(e); return DD_ERR_CUDA; }
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mcf_kernel, threads, kTileSmemBytes);
   if (per <= 0) { err = "mcf kernel cannot be resident"; return DD_ERR_CUDA; }
   long long want = (I + threads - 1) / threads;
-  long long blocks = (long long)nsm;
+  long long blocks = (long long)nsm * (TH < 16 ? per : 1);
   if (want < blocks) blocks = want;
   if (blocks < 1) blocks = 1;
   void* args[] = {&A};
