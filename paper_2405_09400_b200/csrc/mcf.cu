@@ -954,7 +954,7 @@ dd_status mcf_solve_device(int n1, int n2, const int64_t* d_q, const int64_t* d_
   A.gu_every = 50;
   A.tiled = 1;
   A.tile_rounds = 16;
-  A.gu_tiled = 12;   // tile phases between global price updates (8 x 32 tiles; profiles/r02_mcf_experiments.txt)
+  A.gu_tiled = 8;    // tile phases between global price updates (profiles/r02_mcf_experiments.txt)
   A.alpha = 16;
   A.bf_sweeps = kSweeps;
   A.pr_cap = 0;
